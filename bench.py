@@ -1,0 +1,300 @@
+#!/usr/bin/env python
+"""Benchmark of the BQNPM hot path on B200 (driver contract: ONE JSON line on rank 0).
+
+Headline workload = BASELINE.json configs[1] (config 2): the weighted-TV prox
+microbench, 128^3 fp32, W = diag(d) + u u^T, isotropic TV reg 0.05, box
+[0, inf), exactly 100 FGP iterations (eps = 1e-300), P0 = 0, beta0 = 0.
+A "step" is one full prox solve (one persistent-kernel launch).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 128]
+
+--impl reference times the CPU restatement of the reference algorithm
+(oracle/prox.py, the reference package itself cannot travel to the GPU box)
+on a bounded sample of the same workload; under torchrun only rank 0 runs it.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "wTV-prox voxel-iters/s"
+UNIT = "voxel*iter/s"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+FALLBACK_HBM_GBS = 6650.0
+
+
+def hbm_peak():
+    try:
+        return float(json.loads(PEAKS.read_text())["hbm_gbs"]), "measured"
+    except Exception:
+        return FALLBACK_HBM_GBS, "fallback"
+
+
+def bytes_per_voxel_iter(word: int, rank: int, per_voxel_d: bool) -> int:
+    """B_wtv = s * (13 + r + delta_d): read P_bar, P, write P, P_bar
+    (3 each), read v, U (r), d (per-voxel)."""
+    return word * (13 + rank + (1 if per_voxel_d else 0))
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                for line in out.stdout.strip().splitlines():
+                    self.rows.append([c.strip() for c in line.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and "Active" in r[2 + i]
+                          and "Not" not in r[2 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ---------------------------------------------------------------------------
+# reference arm: CPU restatement on the host cores
+# ---------------------------------------------------------------------------
+def cpu_prox_sample(inp, iters: int):
+    from oracle import prox as O
+
+    n = inp["n"]
+    w = O.Metric(U=inp["u"][:, None], d=inp["d"])
+    t0 = time.perf_counter()
+    O.fgp_prox((n, n, n), inp["v"], w, reg=inp["reg"], eps=1e-300, max_iter=iters)
+    dt = time.perf_counter() - t0
+    return n ** 3 * iters / dt, dt
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    from paper_2307_02043_b200.configs import config2_inputs
+
+    inp = config2_inputs(args.n)
+    vals = []
+    sample_iters = args.cpu_iters
+    for _ in range(args.warmup):
+        cpu_prox_sample(inp, 1)
+    t_all = time.perf_counter()
+    for _ in range(args.steps):
+        v, _ = cpu_prox_sample(inp, sample_iters)
+        vals.append(v)
+    wall = time.perf_counter() - t_all
+    value = float(np.median(vals))
+    sample = f"config-2 prox {args.n}^3 f64 diag(d)+uu^T, {sample_iters} FGP iterations per step (numpy port)"
+    line = {
+        "impl": "reference",
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 phantom)",
+        "config": {"workload": f"config2 wTV prox {args.n}^3 diag(d)+uu^T iso reg 0.05 box [0,inf)",
+                   "sample_iters_per_step": sample_iters},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if ws > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    import paper_2307_02043_b200 as bq
+    from paper_2307_02043_b200 import dual_tv_solver as D
+    from paper_2307_02043_b200.configs import config2_inputs
+    from paper_2307_02043_b200.wpm import BoxSet, DiagPlusLowRank
+
+    n = args.n
+    N = n ** 3
+    dtype = torch.float32
+    inp = config2_inputs(n)
+    grid = bq.Grid((n, n, n))
+    v_h = torch.from_numpy(inp["v"].astype(np.float32)).pin_memory()
+    d_h = torch.from_numpy(inp["d"].astype(np.float32)).pin_memory()
+    u_h = torch.from_numpy(inp["u"].astype(np.float32)).pin_memory()
+    v = v_h.to(dev)
+    d = d_h.to(dev)
+    u = u_h.to(dev)
+    w = DiagPlusLowRank(1.0, u[:, None], d=d)
+    prob = D.DualTvProblem(grid=grid, v=v, w=w, reg=inp["reg"], box=BoxSet(0.0, np.inf))
+    wsp = D.ProxWorkspace(grid, dtype, dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # 256 MB > L2
+    iters = inp["iters"]
+
+    def step():
+        D.solve_async(prob, wsp, eps=1e-300, max_iter=iters)
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    rep = D.read_report(wsp)
+    assert rep.iterations == iters, rep.iterations
+
+    stream = torch.cuda.current_stream(dev)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    sampler = ClockSampler(local)
+    if ws > 1:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    with sampler:
+        t_wall = time.perf_counter()
+        for i in range(args.steps):
+            flush.fill_(float(i))  # evict L2 between timed steps (not inside the event pair)
+            starts[i].record(stream)
+            step()
+            ends[i].record(stream)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - t_wall
+    if ws > 1:
+        dist.barrier()
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    ms = float(np.mean(step_ms))
+    if ws > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    value = ws * N * iters / (ms * 1e-3)
+
+    # ---- e2e: host buffers through the public API, copies inside the timed region
+    e2e_ms = []
+    out_h = torch.empty(N, dtype=dtype).pin_memory()
+    for i in range(args.steps + 1):
+        torch.cuda.synchronize(dev)
+        t0 = time.perf_counter()
+        vv = v_h.to(dev, non_blocking=True)
+        dd = d_h.to(dev, non_blocking=True)
+        uu = u_h.to(dev, non_blocking=True)
+        ww = DiagPlusLowRank(1.0, uu[:, None], d=dd)
+        pp = D.DualTvProblem(grid=grid, v=vv, w=ww, reg=inp["reg"], box=BoxSet(0.0, np.inf))
+        D.solve_async(pp, wsp, eps=1e-300, max_iter=iters)
+        out_h.copy_(wsp.x, non_blocking=True)
+        torch.cuda.synchronize(dev)
+        if i > 0:
+            e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e = float(np.mean(e2e_ms))
+    if ws > 1:
+        t = torch.tensor([e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e = float(t.item())
+
+    if rank == 0:
+        peak, peak_kind = hbm_peak()
+        bpv = bytes_per_voxel_iter(4, 1, True)
+        achieved = bpv * N * iters / (ms * 1e-3) / 1e9
+        traffic = None
+        summ = ROOT / "profiles" / "ncu_summary.json"
+        if summ.exists():
+            try:
+                traffic = json.loads(summ.read_text()).get("wtv_prox_kernel", {}).get("dram_bytes_per_launch")
+            except Exception:
+                traffic = None
+        cpu = None
+        if ws == 1 and not args.no_cpu:
+            inp64 = inp
+            cv, cdt = cpu_prox_sample(inp64, args.cpu_iters)
+            cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port",
+                   "sample": f"config-2 prox {n}^3 f64 diag(d)+uu^T, {args.cpu_iters} FGP iterations "
+                             f"(numpy port, {cdt:.1f} s)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded config-2 box phantom + N(0,1) noise)",
+            "config": {"workload": f"config2 wTV prox {n}^3 W=diag(d)+uu^T iso TV reg 0.05 box [0,inf), "
+                                   f"{iters} FGP iterations per step",
+                       "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{ws}"},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "peak_source": peak_kind, "algorithmic_bytes_per_voxel_iter": bpv},
+            "cpu_baseline": cpu,
+            "e2e": {"value": ws * N * iters / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
+                    "h2d_bytes_per_step": 3 * N * 4, "d2h_bytes_per_step": N * 4},
+            "gpu_launches": args.steps,
+            "clocks": sampler.summary(),
+            "wall_s_timed_region": wall,
+            "step_ms": step_ms,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=128)
+    ap.add_argument("--cpu-iters", type=int, default=8)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

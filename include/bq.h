@@ -1,0 +1,164 @@
+/*
+ * bq.h — C ABI of the B200-native BQNPM hot path (libbq.so).
+ *
+ * Plain C: no torch, numpy or C++ types cross this boundary.  Every device
+ * buffer is owned by the caller (a torch tensor on the Python side) and is
+ * passed as a raw device pointer plus sizes; streams are passed as the raw
+ * cudaStream_t value (void*).  Every entry point returns an int status:
+ * 0 = ok, <0 = error (BQ_E*), with the text available from bq_last_error()
+ * (thread-local).  Nothing throws or exits across the ABI.  All calls are
+ * stream-ordered and asynchronous unless stated otherwise.
+ *
+ * Reference interfaces replaced (paths under /root/reference/pkg/src/tvqn/):
+ *   bq_wtv_prox          dual_tv_solver.py:161-250  solve(prob, eps, max_iter, accelerated)
+ *                        (with w_of_p :119-123, _prox_of :126-135, dual_step_size :155-158,
+ *                         tv_ops.py:107-180 stencils/projection, wpm.py:145-253 wpm_box)
+ *   bq_wpm_box           wpm.py:234-253             wpm_box(x, w, box, beta0, eps, max_iter)
+ *   bq_metric_gram       wpm.py:50-56               DiagPlusLowRank.__post_init__ (I +/- U^T U / tau)
+ *   bq_metric_apply      wpm.py:81-89               apply_metric(w, x)
+ *   bq_metric_inverse    wpm.py:92-106              apply_metric_inverse(w, x)
+ *   bq_sr1               hessian_sr1.py:52-101      estimate_sr1(s, m, gamma, alpha_fallback)
+ *   bq_vk                solvers.py:80-89           compute_v_k(slots, w, step)
+ *   bq_dot               (reduction helper used by the host mirrors; fixed-order, deterministic)
+ *   bq_tv_value          tv_ops.py:162-167          tv_value(grid, x, mode)
+ *   bq_dct_views         forward_models.py:86-91,139-150,166-183 DCT stand-in view batch
+ *   bq_born_views        (absent in reference; north star (1)) first-Born view batch
+ *   bq_ls_*              (absent in reference; north star (1)(2)) Lippmann-Schwinger views
+ */
+#ifndef BQ_H_
+#define BQ_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+#if defined(__GNUC__)
+#pragma GCC visibility push(default)
+#endif
+
+#define BQ_OK 0
+#define BQ_EINVAL -1      /* invalid argument (maps to ValueError) */
+#define BQ_ECUDA -2       /* CUDA runtime / cuFFT failure (RuntimeError) */
+#define BQ_ENOTPD -3      /* metric not positive definite (ValueError) */
+#define BQ_ETIMEOUT -4    /* device-side grid barrier timed out (RuntimeError) */
+#define BQ_ENOMEM -5
+
+#define BQ_F32 0
+#define BQ_F64 1
+
+#define BQ_TV_ISO 0
+#define BQ_TV_ANISO 1
+
+#define BQ_MAX_RANK 8
+
+typedef struct bq_ctx bq_ctx;
+
+/* Context: one per (device, host thread).  Holds the grid-barrier/control
+ * workspace of the persistent kernels and the cuFFT plan cache. */
+int bq_ctx_create(int device, bq_ctx** out);
+int bq_ctx_destroy(bq_ctx* ctx);
+const char* bq_last_error(void);
+/* Version / capability string ("bq 0.1 sm_100a"). */
+const char* bq_version(void);
+
+/* ---------------------------------------------------------------------------
+ * Weighted constrained TV prox (FGP dual iteration + structured WPM Newton).
+ *   x* = argmin_{lo<=x<=hi} 1/2 ||x - v||_W^2 + reg TV(x),
+ *   W = diag(d) + sign U U^T  (d == NULL: d == tau, the reference's tau*I)
+ * Layout: flat Fortran order over dims (dims[0] fastest) == C-order (K3,K2,K1).
+ * U: rank contiguous N-vectors (column c at U + c*N).  P: ndim contiguous
+ * N-vectors.  beta: rank doubles (device).  One persistent cooperative
+ * kernel runs the whole solve; every decision is taken on the device.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t ndim;          /* 1..3 (the reference Grid.ndim; drives the step) */
+  int32_t dtype;         /* BQ_F32 / BQ_F64 for every field */
+  int64_t dims[3];       /* K1, K2, K3 (unused dims = 1) */
+  int32_t mode;          /* BQ_TV_ISO / BQ_TV_ANISO */
+  int32_t rank;          /* r = columns of U, 0..BQ_MAX_RANK */
+  int32_t sign;          /* +1 / -1 */
+  int32_t accelerated;   /* FISTA momentum on/off */
+  double tau;            /* scalar diagonal (used when d == NULL) */
+  double reg;            /* TV weight (>= 0) */
+  double step;           /* dual step 1/(4 ndim omega reg); ignored when reg == 0 */
+  double eps;            /* FGP relative-change tolerance */
+  int32_t max_iter;      /* FGP cap */
+  int32_t newton_max_iter;
+  double newton_eps;
+  double lo, hi;         /* scalar box (may be +/-inf) */
+  const void* lo_arr;    /* optional per-voxel bounds (NULL -> scalar) */
+  const void* hi_arr;
+  const void* d;         /* optional per-voxel diagonal (NULL -> tau) */
+  const void* U;         /* rank x N */
+  const void* v;         /* N   center */
+  void* p;               /* ndim x N  in: warm start (zeros if none); out: P* */
+  void* pb;              /* ndim x N  scratch (momentum field) */
+  void* a;               /* N   scratch */
+  void* x;               /* N   out: the prox */
+  double* beta;          /* rank doubles in (warm) / out (beta*) ; may be NULL if rank==0 */
+  void* report;          /* device bq_wtv_report (out) */
+} bq_wtv_desc;
+
+typedef struct {
+  int32_t iterations;
+  int32_t converged;
+  int32_t newton_iterations;
+  int32_t status;        /* 0 ok, BQ_ENOTPD, BQ_ETIMEOUT */
+  double rel_change;
+  double newton_residual; /* residual of the last wpm_box call */
+  int32_t last_newton_iterations;
+  int32_t last_newton_converged;
+} bq_wtv_report;
+
+int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream);
+
+/* Structured weighted box projection (wpm_box) alone: x_out = clamp(x - sign D^-1 U beta*).
+ * Uses the same device Newton as the prox; report as above (iterations = 1). */
+int bq_wpm_box(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign, double tau,
+               const void* d, const void* U, const void* x, double lo, double hi,
+               const void* lo_arr, const void* hi_arr, double* beta_inout, double newton_eps,
+               int32_t newton_max_iter, void* x_out, void* a_scratch, void* report, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Metric algebra (W = diag(d) + sign U U^T), deterministic fixed-order reductions.
+ * ------------------------------------------------------------------------ */
+/* gram_out (device, rank*rank doubles, row-major) = U^T D^-1 U  (D = tau I when d == NULL). */
+int bq_metric_gram(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, double tau, const void* d,
+                   const void* U, double* gram_out, void* stream);
+/* out = W x  (or W^-1 x via Woodbury when inverse != 0).  For the inverse,
+ * gram (device, rank*rank doubles) is bq_metric_gram's U^T D^-1 U; the
+ * capacitance I + sign gram(/tau) is factorised on the device. */
+int bq_metric_apply(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign, double tau,
+                    const void* d, const void* U, const double* gram, int32_t inverse,
+                    const void* x, void* out, void* stream);
+
+/* dots_out[k] = <a_k, b_k> for k < count (device doubles). */
+int bq_dot(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const void* const* a_ptrs,
+           const void* const* b_ptrs, double* dots_out, void* stream);
+
+/* SR1 estimate B = tau I + u u^T from (s, m) (hessian_sr1.py:52-101).
+ * Writes u (N; zeros when rejected) and est_out (device, 9 doubles):
+ * {tau, has_u, <s,m>, curv, <m,m>, nnz(s), ||s||, ||m - tau s||, status}. */
+int bq_sr1(bq_ctx* ctx, int32_t dtype, int64_t n, const void* s, const void* m, double gamma,
+           double alpha_fallback, void* u_out, double* est_out, void* stream);
+
+/* v = W^-1 sum_t (tau_t x_t + u_t (u_t^T x_t) - step g_t)   (solvers.py:80-89).
+ * slots: count (<= 8) triples; u_t may be NULL (rank-0 slot); taus is a host
+ * array.  W = tau_w I + sign U_w U_w^T with gram_w = U_w^T U_w (device). */
+int bq_vk(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const void* const* xs,
+          const void* const* gs, const void* const* us, const double* taus, double step,
+          int32_t rank, int32_t sign, double tau_w, const void* U_w, const double* gram_w,
+          void* acc_scratch, void* v_out, void* stream);
+
+/* TV value (tv_ops.py:162-167) -> out (device double). */
+int bq_tv_value(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64_t* dims, int32_t mode,
+                const void* x, double* out, void* stream);
+
+#if defined(__GNUC__)
+#pragma GCC visibility pop
+#endif
+#ifdef __cplusplus
+}
+#endif
+#endif /* BQ_H_ */

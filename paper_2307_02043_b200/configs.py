@@ -1,0 +1,42 @@
+"""Seeded synthetic inputs for the BASELINE.json configurations.
+
+Seeds follow SURVEY 8d: ``numpy.random.default_rng(1000*c + k)`` for config c,
+k = 0 phantom, 1 noise, 2 metric (d, u), 3 prox-volume noise.  No public
+dataset is involved; these seeded phantoms stand in for the paper's data.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+
+def _rng(config: int, k: int):
+    return np.random.default_rng(1000 * config + k)
+
+
+def box_phantom(n: int, n_boxes: int = 16, rng=None) -> np.ndarray:
+    """Piecewise-constant volume of axis-aligned random boxes, later boxes
+    overwrite earlier ones; returned flat in Fortran order over (n, n, n)."""
+    rng = rng or _rng(2, 0)
+    vol = np.zeros((n, n, n))  # C-order (K3, K2, K1) == flat Fortran over dims
+    for _ in range(n_boxes):
+        side = rng.uniform(n / 16, n / 4, size=3)
+        corner = rng.uniform(0, n, size=3)
+        val = rng.uniform(0.0, 1.0)
+        lo = np.floor(corner).astype(int)
+        hi = np.minimum(n, np.floor(corner + side).astype(int) + 1)
+        vol[lo[2]:hi[2], lo[1]:hi[1], lo[0]:hi[0]] = val
+    return vol.reshape(-1)
+
+
+def config2_inputs(n: int = 128):
+    """Config 2 (weighted-TV prox microbench): v = box phantom + N(0,1) noise,
+    W = diag(d) + u u^T with d ~ U[0.5, 2], u ~ N(0,1)/sqrt(N); scalar-tau twin d == 1.25."""
+    N = n ** 3
+    phantom = box_phantom(n, rng=_rng(2, 0))
+    v = phantom + _rng(2, 3).standard_normal(N)
+    rm = _rng(2, 2)
+    d = rm.uniform(0.5, 2.0, N)
+    u = rm.standard_normal(N) / np.sqrt(N)
+    return {"n": n, "v": v, "d": d, "u": u, "phantom": phantom, "reg": 0.05, "lo": 0.0, "hi": np.inf,
+            "iters": 100, "tau_twin": 1.25}

@@ -1,0 +1,81 @@
+// ctx.cu — context lifetime, thread-local error text, version string.
+#include <stdarg.h>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace bq {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  set_error("CUDA error %s (%s) at %s", cudaGetErrorName(e), cudaGetErrorString(e), where);
+  return BQ_ECUDA;
+}
+
+void fft_cache_destroy(void* cache);  // views code
+
+}  // namespace bq
+
+extern "C" const char* bq_last_error(void) { return bq::g_err; }
+
+extern "C" const char* bq_version(void) { return "bq 0.1 sm_100a"; }
+
+extern "C" int bq_ctx_create(int device, bq_ctx** out) {
+  using namespace bq;
+  BQ_CHECK(out, BQ_EINVAL, "bq_ctx_create: null out");
+  *out = nullptr;
+  int ndev = 0;
+  BQ_CUDA(cudaGetDeviceCount(&ndev));
+  BQ_CHECK(device >= 0 && device < ndev, BQ_EINVAL, "device %d out of range (%d devices)", device, ndev);
+  BQ_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop;
+  BQ_CUDA(cudaGetDeviceProperties(&prop, device));
+  BQ_CHECK(prop.major == 10 && prop.minor == 0, BQ_EINVAL,
+           "libbq is built for sm_100a (B200); device %d is sm_%d%d", device, prop.major, prop.minor);
+  int coop = 0;
+  BQ_CUDA(cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, device));
+  BQ_CHECK(coop, BQ_ECUDA, "device %d does not support cooperative launch", device);
+  bq_ctx* c = new bq_ctx();
+  c->device = device;
+  c->num_sms = prop.multiProcessorCount;
+  c->ws.ctl_bytes = 4096;
+  cudaError_t e;
+  if ((e = cudaMalloc(&c->ws.partials, sizeof(double) * kMaxBlocks * kMaxVals)) != cudaSuccess ||
+      (e = cudaMalloc(&c->ws.barrier, 64)) != cudaSuccess ||
+      (e = cudaMalloc(&c->ws.ctl, c->ws.ctl_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&c->ws.scratch, sizeof(double) * 4096)) != cudaSuccess ||
+      (e = cudaMemset(c->ws.barrier, 0, 64)) != cudaSuccess ||
+      (e = cudaMemset(c->ws.ctl, 0, c->ws.ctl_bytes)) != cudaSuccess) {
+    cudaFree(c->ws.partials);
+    cudaFree(c->ws.barrier);
+    cudaFree(c->ws.ctl);
+    cudaFree(c->ws.scratch);
+    delete c;
+    return cuda_fail(e, "bq_ctx_create workspace");
+  }
+  *out = c;
+  return BQ_OK;
+}
+
+extern "C" int bq_ctx_destroy(bq_ctx* c) {
+  using namespace bq;
+  if (!c) return BQ_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  fft_cache_destroy(c->fft_cache);
+  cudaFree(c->ws.partials);
+  cudaFree(c->ws.barrier);
+  cudaFree(c->ws.ctl);
+  cudaFree(c->ws.scratch);
+  delete c;
+  return BQ_OK;
+}

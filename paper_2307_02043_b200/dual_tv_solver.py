@@ -1,0 +1,189 @@
+"""Weighted constrained TV prox on the device — drop-in for ``tvqn.dual_tv_solver``.
+
+Reference: ``/root/reference/pkg/src/tvqn/dual_tv_solver.py``
+  * ``DualTvProblem`` (:25-79): same fields, defaults and validation; omega
+    defaults to 1/tau (scalar metric) or 1/min(d) (per-voxel diagonal, D-6).
+  * ``DualSolveReport`` (:82-92): same fields.
+  * ``dual_step_size`` (:155-158): 1 / (4 ndim omega reg).
+  * ``solve(prob, eps=1e-5, max_iter=100, accelerated=True)`` (:161-250):
+    ONE ``bq_wtv_prox`` launch (persistent cooperative kernel running the FGP
+    loop, the Woodbury shift, the semi-smooth Newton, the projection and the
+    momentum, with every stop/accept decision on the device).
+
+numpy inputs give numpy outputs (float64 compute); torch CUDA inputs give
+torch outputs in their dtype (float32 or float64).  ``solve_async`` is the
+GPU-resident variant that leaves the report on the device.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._tensors import is_torch, out_like, to_dev
+from .tv_ops import Grid, TvMode
+from .wpm import BoxSet, DiagPlusLowRank
+
+
+@dataclass
+class DualTvProblem:
+    grid: Grid
+    v: object
+    w: DiagPlusLowRank
+    reg: float
+    mode: TvMode = TvMode.ISOTROPIC
+    box: BoxSet = field(default_factory=BoxSet)
+    omega: float = None
+    warm_start: object = None
+    beta_warm: object = None
+    newton_eps: float = 1e-6
+    newton_max_iter: int = 50
+
+    def __post_init__(self):
+        if self.reg < 0:
+            raise ValueError("reg must be nonnegative")
+        if self.omega is None:
+            self.omega = 1.0 / self.w.min_diag()
+        if not self.omega > 0:
+            raise ValueError("omega must be positive")
+        if self.beta_warm is not None and not is_torch(self.beta_warm):
+            self.beta_warm = np.asarray(self.beta_warm, dtype=float)
+        self.mode = TvMode.parse(self.mode)
+
+
+@dataclass
+class DualSolveReport:
+    x: object
+    p_star: object
+    iterations: int
+    rel_change: float
+    converged: bool
+    newton_iterations: int = 0
+    beta_star: object = None
+
+
+def dual_step_size(prob: DualTvProblem) -> float:
+    return 1.0 / (4.0 * prob.grid.ndim * prob.omega * prob.reg)
+
+
+class ProxWorkspace:
+    """Reusable device buffers for repeated solves on one grid (no allocation per call)."""
+
+    def __init__(self, grid: Grid, dtype, device):
+        n, d = grid.size, grid.ndim
+        self.grid, self.dtype, self.device = grid, dtype, device
+        self.p = torch.zeros(d, n, dtype=dtype, device=device)
+        self.pb = torch.empty(d, n, dtype=dtype, device=device)
+        self.a = torch.empty(n, dtype=dtype, device=device)
+        self.x = torch.empty(n, dtype=dtype, device=device)
+        self.beta = torch.zeros(_abi.BQ_MAX_RANK, dtype=torch.float64, device=device)
+        self.report = torch.zeros(_abi.REPORT_BYTES, dtype=torch.uint8, device=device)
+
+
+def _launch(prob: DualTvProblem, v: torch.Tensor, ws: ProxWorkspace, eps, max_iter, accelerated):
+    g, w = prob.grid, prob.w
+    if v.numel() != g.size:
+        raise ValueError(f"expected {g.size} entries, got {v.numel()}")
+    if w.rank and w.dim != g.size:
+        raise ValueError(f"dimension mismatch: metric is {w.dim}, grid is {g.size}")
+    lo, hi, lo_a, hi_a = prob.box.device_args(ws.dtype, ws.device)
+    desc = _abi.WtvDesc()
+    desc.ndim = g.ndim
+    desc.dtype = _abi.dtype_code(ws.dtype)
+    desc.dims[:] = g.dims3
+    desc.mode = prob.mode.code
+    desc.rank = w.rank
+    desc.sign = w.sign
+    desc.accelerated = int(bool(accelerated))
+    desc.tau = w.tau if w.d is None else 0.0
+    desc.reg = float(prob.reg)
+    desc.step = dual_step_size(prob) if prob.reg > 0 else 0.0
+    desc.eps = float(eps)
+    desc.max_iter = int(max_iter)
+    desc.newton_max_iter = int(prob.newton_max_iter)
+    desc.newton_eps = float(prob.newton_eps)
+    desc.lo, desc.hi = lo, hi
+    desc.lo_arr, desc.hi_arr = _abi.ptr(lo_a), _abi.ptr(hi_a)
+    desc.d = _abi.ptr(w.d)
+    desc.U = w.Ut.data_ptr() if w.rank else None
+    desc.v = v.data_ptr()
+    desc.p, desc.pb, desc.a, desc.x = ws.p.data_ptr(), ws.pb.data_ptr(), ws.a.data_ptr(), ws.x.data_ptr()
+    desc.beta = ws.beta.data_ptr()
+    desc.report = ws.report.data_ptr()
+    lib = _abi.load_library()
+    _abi.check(lib.bq_wtv_prox(_abi.ctx_for(ws.device), desc, _abi.stream_ptr(ws.device)), "solve")
+    # keep optional temporaries alive until the stream has consumed them
+    ws._keep = (lo_a, hi_a, v)
+
+
+def _check_args(prob, eps, max_iter):
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+
+
+def solve_async(prob: DualTvProblem, ws: ProxWorkspace, eps=1e-5, max_iter=100, accelerated=True,
+                load_warm=True):
+    """GPU-resident solve: reads v/warm start from ``prob`` (torch), writes ws.x,
+    ws.p (P*), ws.beta (beta*) and the device report.  No host sync."""
+    _check_args(prob, eps, max_iter)
+    v = to_dev(prob.v, ws.dtype, ws.device)
+    d, n = prob.grid.ndim, prob.grid.size
+    if load_warm:
+        if prob.warm_start is not None:
+            p0 = to_dev(prob.warm_start, ws.dtype, ws.device)
+            if p0.numel() != d * n or (not is_torch(prob.warm_start) and np.shape(prob.warm_start) != (d, n)):
+                raise ValueError(f"warm start must have shape {(d, n)}")
+            ws.p.copy_(p0.reshape(d, n))
+        else:
+            ws.p.zero_()
+        ws.beta.zero_()
+        bw = prob.beta_warm
+        if bw is not None and np.shape(bw)[0] == prob.w.rank and prob.w.rank:
+            ws.beta[: prob.w.rank] = to_dev(bw, torch.float64, ws.device)
+    _launch(prob, v, ws, eps, max_iter, accelerated)
+    return ws
+
+
+def read_report(ws: ProxWorkspace) -> _abi.WtvReport:
+    rep = _abi.WtvReport.from_buffer_copy(ws.report.cpu().numpy().tobytes())
+    if rep.status:
+        _abi.check(rep.status, "solve")
+    return rep
+
+
+def solve(prob: DualTvProblem, eps=1e-5, max_iter=100, accelerated=True) -> DualSolveReport:
+    """Drop-in for ``tvqn.dual_tv_solver.solve`` (dual_tv_solver.py:161-250)."""
+    _check_args(prob, eps, max_iter)
+    dtype = prob.w.dtype
+    if is_torch(prob.v) and prob.v.dtype in (torch.float32, torch.float64):
+        dtype = prob.v.dtype
+    ws = ProxWorkspace(prob.grid, dtype, prob.w.device)
+    solve_async(prob, ws, eps, max_iter, accelerated)
+    rep = read_report(ws)
+    r = prob.w.rank
+    like = prob.v
+    beta = ws.beta[:r]
+    if prob.reg == 0.0:
+        p_star = prob.warm_start if prob.warm_start is not None else out_like(like, torch.zeros_like(ws.p))
+        if not is_torch(like) and prob.warm_start is not None:
+            p_star = np.asarray(prob.warm_start)
+    else:
+        p_star = out_like(like, ws.p)
+    return DualSolveReport(
+        x=out_like(like, ws.x),
+        p_star=p_star,
+        iterations=int(rep.iterations),
+        rel_change=float(rep.rel_change),
+        converged=bool(rep.converged),
+        newton_iterations=int(rep.newton_iterations),
+        beta_star=out_like(like, beta) if r else (np.zeros(0) if not is_torch(like) else beta),
+    )
+
+
+__all__ = ["DualTvProblem", "DualSolveReport", "dual_step_size", "solve", "solve_async",
+           "ProxWorkspace", "read_report"]

@@ -1,0 +1,236 @@
+"""Metric W = diag(d) +/- U U^T and the structured weighted box projection.
+
+Mirror of the reference ``tvqn.wpm`` surface used on the hot path
+(``/root/reference/pkg/src/tvqn/wpm.py``), executed by libbq on the device:
+
+* ``DiagPlusLowRank(tau, U, sign=1)`` (:24-78).  Extension: ``d=`` gives a
+  per-voxel diagonal (W = diag(d) + sign U U^T, the Theorem-1 extension that
+  BASELINE config 2 needs and the reference cannot represent).
+  Construction raises ``ValueError`` on tau <= 0, bad sign, or a capacitance
+  that is not positive definite, like the reference.
+* ``apply_metric`` (:81-89) / ``apply_metric_inverse`` (:92-106) ->
+  ``bq_metric_apply``.
+* ``BoxSet`` (:109-133), ``prox_box_diag`` (:136-142).
+* ``wpm_box`` (:234-253) -> ``bq_wpm_box`` (device semi-smooth Newton with
+  the reference's best-residual / Levenberg rules, all decisions on device).
+
+Storage: U lives on the device as ``rank`` contiguous N-vectors (shape
+(r, N)), the coalesced layout of every kernel.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._tensors import default_device, is_torch, out_like, pick_dtype, to_dev
+
+
+class DiagPlusLowRank:
+    """W = tau*I (or diag(d)) + sign * U U^T, U of shape (N, r)."""
+
+    def __init__(self, tau, U, sign=1, d=None, dtype=None, device=None):
+        if d is None and not (np.ndim(tau) == 0 and float(tau) > 0):
+            raise ValueError(f"tau must be positive, got {tau}")
+        if sign not in (1, -1):
+            raise ValueError(f"sign must be +1 or -1, got {sign}")
+        self.tau = float(tau) if d is None else float("nan")
+        self.sign = int(sign)
+        dtype = dtype or pick_dtype(U, d)
+        device = device or default_device()
+        self.dtype = dtype
+        self.device = device
+        if is_torch(U):
+            u = U.to(device=device, dtype=dtype)
+        else:
+            u = torch.from_numpy(np.asarray(U, dtype=np.float64)).to(device=device, dtype=dtype)
+        if u.ndim == 1:
+            u = u[:, None] if u.numel() else u.reshape(0, 0)
+        if u.ndim != 2:
+            raise ValueError("U must be a 2-D array of shape (N, r)")
+        if u.shape[1] > _abi.BQ_MAX_RANK:
+            raise ValueError(f"rank {u.shape[1]} exceeds the device limit {_abi.BQ_MAX_RANK}")
+        self._n = int(u.shape[0])
+        self.Ut = u.t().contiguous()  # (r, N) device
+        self.d = None
+        if d is not None:
+            dt = to_dev(d, dtype, device)
+            if dt.numel() != self._n and self._n:
+                raise ValueError("d must have one entry per voxel")
+            if not bool((dt > 0).all()):
+                raise ValueError("diagonal d must be positive")
+            self.d = dt
+        self.gram = None
+        if self.rank:
+            self.gram = torch.empty(self.rank * self.rank, dtype=torch.float64, device=device)
+            lib = _abi.load_library()
+            _abi.check(
+                lib.bq_metric_gram(
+                    _abi.ctx_for(device), _abi.dtype_code(dtype), self._n, self.rank,
+                    self.tau if self.d is None else 0.0, _abi.ptr(self.d), self.Ut.data_ptr(),
+                    self.gram.data_ptr(), _abi.stream_ptr(device),
+                ),
+                "DiagPlusLowRank",
+            )
+            g = self.gram.cpu().numpy().reshape(self.rank, self.rank)
+            cap = np.eye(self.rank) + self.sign * (g / self.tau if self.d is None else g)
+            try:
+                np.linalg.cholesky(cap)
+            except np.linalg.LinAlgError as exc:
+                raise ValueError("metric is not positive definite") from exc
+
+    @classmethod
+    def diagonal(cls, tau, n=0, **kw):
+        return cls(tau=tau, U=np.zeros((n, 0)), **kw)
+
+    @property
+    def rank(self) -> int:
+        return int(self.Ut.shape[0])
+
+    @property
+    def dim(self) -> int:
+        return self._n
+
+    @property
+    def U(self) -> np.ndarray:
+        return self.Ut.t().cpu().numpy()
+
+    def min_diag(self) -> float:
+        """Smallest diagonal entry: the safe lower eigen-bound for omega (D-6)."""
+        return self.tau if self.d is None else float(self.d.min().item())
+
+    def dense(self, n=None):
+        n = self.dim if n is None else n
+        diag = np.full(n, self.tau) if self.d is None else self.d.cpu().numpy().astype(float)
+        w = np.diag(diag)
+        if self.rank:
+            u = self.U.astype(float)
+            w = w + self.sign * (u @ u.T)
+        return w
+
+
+def _metric_call(w: DiagPlusLowRank, x, inverse: bool):
+    xt = to_dev(x, w.dtype, w.device)
+    if w.rank and xt.numel() != w.dim:
+        raise ValueError(f"dimension mismatch: metric is {w.dim}, vector is {xt.numel()}")
+    out = torch.empty_like(xt)
+    lib = _abi.load_library()
+    _abi.check(
+        lib.bq_metric_apply(
+            _abi.ctx_for(w.device), _abi.dtype_code(w.dtype), xt.numel(), w.rank, w.sign,
+            w.tau if w.d is None else 0.0, _abi.ptr(w.d), _abi.ptr(w.Ut) if w.rank else None,
+            _abi.ptr(w.gram), int(inverse), xt.data_ptr(), out.data_ptr(), _abi.stream_ptr(w.device),
+        ),
+        "apply_metric_inverse" if inverse else "apply_metric",
+    )
+    return out_like(x, out)
+
+
+def apply_metric(w: DiagPlusLowRank, x):
+    """W x (reference wpm.py:81-89)."""
+    return _metric_call(w, x, False)
+
+
+def apply_metric_inverse(w: DiagPlusLowRank, x):
+    """W^-1 x by Woodbury with the device-factorised capacitance (wpm.py:92-106)."""
+    return _metric_call(w, x, True)
+
+
+@dataclass(frozen=True, eq=False)
+class BoxSet:
+    """Componentwise bounds (scalars or per-voxel arrays); default [0, inf)."""
+
+    lower: object = 0.0
+    upper: object = np.inf
+
+    def __post_init__(self):
+        lo = self.lower.detach().cpu().numpy() if is_torch(self.lower) else np.asarray(self.lower, dtype=float)
+        hi = self.upper.detach().cpu().numpy() if is_torch(self.upper) else np.asarray(self.upper, dtype=float)
+        if np.any(lo > hi):
+            raise ValueError("box lower bounds exceed upper bounds")
+        object.__setattr__(self, "lower", lo if lo.ndim else float(lo))
+        object.__setattr__(self, "upper", hi if hi.ndim else float(hi))
+
+    @classmethod
+    def nonnegative(cls):
+        return cls(0.0, np.inf)
+
+    @classmethod
+    def unbounded(cls):
+        return cls(-np.inf, np.inf)
+
+    def is_unbounded(self):
+        return bool(np.all(np.isneginf(self.lower)) and np.all(np.isposinf(self.upper)))
+
+    def device_args(self, dtype, device):
+        """(lo, hi, lo_tensor|None, hi_tensor|None) for the C ABI."""
+        lo_a = hi_a = None
+        lo = hi = 0.0
+        if isinstance(self.lower, np.ndarray):
+            lo_a = to_dev(self.lower, dtype, device)
+        else:
+            lo = float(self.lower)
+        if isinstance(self.upper, np.ndarray):
+            hi_a = to_dev(self.upper, dtype, device)
+        else:
+            hi = float(self.upper)
+        return lo, hi, lo_a, hi_a
+
+
+def prox_box_diag(x, box: BoxSet):
+    """Componentwise clamp (wpm.py:136-142): wpm_box under a rank-0 metric."""
+    n = int(np.prod(np.shape(x))) if not is_torch(x) else x.numel()
+    return wpm_box(x, DiagPlusLowRank.diagonal(1.0, n, dtype=pick_dtype(x)), box)
+
+
+def wpm_box(x, w: DiagPlusLowRank, box: BoxSet, beta0=None, eps=1e-6, max_iter=50, full_output=False):
+    """Weighted projection of x onto the box under W (wpm.py:234-253) on the device."""
+    xt = to_dev(x, w.dtype, w.device)
+    n = xt.numel()
+    if w.rank and n != w.dim:
+        raise ValueError(f"dimension mismatch: metric is {w.dim}, vector is {n}")
+    lo, hi, lo_a, hi_a = box.device_args(w.dtype, w.device)
+    beta = torch.zeros(max(w.rank, 1), dtype=torch.float64, device=w.device)
+    if beta0 is not None and w.rank:
+        beta[: w.rank] = to_dev(beta0, torch.float64, w.device)
+    out = torch.empty_like(xt)
+    a_scr = torch.empty_like(xt)
+    report = torch.zeros(_abi.REPORT_BYTES, dtype=torch.uint8, device=w.device)
+    lib = _abi.load_library()
+    _abi.check(
+        lib.bq_wpm_box(
+            _abi.ctx_for(w.device), _abi.dtype_code(w.dtype), n, w.rank, w.sign,
+            w.tau if w.d is None else 0.0, _abi.ptr(w.d), _abi.ptr(w.Ut) if w.rank else None,
+            xt.data_ptr(), lo, hi, _abi.ptr(lo_a), _abi.ptr(hi_a), beta.data_ptr(), float(eps),
+            int(max_iter), out.data_ptr(), a_scr.data_ptr(), report.data_ptr(), _abi.stream_ptr(w.device),
+        ),
+        "wpm_box",
+    )
+    u = out_like(x, out)
+    if not full_output:
+        return u
+    rep = _abi.WtvReport.from_buffer_copy(report.cpu().numpy().tobytes())
+    if rep.status:
+        _abi.check(rep.status, "wpm_box")
+    b = beta[: w.rank]
+    info = {
+        "beta": out_like(beta0 if beta0 is not None else x, b) if w.rank else np.zeros(0),
+        "iterations": int(rep.last_newton_iterations),
+        "residual": float(rep.newton_residual),
+        "converged": bool(rep.last_newton_converged),
+    }
+    return u, info
+
+
+__all__ = [
+    "DiagPlusLowRank",
+    "BoxSet",
+    "apply_metric",
+    "apply_metric_inverse",
+    "prox_box_diag",
+    "wpm_box",
+]

@@ -1,0 +1,220 @@
+"""Generate golden vectors by running the REFERENCE implementation.
+
+Run in the build container (where /root/reference exists):
+
+    python tests/golden/make_golden.py
+
+It imports the unmodified reference package (``/root/reference/pkg/src``)
+and its independent dense test oracles (``/root/reference/pkg/tests/oracles.py``),
+evaluates them on seeded inputs, and writes ``tests/golden/*.npz``.  The
+GPU box never sees /root/reference: tests there read only these fixtures.
+"""
+
+from __future__ import annotations
+
+import sys
+from pathlib import Path
+
+import numpy as np
+
+REF = Path("/root/reference/pkg")
+OUT = Path(__file__).resolve().parent
+
+
+def _import_reference():
+    sys.path.insert(0, str(REF / "src"))
+    sys.path.insert(0, str(REF / "tests"))
+    import tvqn  # noqa: F401
+    from tvqn import dual_tv_solver, forward_models, hessian_sr1, solvers, tv_ops, wpm
+    import oracles
+
+    return tv_ops, wpm, dual_tv_solver, hessian_sr1, solvers, forward_models, oracles
+
+
+def main():
+    tv_ops, wpm, dts, sr1, solvers, fm, oracles = _import_reference()
+    Grid, TvMode = tv_ops.Grid, tv_ops.TvMode
+    out = {}
+
+    # ---- stencils and TV value (tv_ops.py:107-167) ------------------------
+    rng = np.random.default_rng(101)
+    for dims in [(7,), (5, 4), (4, 3, 2), (6, 5, 4)]:
+        g = Grid(dims)
+        x = rng.standard_normal(g.size)
+        p = rng.standard_normal((g.ndim, g.size))
+        key = "x".join(map(str, dims))
+        out[f"stencil_{key}_x"] = x
+        out[f"stencil_{key}_p"] = p
+        out[f"stencil_{key}_grad"] = tv_ops.gradient_stack(g, x)
+        out[f"stencil_{key}_div"] = tv_ops.dual_divergence(g, p)
+        out[f"stencil_{key}_tv_iso"] = np.array(tv_ops.tv_value(g, x, TvMode.ISOTROPIC))
+        out[f"stencil_{key}_tv_aniso"] = np.array(tv_ops.tv_value(g, x, TvMode.ANISOTROPIC))
+        out[f"stencil_{key}_proj_iso"] = tv_ops.project_dual(2.0 * p, TvMode.ISOTROPIC)
+        out[f"stencil_{key}_proj_aniso"] = tv_ops.project_dual(2.0 * p, TvMode.ANISOTROPIC)
+
+    # ---- metric apply / inverse (wpm.py:81-106) ---------------------------
+    rng = np.random.default_rng(202)
+    for i, (n, r, sign, scale) in enumerate([(64, 0, 1, 1.0), (64, 1, 1, 1.0), (256, 4, 1, 1.0),
+                                             (32, 2, -1, 0.08), (100, 8, 1, 2.0)]):
+        tau = float(rng.uniform(0.5, 2.0))
+        u = scale * rng.standard_normal((n, r)) / (np.sqrt(n) if sign > 0 else 1.0)
+        w = wpm.DiagPlusLowRank(tau, u, sign=sign)
+        x = rng.standard_normal(n)
+        out[f"metric{i}_tau"] = np.array(tau)
+        out[f"metric{i}_U"] = u
+        out[f"metric{i}_sign"] = np.array(sign)
+        out[f"metric{i}_x"] = x
+        out[f"metric{i}_Wx"] = wpm.apply_metric(w, x)
+        out[f"metric{i}_Winvx"] = wpm.apply_metric_inverse(w, x)
+
+    # ---- wpm_box (wpm.py:234-253) -----------------------------------------
+    rng = np.random.default_rng(303)
+    cases = [(200, 1, 0.0, np.inf, None), (200, 3, -0.5, 1.5, None), (500, 2, 0.0, np.inf, "warm"),
+             (64, 4, 0.0, 0.1, None)]
+    for i, (n, r, lo, hi, warm) in enumerate(cases):
+        tau = float(rng.uniform(0.5, 2.0))
+        u = rng.standard_normal((n, r)) / np.sqrt(n) * 3.0
+        w = wpm.DiagPlusLowRank(tau, u)
+        x = rng.standard_normal(n)
+        beta0 = rng.standard_normal(r) * 0.1 if warm else None
+        uo, info = wpm.wpm_box(x, w, wpm.BoxSet(lo, hi), beta0=beta0, full_output=True)
+        out[f"wpm{i}_tau"] = np.array(tau)
+        out[f"wpm{i}_U"] = u
+        out[f"wpm{i}_x"] = x
+        out[f"wpm{i}_lo"] = np.array(lo)
+        out[f"wpm{i}_hi"] = np.array(hi)
+        out[f"wpm{i}_beta0"] = np.zeros(r) if beta0 is None else beta0
+        out[f"wpm{i}_has_beta0"] = np.array(beta0 is not None)
+        out[f"wpm{i}_u"] = uo
+        out[f"wpm{i}_beta"] = info["beta"]
+        out[f"wpm{i}_iters"] = np.array(info["iterations"])
+
+    # ---- prox solve (dual_tv_solver.py:161-250) ---------------------------
+    rng = np.random.default_rng(404)
+    prox_cases = [
+        # dims, rank, reg, mode, lo, hi, eps, max_iter, accelerated, tau, warm
+        ((8, 8), 1, 0.3, "iso", 0.0, np.inf, 1e-5, 100, True, 1.0, False),
+        ((6, 6), 1, 0.3, "aniso", 0.0, np.inf, 1e-5, 100, True, 1.3, False),
+        ((8, 8), 2, 0.5, "iso", 0.0, np.inf, 1e-5, 30, True, 0.7, False),
+        ((6, 6), 1, 0.4, "iso", 0.0, np.inf, 1e-15, 1, False, 1.0, True),
+        ((4, 4, 4), 1, 0.3, "iso", 0.0, np.inf, 1e-5, 100, True, 1.0, False),
+        ((16, 16, 16), 1, 0.05, "iso", 0.0, np.inf, 1e-300, 40, True, 1.25, False),
+        ((12, 10, 8), 4, 0.02, "iso", 0.0, 0.1, 1e-5, 100, True, 3.0, True),
+        ((24, 24, 24), 1, 0.05, "iso", 0.0, np.inf, 1e-300, 100, True, 1.25, False),
+        ((10, 9, 7), 0, 0.1, "aniso", -0.2, 0.5, 1e-5, 60, True, 2.0, False),
+        ((9, 7), 3, 0.0, "iso", 0.0, np.inf, 1e-5, 100, True, 1.0, True),
+        ((33, 17), 1, 0.2, "iso", 0.0, np.inf, 1e-8, 200, True, 0.9, False),
+        ((20,), 1, 0.3, "iso", 0.0, np.inf, 1e-6, 100, True, 1.0, False),
+    ]
+    for i, (dims, r, reg, mode, lo, hi, eps, mi, acc, tau, warm) in enumerate(prox_cases):
+        g = Grid(dims)
+        v = rng.standard_normal(g.size) * 0.5 + 0.3
+        u = rng.standard_normal((g.size, r)) / np.sqrt(g.size)
+        w = wpm.DiagPlusLowRank(tau, u) if r else wpm.DiagPlusLowRank.diagonal(tau, g.size)
+        p0 = 0.3 * rng.standard_normal((g.ndim, g.size)) if warm else None
+        b0 = 0.01 * rng.standard_normal(r) if (warm and r) else None
+        prob = dts.DualTvProblem(grid=g, v=v, w=w, reg=reg, mode=mode, box=wpm.BoxSet(lo, hi),
+                                 warm_start=p0, beta_warm=b0)
+        rep = dts.solve(prob, eps=eps, max_iter=mi, accelerated=acc)
+        k = f"prox{i}"
+        out[k + "_dims"] = np.array(dims)
+        out[k + "_rank"] = np.array(r)
+        out[k + "_reg"] = np.array(reg)
+        out[k + "_iso"] = np.array(mode == "iso")
+        out[k + "_lo"] = np.array(lo)
+        out[k + "_hi"] = np.array(hi)
+        out[k + "_eps"] = np.array(eps)
+        out[k + "_max_iter"] = np.array(mi)
+        out[k + "_acc"] = np.array(acc)
+        out[k + "_tau"] = np.array(tau)
+        out[k + "_v"] = v
+        out[k + "_U"] = u
+        out[k + "_has_warm"] = np.array(bool(warm))
+        out[k + "_p0"] = p0 if p0 is not None else np.zeros((g.ndim, g.size))
+        out[k + "_b0"] = b0 if b0 is not None else np.zeros(r)
+        out[k + "_x"] = rep.x
+        out[k + "_p_star"] = np.asarray(rep.p_star)
+        out[k + "_iterations"] = np.array(rep.iterations)
+        out[k + "_rel"] = np.array(rep.rel_change)
+        out[k + "_converged"] = np.array(rep.converged)
+        out[k + "_newton"] = np.array(rep.newton_iterations)
+        out[k + "_beta"] = np.asarray(rep.beta_star if rep.beta_star is not None else np.zeros(0))
+    out["prox_count"] = np.array(len(prox_cases))
+
+    # ---- diag(d) extension pinned by the reference's Condat-Vu dense oracle
+    rng = np.random.default_rng(505)
+    for i, (dims, iso) in enumerate([((8, 8), True), ((6, 6), False), ((4, 4, 3), True)]):
+        n = int(np.prod(dims))
+        d = rng.uniform(0.5, 2.0, n)
+        u = rng.standard_normal((n, 1)) / np.sqrt(n)
+        v = rng.standard_normal(n)
+        reg = 0.3
+        wd = np.diag(d) + u @ u.T
+        xref = oracles.condat_vu_tv(dims, wd, v, reg, 0.0, np.inf, iters=40000, isotropic=iso)
+        out[f"diag{i}_dims"] = np.array(dims)
+        out[f"diag{i}_iso"] = np.array(iso)
+        out[f"diag{i}_d"] = d
+        out[f"diag{i}_U"] = u
+        out[f"diag{i}_v"] = v
+        out[f"diag{i}_reg"] = np.array(reg)
+        out[f"diag{i}_x_cv"] = xref
+        out[f"diag{i}_obj_cv"] = np.array(oracles.tv_objective(dims, wd, v, reg, xref, isotropic=iso))
+
+    # ---- SR1 (hessian_sr1.py:52-101) ---------------------------------------
+    rng = np.random.default_rng(606)
+    s_list, m_list, tau_l, u_l, has_l = [], [], [], [], []
+    for trial in range(40):
+        n = 50
+        s = rng.standard_normal(n)
+        if trial % 4 == 0:
+            m = -s  # negative curvature -> fallback
+        elif trial % 4 == 1:
+            m = 2.0 * s + 1e-3 * rng.standard_normal(n)
+        elif trial % 4 == 2:
+            a = rng.standard_normal((n, n))
+            m = (a @ a.T / n + 0.5 * np.eye(n)) @ s
+        else:
+            m = rng.standard_normal(n)
+        est = sr1.estimate_sr1(s, m, gamma=0.8, alpha_fallback=1.7)
+        s_list.append(s)
+        m_list.append(m)
+        tau_l.append(est.tau)
+        has_l.append(est.u is not None)
+        u_l.append(est.u if est.u is not None else np.zeros(n))
+    out["sr1_s"] = np.array(s_list)
+    out["sr1_m"] = np.array(m_list)
+    out["sr1_tau"] = np.array(tau_l)
+    out["sr1_u"] = np.array(u_l)
+    out["sr1_has_u"] = np.array(has_l)
+
+    # ---- aggregate_metric + compute_v_k (solvers.py:67-89) ----------------
+    rng = np.random.default_rng(707)
+    n = 300
+    slots = []
+    for t in range(4):
+        x = rng.standard_normal(n)
+        g = rng.standard_normal(n)
+        u = rng.standard_normal(n) / np.sqrt(n) if t != 2 else None
+        tau = float(rng.uniform(0.5, 2.0))
+        slots.append(solvers.SubsetSlot(x=x, grad=g, hess=sr1.Sr1Estimate(tau=tau, u=u)))
+        out[f"vk_x{t}"] = x
+        out[f"vk_g{t}"] = g
+        out[f"vk_tau{t}"] = np.array(tau)
+        out[f"vk_u{t}"] = u if u is not None else np.zeros(n)
+        out[f"vk_has_u{t}"] = np.array(u is not None)
+    w = solvers.aggregate_metric(slots)
+    out["vk_v"] = solvers.compute_v_k(slots, w, 0.7)
+    out["vk_tau_w"] = np.array(w.tau)
+    out["vk_U_w"] = w.U
+
+    # ---- schedule (solvers.py:29-55) ---------------------------------------
+    out["kappa_table"] = np.array([[solvers.kappa(k, t, 4) for t in range(1, 5)] for k in range(1, 13)])
+    out["partition_equi_30_4"] = np.concatenate(solvers.partition_views(30, 4))
+    out["partition_contig_30_4"] = np.concatenate(solvers.partition_views(30, 4, "contiguous"))
+
+    np.savez_compressed(OUT / "reference_golden.npz", **out)
+    print(f"wrote {OUT / 'reference_golden.npz'} ({len(out)} arrays)")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,179 @@
+"""Parity of the device prox / WPM / metric path (through the C ABI) against the
+reference golden vectors and the CPU oracle.  Tolerances (north star):
+fp64 <= 1e-10 relative L2, fp32 <= 1e-4."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from oracle import prox as O
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # collected on CPU boxes, skipped there
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_2307_02043_b200 as bq  # noqa: E402
+from paper_2307_02043_b200 import dual_tv_solver as D  # noqa: E402
+from paper_2307_02043_b200 import wpm as W  # noqa: E402
+
+F64_TOL = 1e-10
+F32_TOL = 1e-4
+
+
+def _prox_problem(golden, i, dtype=None):
+    k = f"prox{i}"
+    dims = tuple(int(v) for v in golden[k + "_dims"])
+    r = int(golden[k + "_rank"])
+    n = int(np.prod(dims))
+    tau = float(golden[k + "_tau"])
+    if dtype is None:
+        w = W.DiagPlusLowRank(tau, golden[k + "_U"]) if r else W.DiagPlusLowRank.diagonal(tau, n)
+        v = golden[k + "_v"]
+    else:
+        u = torch.tensor(golden[k + "_U"], dtype=dtype, device="cuda")
+        w = W.DiagPlusLowRank(tau, u) if r else W.DiagPlusLowRank.diagonal(tau, n, dtype=dtype)
+        v = torch.tensor(golden[k + "_v"], dtype=dtype, device="cuda")
+    warm = bool(golden[k + "_has_warm"])
+    prob = D.DualTvProblem(
+        grid=bq.Grid(dims), v=v, w=w, reg=float(golden[k + "_reg"]),
+        mode="iso" if bool(golden[k + "_iso"]) else "aniso",
+        box=W.BoxSet(float(golden[k + "_lo"]), float(golden[k + "_hi"])),
+        warm_start=golden[k + "_p0"] if warm else None,
+        beta_warm=golden[k + "_b0"] if (warm and r) else None,
+    )
+    kw = dict(eps=float(golden[k + "_eps"]), max_iter=int(golden[k + "_max_iter"]),
+              accelerated=bool(golden[k + "_acc"]))
+    return prob, kw
+
+
+@pytest.mark.parametrize("i", range(12))
+def test_prox_f64_matches_reference_golden(golden, i):
+    prob, kw = _prox_problem(golden, i)
+    rep = D.solve(prob, **kw)
+    k = f"prox{i}"
+    assert isinstance(rep.x, np.ndarray)
+    assert rel_l2(rep.x, golden[k + "_x"]) <= F64_TOL
+    assert rel_l2(rep.p_star, golden[k + "_p_star"]) <= F64_TOL
+    assert rep.iterations == int(golden[k + "_iterations"])
+    assert rep.converged == bool(golden[k + "_converged"])
+    assert rep.newton_iterations == int(golden[k + "_newton"])
+    if int(golden[k + "_rank"]):
+        assert rel_l2(rep.beta_star, golden[k + "_beta"]) <= 1e-8
+    assert np.all(rep.x >= float(golden[k + "_lo"])) and np.all(rep.x <= float(golden[k + "_hi"]))
+
+
+@pytest.mark.parametrize("i", [0, 4, 5, 7, 10])
+def test_prox_f32_close_to_reference(golden, i):
+    prob, kw = _prox_problem(golden, i, dtype=torch.float32)
+    # fixed iteration count so fp32 roundoff cannot move the stopping decision
+    kw["eps"] = 1e-300
+    rep = D.solve(prob, **kw)
+    ref = O.fgp_prox(prob.grid.dims, golden[f"prox{i}_v"],
+                     O.Metric(tau=prob.w.tau, U=golden[f"prox{i}_U"] if prob.w.rank else None, n=prob.grid.size),
+                     reg=prob.reg, lo=float(golden[f"prox{i}_lo"]), hi=float(golden[f"prox{i}_hi"]),
+                     isotropic=prob.mode.value == "isotropic", eps=1e-300, max_iter=kw["max_iter"],
+                     accelerated=kw["accelerated"])
+    assert rep.x.dtype == torch.float32
+    assert rel_l2(rep.x.cpu().numpy(), ref["x"]) <= F32_TOL
+    assert rel_l2(rep.p_star.cpu().numpy(), ref["p_star"]) <= F32_TOL
+
+
+def _diag_problem(seed, dims, r=1, reg=0.05, iso=True, lo=0.0, hi=np.inf):
+    rng = np.random.default_rng(seed)
+    n = int(np.prod(dims))
+    d = rng.uniform(0.5, 2.0, n)
+    u = rng.standard_normal((n, r)) / np.sqrt(n)
+    v = rng.standard_normal(n) * 0.5 + 0.3
+    return d, u, v
+
+
+@pytest.mark.parametrize("dims,r,iso", [((16, 16, 16), 1, True), ((32, 24, 20), 2, True), ((40, 33), 3, False),
+                                        ((20, 18, 16), 4, True)])
+def test_diag_prox_f64_vs_oracle(dims, r, iso):
+    d, u, v = _diag_problem(7, dims, r)
+    prob = D.DualTvProblem(grid=bq.Grid(dims), v=v, w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05,
+                           mode="iso" if iso else "aniso", box=W.BoxSet(0.0, np.inf))
+    rep = D.solve(prob, eps=1e-300, max_iter=60)
+    ref = O.fgp_prox(dims, v, O.Metric(U=u, d=d), reg=0.05, isotropic=iso, eps=1e-300, max_iter=60)
+    assert rel_l2(rep.x, ref["x"]) <= F64_TOL
+    assert rel_l2(rep.p_star, ref["p_star"]) <= F64_TOL
+    assert rep.newton_iterations == ref["newton_iterations"]
+
+
+def test_config2_shape_f32_vs_f64_and_oracle_64():
+    """Config-2 law (W = diag(d) + uu^T, iso TV 0.05, box [0, inf), 100 FGP iters)
+    at 64^3: fp32 and fp64 device results vs the fp64 oracle."""
+    from paper_2307_02043_b200.configs import config2_inputs
+
+    inp = config2_inputs(n=64)
+    ref = O.fgp_prox((64, 64, 64), inp["v"], O.Metric(U=inp["u"][:, None], d=inp["d"]), reg=0.05,
+                     eps=1e-300, max_iter=100)
+    for dtype, tol in [(torch.float64, F64_TOL), (torch.float32, F32_TOL)]:
+        w = W.DiagPlusLowRank(1.0, torch.tensor(inp["u"][:, None], dtype=dtype, device="cuda"),
+                              d=torch.tensor(inp["d"], dtype=dtype, device="cuda"))
+        v = torch.tensor(inp["v"], dtype=dtype, device="cuda")
+        rep = D.solve(D.DualTvProblem(grid=bq.Grid((64, 64, 64)), v=v, w=w, reg=0.05), eps=1e-300, max_iter=100)
+        assert rel_l2(rep.x.double().cpu().numpy(), ref["x"]) <= tol
+        assert rel_l2(rep.p_star.double().cpu().numpy(), ref["p_star"]) <= tol
+
+
+def test_prox_is_deterministic():
+    d, u, v = _diag_problem(3, (32, 32, 32), 2)
+    prob = D.DualTvProblem(grid=bq.Grid((32, 32, 32)), v=torch.tensor(v, device="cuda"),
+                           w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05)
+    a = D.solve(prob, eps=1e-300, max_iter=50)
+    b = D.solve(prob, eps=1e-300, max_iter=50)
+    assert torch.equal(a.x, b.x) and torch.equal(a.p_star, b.p_star)
+
+
+@pytest.mark.parametrize("i", range(4))
+def test_wpm_box_matches_reference_golden(golden, i):
+    w = W.DiagPlusLowRank(float(golden[f"wpm{i}_tau"]), golden[f"wpm{i}_U"])
+    beta0 = golden[f"wpm{i}_beta0"] if bool(golden[f"wpm{i}_has_beta0"]) else None
+    u, info = W.wpm_box(golden[f"wpm{i}_x"], w, W.BoxSet(float(golden[f"wpm{i}_lo"]), float(golden[f"wpm{i}_hi"])),
+                        beta0=beta0, full_output=True)
+    assert rel_l2(u, golden[f"wpm{i}_u"]) <= F64_TOL
+    assert rel_l2(info["beta"], golden[f"wpm{i}_beta"]) <= 1e-8
+    assert info["iterations"] == int(golden[f"wpm{i}_iters"])
+
+
+@pytest.mark.parametrize("i", range(5))
+def test_metric_matches_reference_golden(golden, i):
+    w = W.DiagPlusLowRank(float(golden[f"metric{i}_tau"]), golden[f"metric{i}_U"], sign=int(golden[f"metric{i}_sign"]))
+    x = golden[f"metric{i}_x"]
+    assert rel_l2(W.apply_metric(w, x), golden[f"metric{i}_Wx"]) <= 1e-13
+    assert rel_l2(W.apply_metric_inverse(w, x), golden[f"metric{i}_Winvx"]) <= 1e-12
+
+
+def test_metric_errors_map_to_value_error():
+    with pytest.raises(ValueError):
+        W.DiagPlusLowRank(0.0, np.zeros((3, 0)))
+    with pytest.raises(ValueError):
+        W.DiagPlusLowRank(1.0, np.array([[2.0], [0.0]]), sign=-1)
+    W.DiagPlusLowRank(1.0, 0.4 * np.array([[2.0], [0.0]]), sign=-1)
+    w = W.DiagPlusLowRank(1.0, np.ones((4, 1)))
+    with pytest.raises(ValueError):
+        W.apply_metric(w, np.ones(5))
+
+
+def test_solve_rejects_bad_arguments():
+    rng = np.random.default_rng(15)
+    prob = D.DualTvProblem(grid=bq.Grid((8, 8)), v=rng.standard_normal(64),
+                           w=W.DiagPlusLowRank(1.0, rng.standard_normal((64, 1)) / 8), reg=0.3)
+    with pytest.raises(ValueError):
+        D.solve(prob, eps=0.0)
+    with pytest.raises(ValueError):
+        D.solve(prob, max_iter=0)
+    with pytest.raises(ValueError):
+        D.DualTvProblem(grid=prob.grid, v=prob.v, w=prob.w, reg=-1.0)
+
+
+def test_tv_value_matches_reference_golden(golden):
+    for key in ["7", "5x4", "4x3x2", "6x5x4"]:
+        dims = tuple(int(k) for k in key.split("x"))
+        x = golden[f"stencil_{key}_x"]
+        assert bq.tv_value(bq.Grid(dims), x, "iso") == pytest.approx(float(golden[f"stencil_{key}_tv_iso"]), rel=1e-13)
+        assert bq.tv_value(bq.Grid(dims), x, "aniso") == pytest.approx(float(golden[f"stencil_{key}_tv_aniso"]),
+                                                                        rel=1e-13)
