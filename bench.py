@@ -210,6 +210,9 @@ def run_ours(args):
     if ws > 1:
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    last = D.read_report(wsp)
+    names = ["setup", "div", "newton", "dual", "final"]
+    phases = {nm: {"ms": last.phase_ns[i] / 1e6, "visits": int(last.phase_count[i])} for i, nm in enumerate(names)}
     ms = float(np.mean(step_ms))
     if ws > 1:
         t = torch.tensor([ms], device=dev)
@@ -273,6 +276,8 @@ def run_ours(args):
             "gpu_launches": args.steps,
             "clocks": sampler.summary(),
             "wall_s_timed_region": wall,
+            "prox_phases_last_step": phases,
+            "newton_steps_last_step": int(last.newton_iterations),
             "step_ms": step_ms,
         }
         print(json.dumps(line), flush=True)

@@ -109,6 +109,11 @@ typedef struct {
   double newton_residual; /* residual of the last wpm_box call */
   int32_t last_newton_iterations;
   int32_t last_newton_converged;
+  /* device-side phase timeline (globaltimer at every grid barrier, taken by the
+   * last-arriving block): nanoseconds and visits per phase
+   * [setup, div, newton, dual, final, unused] */
+  double phase_ns[6];
+  int32_t phase_count[6];
 } bq_wtv_report;
 
 int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream);

@@ -86,6 +86,8 @@ class WtvReport(C.Structure):
         ("newton_residual", C.c_double),
         ("last_newton_iterations", C.c_int32),
         ("last_newton_converged", C.c_int32),
+        ("phase_ns", C.c_double * 6),
+        ("phase_count", C.c_int32 * 6),
     ]
 
 

@@ -46,6 +46,9 @@ struct ProxCtl {
   double t, mom, rel, best_res, last_res, pad2_;
   double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
   double chol[BQ_MAX_RANK * BQ_MAX_RANK];
+  unsigned long long t_last;
+  unsigned long long phase_ns[6];
+  int phase_cnt[6];
 };
 
 template <typename T>
@@ -145,6 +148,16 @@ __device__ __noinline__ bool lu_solve(double* a, int r, double* b) {
 template <typename T, int R>
 __device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const double* red) {
   ProxCtl* c = A.ctl;
+  {
+    const unsigned long long now = global_ns();
+    if (phase == PH_SETUP) {
+      for (int i = 0; i < 6; ++i) c->phase_ns[i] = 0, c->phase_cnt[i] = 0;
+    } else {
+      c->phase_ns[phase] += now - c->t_last;
+      c->phase_cnt[phase] += 1;
+    }
+    c->t_last = now;
+  }
   const bool diag = A.d != nullptr;
   auto start_newton = [&]() {
     c->newton_it = 0;
@@ -309,6 +322,7 @@ __device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const d
       rp->last_newton_converged = c->last_newton_conv;
       if (A.beta_io)
         for (int i = 0; i < R; ++i) A.beta_io[i] = c->beta[i];
+      for (int i = 0; i < 6; ++i) rp->phase_ns[i] = (double)c->phase_ns[i], rp->phase_count[i] = c->phase_cnt[i];
       c->phase = PH_DONE;
       return;
     }
