@@ -212,7 +212,8 @@ def run_ours(args):
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     last = D.read_report(wsp)
     names = ["setup", "div", "newton", "dual", "final"]
-    phases = {nm: {"ms": last.phase_ns[i] / 1e6, "visits": int(last.phase_count[i])} for i, nm in enumerate(names)}
+    phases = {nm: {"ms": last.phase_ns[i] / 1e6, "work_ms": last.phase_work_ns[i] / 1e6,
+                   "visits": int(last.phase_count[i])} for i, nm in enumerate(names)}
     ms = float(np.mean(step_ms))
     if ws > 1:
         t = torch.tensor([ms], device=dev)

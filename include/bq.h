@@ -114,6 +114,9 @@ typedef struct {
    * [setup, div, newton, dual, final, unused] */
   double phase_ns[6];
   int32_t phase_count[6];
+  /* part of phase_ns spent before the LAST block arrived at the barrier
+   * (i.e. the slowest block's work); the rest is barrier latency */
+  double phase_work_ns[6];
 } bq_wtv_report;
 
 int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream);

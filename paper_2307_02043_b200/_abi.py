@@ -88,6 +88,7 @@ class WtvReport(C.Structure):
         ("last_newton_converged", C.c_int32),
         ("phase_ns", C.c_double * 6),
         ("phase_count", C.c_int32 * 6),
+        ("phase_work_ns", C.c_double * 6),
     ]
 
 

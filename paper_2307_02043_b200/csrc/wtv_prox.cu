@@ -13,48 +13,54 @@
 // the reference's tau*I exactly).
 //
 // Design (B200-first):
-//  * The whole solve is one launch.  Blocks (all co-resident) walk a fixed
-//    phase machine; between phases they meet at a device-wide barrier whose
-//    LAST arriving block reduces the per-block partial sums in block order
-//    (deterministic, no float atomics) and runs the scalar controller (r x r
-//    Cholesky / LU, Newton accept/stop, FISTA t-sequence, rel-change test).
-//    No host round trip, no per-iteration launches.
+//  * The whole solve is one launch.  Blocks (all co-resident, one or two per
+//    SM) walk a fixed phase machine.  Between phases they meet at a
+//    device-wide barrier whose LAST arriving block reduces the per-block
+//    partial sums in block order (deterministic, no float atomics) and
+//    publishes the totals; every block then runs the scalar controller
+//    (r x r Cholesky / LU, Newton accept/stop, FISTA t-sequence, rel-change
+//    test) redundantly on its own shared-memory copy of the control state, so
+//    no block ever waits on serialized global control traffic.
 //  * Phases per FGP iteration:  DIV (z-marching stencil: a = v - reg D^-1
 //    div(P_bar), partial U^T D^-1 div)  ->  NEWTON x (1 + steps) (pointwise
-//    phi / generalized-Jacobian partials over a, d, U)  ->  DUAL (z-marching:
-//    q = clamp(...) evaluated on the fly, forward differences, projection,
-//    momentum, in-place P/P_bar update, ||P_next-P||^2, ||P||^2 partials).
-//  * Stencil phases: a warp owns 32 consecutive x (coalesced), 8 warps own 8
-//    rows y, and each thread marches a z-chunk carrying the z-1 (DIV) / z+1
-//    (DUAL) neighbour in registers; x+1 comes by warp shuffle.
+//    phi / generalized-Jacobian partials over a, d, U; 16-byte vector loads)
+//    ->  DUAL (z-marching: q = clamp(...) evaluated on the fly, forward
+//    differences, projection, momentum, in-place P/P_bar update,
+//    ||P_next-P||^2 and ||P||^2 partials).
+//  * Stencil phases: a warp owns 32 consecutive x (coalesced), the block's
+//    warps own consecutive rows y, and each block marches one contiguous,
+//    equal-length run of (tile, z) planes carrying the z-1 (DIV) / z+1 (DUAL)
+//    neighbour in registers; x+1 comes by warp shuffle, y+1 through L1.
 //  * Fields: T (f32 or f64); every reduction and scalar in f64.
-#include <cooperative_groups.h>
+#include <algorithm>
 
 #include "common.cuh"
 
 namespace bq {
 namespace {
 
-constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int TX = 32;
 
 enum Phase : int { PH_SETUP = 0, PH_DIV = 1, PH_NEWTON = 2, PH_DUAL = 3, PH_FINAL = 4, PH_DONE = 5 };
 
-struct ProxCtl {
-  int phase, abort, div_src, final_mode;
-  int it, newton_it, newton_total, converged;
-  int status, last_newton_it, last_newton_conv, pad_;
-  double t, mom, rel, best_res, last_res, pad2_;
+// Control state; one copy per block in shared memory.
+struct Ctl {
+  int phase, div_src, final_mode, it;
+  int newton_it, newton_total, converged, status;
+  int last_newton_it, last_newton_conv, abort, pad_;
+  double t, mom, rel, best_res, last_res;
   double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
   double chol[BQ_MAX_RANK * BQ_MAX_RANK];
   unsigned long long t_last;
   unsigned long long phase_ns[6];
+  unsigned long long phase_work_ns[6];
   int phase_cnt[6];
 };
 
 template <typename T>
 struct ProxArgs {
   int ndim, mode, rank, sign, accelerated, max_iter, newton_max_iter, wpm_only;
-  int K1, K2, K3;
+  int K1, K2, K3, vec, vx;
   long long N, plane;
   double tau, reg, step, eps, newton_eps, lo, hi;
   const T* lo_arr;
@@ -69,9 +75,10 @@ struct ProxArgs {
   double* beta_io;
   bq_wtv_report* report;
   double* partials;
+  double* red;  // published totals of the last barrier (kMaxVals)
   unsigned* bar;
-  ProxCtl* ctl;
-  int zc, ntx, nty, items;
+  int ntx, nty;
+  long long tile_planes;  // ntx * nty * K3
 };
 
 template <int R>
@@ -145,47 +152,36 @@ __device__ __noinline__ bool lu_solve(double* a, int r, double* b) {
   return true;
 }
 
+// Runs in thread 0 of EVERY block on its shared copy `c` (identical inputs ->
+// identical decisions).  `writer` (block 0) also publishes report and beta*.
 template <typename T, int R>
-__device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const double* red) {
-  ProxCtl* c = A.ctl;
+__device__ __noinline__ void controller(const ProxArgs<T>& A, Ctl& c, int phase, const double* red, bool writer) {
+  const bool diag = A.d != nullptr;
   {
     const unsigned long long now = global_ns();
     if (phase == PH_SETUP) {
-      for (int i = 0; i < 6; ++i) c->phase_ns[i] = 0, c->phase_cnt[i] = 0;
+      for (int i = 0; i < 6; ++i) c.phase_ns[i] = 0, c.phase_work_ns[i] = 0, c.phase_cnt[i] = 0;
     } else {
-      c->phase_ns[phase] += now - c->t_last;
-      c->phase_cnt[phase] += 1;
+      const unsigned long long arrive = __double_as_longlong(red[kMaxVals - 1]);
+      c.phase_ns[phase] += now - c.t_last;
+      if (arrive > c.t_last && arrive <= now) c.phase_work_ns[phase] += arrive - c.t_last;
+      c.phase_cnt[phase] += 1;
     }
-    c->t_last = now;
+    c.t_last = now;
   }
-  const bool diag = A.d != nullptr;
-  auto start_newton = [&]() {
-    c->newton_it = 0;
-    c->best_res = INFINITY;
-    for (int i = 0; i < R; ++i) c->best_beta[i] = c->beta[i];
-    c->phase = PH_NEWTON;
-  };
   auto finish_newton = [&](int converged) {
-    for (int i = 0; i < R; ++i) c->beta[i] = c->best_beta[i];
-    c->newton_total += c->newton_it;
-    c->last_newton_it = c->newton_it;
-    c->last_newton_conv = converged;
-    c->last_res = (R == 0) ? 0.0 : c->best_res;
-    if (c->final_mode) {
-      c->phase = PH_FINAL;
+    for (int i = 0; i < R; ++i) c.beta[i] = c.best_beta[i];
+    c.newton_total += c.newton_it;
+    c.last_newton_it = c.newton_it;
+    c.last_newton_conv = converged;
+    c.last_res = (R == 0) ? 0.0 : c.best_res;
+    if (c.final_mode) {
+      c.phase = PH_FINAL;
     } else {
-      double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c->t * c->t));
-      c->mom = A.accelerated ? (c->t - 1.0) / tn : 0.0;
-      c->phase = PH_DUAL;
+      const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c.t * c.t));
+      c.mom = A.accelerated ? (c.t - 1.0) / tn : 0.0;
+      c.phase = PH_DUAL;
     }
-  };
-  auto after_div = [&]() {
-    if (R == 0) {
-      c->newton_it = 0;
-      finish_newton(1);
-      return;
-    }
-    start_newton();
   };
 
   switch (phase) {
@@ -195,46 +191,54 @@ __device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const d
       int k = 0;
       for (int i = 0; i < R; ++i)
         for (int j = 0; j <= i; ++j, ++k) {
-          double g = diag ? red[k] : red[k] / A.tau;
-          double val = (i == j ? 1.0 : 0.0) + A.sign * g;
+          const double g = diag ? red[k] : red[k] / A.tau;
+          const double val = (i == j ? 1.0 : 0.0) + A.sign * g;
           cap[i * R + j] = val;
           cap[j * R + i] = val;
         }
-      c->status = 0;
-      c->abort = 0;
+      c.status = 0;
+      c.abort = 0;
       if (R > 0 && !chol_factor(cap, R)) {
-        c->status = BQ_ENOTPD;
-        c->phase = PH_DONE;
-        A.report->status = BQ_ENOTPD;
+        c.status = BQ_ENOTPD;
+        c.phase = PH_DONE;
+        if (writer) A.report->status = BQ_ENOTPD;
         return;
       }
-      for (int i = 0; i < R * R; ++i) c->chol[i] = cap[i];
+      for (int i = 0; i < R * R; ++i) c.chol[i] = cap[i];
       for (int i = 0; i < R; ++i) {
-        c->beta[i] = A.beta_io ? A.beta_io[i] : 0.0;
-        c->gw[i] = 0.0;
+        c.beta[i] = A.beta_io ? A.beta_io[i] : 0.0;
+        c.gw[i] = 0.0;
       }
-      c->t = 1.0;
-      c->mom = 0.0;
-      c->it = 1;
-      c->newton_total = 0;
-      c->converged = 0;
-      c->rel = INFINITY;
-      c->last_newton_it = 0;
-      c->last_newton_conv = 1;
-      c->last_res = 0.0;
+      c.t = 1.0;
+      c.mom = 0.0;
+      c.it = 1;
+      c.newton_total = 0;
+      c.converged = 0;
+      c.rel = INFINITY;
+      c.last_newton_it = 0;
+      c.last_newton_conv = 1;
+      c.last_res = 0.0;
       const bool single = A.wpm_only || A.reg == 0.0;
-      c->div_src = single ? 1 : 0;  // 1: P (final), 0: P_bar
-      c->final_mode = single ? 1 : 0;
-      c->phase = PH_DIV;
+      c.div_src = single ? 1 : 0;  // 1: P (final prox), 0: P_bar
+      c.final_mode = single ? 1 : 0;
+      c.phase = PH_DIV;
       return;
     }
     case PH_DIV: {
       // Woodbury coefficient: coef = cap^-1 U^T D^-1 div ; gw = reg * coef
       double coef[BQ_MAX_RANK > 0 ? BQ_MAX_RANK : 1];
       for (int i = 0; i < R; ++i) coef[i] = diag ? red[i] : red[i] / A.tau;
-      if (R > 0) chol_solve(c->chol, R, coef);
-      for (int i = 0; i < R; ++i) c->gw[i] = (A.reg == 0.0 || A.wpm_only) ? 0.0 : A.reg * coef[i];
-      after_div();
+      if (R > 0) chol_solve(c.chol, R, coef);
+      for (int i = 0; i < R; ++i) c.gw[i] = (A.reg == 0.0 || A.wpm_only) ? 0.0 : A.reg * coef[i];
+      if (R == 0) {
+        c.newton_it = 0;
+        finish_newton(1);
+        return;
+      }
+      c.newton_it = 0;
+      c.best_res = INFINITY;
+      for (int i = 0; i < R; ++i) c.best_beta[i] = c.beta[i];
+      c.phase = PH_NEWTON;
       return;
     }
     case PH_NEWTON: {
@@ -242,19 +246,19 @@ __device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const d
       double phi[BQ_MAX_RANK > 0 ? BQ_MAX_RANK : 1];
       double ss = 0.0;
       for (int i = 0; i < R; ++i) {
-        phi[i] = red[i] + c->beta[i];
+        phi[i] = red[i] + c.beta[i];
         ss += phi[i] * phi[i];
       }
-      double res = sqrt(ss);
-      if (res < c->best_res) {
-        c->best_res = res;
-        for (int i = 0; i < R; ++i) c->best_beta[i] = c->beta[i];
+      const double res = sqrt(ss);
+      if (res < c.best_res) {
+        c.best_res = res;
+        for (int i = 0; i < R; ++i) c.best_beta[i] = c.beta[i];
       }
       if (res <= A.newton_eps) {
         finish_newton(1);
         return;
       }
-      if (c->newton_it == A.newton_max_iter) {
+      if (c.newton_it == A.newton_max_iter) {
         finish_newton(0);
         return;
       }
@@ -262,8 +266,8 @@ __device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const d
       int k = R;
       for (int i = 0; i < R; ++i)
         for (int j = 0; j <= i; ++j, ++k) {
-          double g = diag ? red[k] : red[k] / A.tau;
-          double val = (i == j ? 1.0 : 0.0) + A.sign * g;
+          const double g = diag ? red[k] : red[k] / A.tau;
+          const double val = (i == j ? 1.0 : 0.0) + A.sign * g;
           h[i * R + j] = val;
           h[j * R + i] = val;
         }
@@ -283,51 +287,57 @@ __device__ __noinline__ void controller(const ProxArgs<T>& A, int phase, const d
         for (int i = 0; i < R; ++i) hs[i * R + i] += 1e-8 * ninf, st[i] = phi[i];
         lu_solve(hs, R, st);
       }
-      for (int i = 0; i < R; ++i) c->beta[i] -= st[i];
-      c->newton_it += 1;
-      c->phase = PH_NEWTON;
+      for (int i = 0; i < R; ++i) c.beta[i] -= st[i];
+      c.newton_it += 1;
+      c.phase = PH_NEWTON;
       return;
     }
     case PH_DUAL: {
       // dual_tv_solver.py:226-239
-      double num = sqrt(red[0]), den = sqrt(red[1]);
-      double rel = (num == 0.0) ? 0.0 : (den > 0.0 ? num / den : INFINITY);
-      c->rel = rel;
+      const double num = sqrt(red[0]), den = sqrt(red[1]);
+      const double rel = (num == 0.0) ? 0.0 : (den > 0.0 ? num / den : INFINITY);
+      c.rel = rel;
       bool stop = false;
       if (rel < A.eps) {
-        c->converged = 1;
+        c.converged = 1;
         stop = true;
       } else {
-        c->t = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c->t * c->t));
-        if (c->it >= A.max_iter) stop = true;
-        else c->it += 1;
+        c.t = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c.t * c.t));
+        if (c.it >= A.max_iter) stop = true;
+        else c.it += 1;
       }
       if (stop) {
-        c->div_src = 1;
-        c->final_mode = 1;
+        c.div_src = 1;
+        c.final_mode = 1;
       }
-      c->phase = PH_DIV;
+      c.phase = PH_DIV;
       return;
     }
     case PH_FINAL: {
-      bq_wtv_report* rp = A.report;
-      const bool single = A.wpm_only || A.reg == 0.0;
-      rp->iterations = single ? 1 : c->it;
-      rp->converged = single ? 1 : c->converged;
-      rp->rel_change = single ? 0.0 : c->rel;
-      rp->newton_iterations = c->newton_total;
-      rp->status = 0;
-      rp->newton_residual = c->last_res;
-      rp->last_newton_iterations = c->last_newton_it;
-      rp->last_newton_converged = c->last_newton_conv;
-      if (A.beta_io)
-        for (int i = 0; i < R; ++i) A.beta_io[i] = c->beta[i];
-      for (int i = 0; i < 6; ++i) rp->phase_ns[i] = (double)c->phase_ns[i], rp->phase_count[i] = c->phase_cnt[i];
-      c->phase = PH_DONE;
+      if (writer) {
+        bq_wtv_report* rp = A.report;
+        const bool single = A.wpm_only || A.reg == 0.0;
+        rp->iterations = single ? 1 : c.it;
+        rp->converged = single ? 1 : c.converged;
+        rp->rel_change = single ? 0.0 : c.rel;
+        rp->newton_iterations = c.newton_total;
+        rp->status = 0;
+        rp->newton_residual = c.last_res;
+        rp->last_newton_iterations = c.last_newton_it;
+        rp->last_newton_converged = c.last_newton_conv;
+        if (A.beta_io)
+          for (int i = 0; i < R; ++i) A.beta_io[i] = c.beta[i];
+        for (int i = 0; i < 6; ++i) {
+          rp->phase_ns[i] = (double)c.phase_ns[i];
+          rp->phase_work_ns[i] = (double)c.phase_work_ns[i];
+          rp->phase_count[i] = c.phase_cnt[i];
+        }
+      }
+      c.phase = PH_DONE;
       return;
     }
     default:
-      c->phase = PH_DONE;
+      c.phase = PH_DONE;
   }
 }
 
@@ -339,62 +349,338 @@ __device__ __forceinline__ T clampv(T z, T lo, T hi) {
   return fmin(fmax(z, lo), hi);  // np.clip == minimum(maximum(z, lo), hi)
 }
 
+// Reciprocal: correctly rounded single-instruction-sequence in f32 (no IEEE
+// division subroutine on the hot path); exact division in f64.
+__device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+
+// Isotropic dual-ball projection p / max(||p||, 1) (tv_ops.py:177-179).
+__device__ __forceinline__ void ball(float (&w)[3], float ss) {
+  if (ss > 1.0f) {
+    const float s = rsqrtf(ss);
+    w[0] *= s, w[1] *= s, w[2] *= s;
+  }
+}
+__device__ __forceinline__ void ball(double (&w)[3], double ss) {
+  const double den = fmax(sqrt(ss), 1.0);
+  w[0] /= den, w[1] /= den, w[2] /= den;
+}
+
+// 4 consecutive elements; 16-byte vector loads (fp32) / 2 x 16 (fp64).
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  static __device__ __forceinline__ void ro(const float* p, float (&o)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+  }
+  static __device__ __forceinline__ void rw(const float* p, float (&o)[4]) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&o)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+};
+template <>
+struct Vec4<double> {
+  static __device__ __forceinline__ void ro(const double* p, double (&o)[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    o[0] = a.x, o[1] = a.y, o[2] = b.x, o[3] = b.y;
+  }
+  static __device__ __forceinline__ void rw(const double* p, double (&o)[4]) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *(reinterpret_cast<const double2*>(p) + 1);
+    o[0] = a.x, o[1] = a.y, o[2] = b.x, o[3] = b.y;
+  }
+  static __device__ __forceinline__ void st(double* p, const double (&o)[4]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(o[0], o[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(o[2], o[3]);
+  }
+};
+
+// Per-voxel shift point (wpm.py:145-158 with W^-1 folded in):
+//   wv = a + sign (U.gw)/e ;  z = wv - sign (U.beta)/e
 template <typename T, int R>
-struct Voxel {
-  // shift point and clamp at voxel j (wpm.py:145-158 with W^-1 folded in):
-  //   wv = a + sign (U.gw)/e ;  z = wv - sign (U.beta)/e ;  q = clamp(z)
-  const ProxArgs<T>& A;
-  const T* gw;
-  const T* beta;
-  __device__ __forceinline__ void eval(long long j, T& wv, T& z, T& e, T (&u)[R > 0 ? R : 1]) const {
-    const T av = A.a[j];
-    e = A.d ? __ldg(A.d + j) : (T)A.tau;
+__device__ __forceinline__ void shift(T av, T e, const T (&u)[R > 0 ? R : 1], const T* gw, const T* beta, T sg,
+                                      T& wv, T& z) {
+  if (R > 0) {
     T uw = 0, ub = 0;
 #pragma unroll
     for (int c = 0; c < R; ++c) {
-      u[c] = __ldg(A.U + (long long)c * A.N + j);
       uw += u[c] * gw[c];
       ub += u[c] * beta[c];
     }
-    if (R > 0) {
-      const T sg = (T)A.sign;
-      wv = av + sg * uw / e;
-      z = wv - sg * ub / e;
-    } else {
-      wv = av;
-      z = av;
-    }
+    const T ie = rcp(e);
+    wv = av + sg * uw * ie;
+    z = wv - sg * ub * ie;
+  } else {
+    wv = av;
+    z = av;
   }
-  __device__ __forceinline__ T bound_lo(long long j) const { return A.lo_arr ? __ldg(A.lo_arr + j) : (T)A.lo; }
-  __device__ __forceinline__ T bound_hi(long long j) const { return A.hi_arr ? __ldg(A.hi_arr + j) : (T)A.hi; }
-  __device__ __forceinline__ T q(long long j) const {
-    T wv, z, e, u[R > 0 ? R : 1];
-    eval(j, wv, z, e, u);
-    return clampv(z, bound_lo(j), bound_hi(j));
+}
+
+template <typename T, int R>
+struct QEval {
+  const T* __restrict__ a;
+  const T* __restrict__ d;
+  const T* __restrict__ U;
+  const T* __restrict__ lo_arr;
+  const T* __restrict__ hi_arr;
+  long long N;
+  T tau, lo, hi, sg;
+  const T* gz;  // gw - beta: z = a + sign (U.gz)/e
+  __device__ __forceinline__ T operator()(long long j) const {
+    T z = a[j];
+    if (R > 0) {
+      const T e = d ? __ldg(d + j) : tau;
+      T uz = 0;
+#pragma unroll
+      for (int c = 0; c < R; ++c) uz += __ldg(U + (long long)c * N + j) * gz[c];
+      z += sg * uz * rcp(e);
+    }
+    return clampv(z, lo_arr ? __ldg(lo_arr + j) : lo, hi_arr ? __ldg(hi_arr + j) : hi);
+  }
+  // four consecutive voxels j..j+3 (j % 4 == 0, 16-byte aligned fields)
+  __device__ __forceinline__ void q4(long long j, T (&q)[4]) const {
+    Vec4<T>::rw(a + j, q);
+    if (R > 0) {
+      T e[4], uz[4] = {0, 0, 0, 0};
+      if (d) Vec4<T>::ro(d + j, e);
+      else e[0] = e[1] = e[2] = e[3] = tau;
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        T u[4];
+        Vec4<T>::ro(U + (long long)c * N + j, u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) uz[k] += u[k] * gz[c];
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) q[k] += sg * uz[k] * rcp(e[k]);
+    }
+    T l[4], h[4];
+    if (lo_arr) Vec4<T>::ro(lo_arr + j, l);
+    else l[0] = l[1] = l[2] = l[3] = lo;
+    if (hi_arr) Vec4<T>::ro(hi_arr + j, h);
+    else h[0] = h[1] = h[2] = h[3] = hi;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) q[k] = clampv(q[k], l[k], h[k]);
   }
 };
+
+// ---------------------------------------------------------------------------
+// Stencil phases, x-vectorised: each lane owns 4 consecutive x (16-byte
+// loads), a warp 128 x, the block TY rows; used when K1 % 4 == 0.
+// ---------------------------------------------------------------------------
+constexpr unsigned FULL = 0xffffffffu;
+constexpr int TXV = 128;
+
+// DIV: a = v - reg D^-1 div(F) ; acc[c] += U_c . D^-1 div(F)
+template <typename T, int R, int TY, int NACC>
+__device__ __forceinline__ void div_vec(const ProxArgs<T>& A, const T* __restrict__ F0, long long seg_begin,
+                                        long long seg_end, int lane, int warp, double (&acc)[NACC]) {
+  const long long N = A.N, plane = A.plane;
+  const T* __restrict__ F1 = F0 + N;
+  const T* __restrict__ F2 = F0 + 2 * N;
+  T* __restrict__ Aout = A.a;
+  const bool diag = A.d != nullptr;
+  const T reg = (T)A.reg, tauT = (T)A.tau;
+  const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
+  long long pos = seg_begin;
+  while (pos < seg_end) {
+    const long long tile = pos / K3;
+    const int z0 = (int)(pos - tile * K3);
+    const int z1 = (int)min((long long)K3, z0 + (seg_end - pos));
+    pos += z1 - z0;
+    const int x0 = (int)(tile % A.ntx) * TXV;
+    const int xb = x0 + 4 * lane;
+    const int y = (int)(tile / A.ntx) * TY + warp;
+    if (y >= K2) continue;  // warp-uniform
+    const bool act = xb < K1;
+    long long j = (long long)z0 * plane + (long long)y * K1 + xb;
+    T prev3[4] = {0, 0, 0, 0};
+    if (act && nd >= 3 && z0 > 0) Vec4<T>::rw(F2 + j - plane, prev3);
+#pragma unroll 2
+    for (int z = z0; z < z1; ++z, j += plane) {
+      T c1[4] = {0, 0, 0, 0};
+      if (act) Vec4<T>::rw(F0 + j, c1);
+      T left = __shfl_up_sync(FULL, c1[3], 1);
+      if (lane == 0) left = (act && xb > 0) ? F0[j - 1] : (T)0;
+      if (!act) continue;
+      // tv_ops.py:122-133 per dimension, summed in dimension order (:151-159)
+      T dv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const T lk = (k == 0) ? left : c1[k - 1];
+        dv[k] = (xb + k < K1 - 1 ? -c1[k] : (T)0) + (xb + k > 0 ? lk : (T)0);
+      }
+      if (nd >= 2) {
+        T c2[4], l2[4] = {0, 0, 0, 0};
+        Vec4<T>::rw(F1 + j, c2);
+        if (y > 0) Vec4<T>::rw(F1 + j - K1, l2);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) dv[k] += (y < K2 - 1 ? -c2[k] : (T)0) + l2[k];
+      }
+      if (nd >= 3) {
+        T c3[4];
+        Vec4<T>::rw(F2 + j, c3);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          dv[k] += (z < K3 - 1 ? -c3[k] : (T)0) + (z > 0 ? prev3[k] : (T)0);
+          prev3[k] = c3[k];
+        }
+      }
+      T e[4], vv[4], out[4];
+      if (diag) Vec4<T>::ro(A.d + j, e);
+      else e[0] = e[1] = e[2] = e[3] = tauT;
+      Vec4<T>::ro(A.v + j, vv);
+      T de[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        de[k] = dv[k] * rcp(e[k]);
+        out[k] = vv[k] - reg * de[k];
+      }
+      Vec4<T>::st(Aout + j, out);
+#pragma unroll
+      for (int c = 0; c < R; ++c) {
+        T u[4];
+        Vec4<T>::ro(A.U + (long long)c * N + j, u);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[c] += (double)u[k] * (double)(diag ? de[k] : dv[k]);
+      }
+    }
+  }
+}
+
+// DUAL: P_next = Proj(P_bar + step D q), P_bar' = P_next + mom (P_next - P);
+// acc[0] += ||P_next - P||^2, acc[1] += ||P||^2   (dual_tv_solver.py:225-239)
+template <typename T, int R, int TY, int NACC>
+__device__ __forceinline__ void dual_vec(const ProxArgs<T>& A, const QEval<T, R>& Q, T step, T mom,
+                                         long long seg_begin, long long seg_end, int lane, int warp,
+                                         double (&acc)[NACC]) {
+  const long long N = A.N, plane = A.plane;
+  T* __restrict__ P0 = A.p;
+  T* __restrict__ PB0 = A.pb;
+  const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
+  const bool iso = A.mode == BQ_TV_ISO;
+  long long pos = seg_begin;
+  while (pos < seg_end) {
+    const long long tile = pos / K3;
+    const int z0 = (int)(pos - tile * K3);
+    const int z1 = (int)min((long long)K3, z0 + (seg_end - pos));
+    pos += z1 - z0;
+    const int x0 = (int)(tile % A.ntx) * TXV;
+    const int xb = x0 + 4 * lane;
+    const int y = (int)(tile / A.ntx) * TY + warp;
+    if (y >= K2) continue;  // warp-uniform
+    const bool act = xb < K1;
+    const bool has_y = nd >= 2 && y < K2 - 1;
+    long long j = (long long)z0 * plane + (long long)y * K1 + xb;
+    T qc[4] = {0, 0, 0, 0};
+    if (act) Q.q4(j, qc);
+#pragma unroll 1
+    for (int z = z0; z < z1; ++z, j += plane) {
+      const bool has_up = nd >= 3 && z < K3 - 1;
+      T qu[4] = {0, 0, 0, 0}, qy[4] = {0, 0, 0, 0};
+      if (act && has_up) Q.q4(j + plane, qu);
+      if (act && has_y) Q.q4(j + K1, qy);
+      T qn = __shfl_down_sync(FULL, qc[0], 1);
+      if (lane == 31) qn = (act && xb + 4 < K1) ? Q(j + 4) : (T)0;
+      if (act) {
+        T w[3][4], po[3][4];
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          if (n < nd) {
+            Vec4<T>::rw(P0 + n * N + j, po[n]);
+            Vec4<T>::rw(PB0 + n * N + j, w[n]);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const T right = (k < 3) ? qc[k + 1] : qn;
+          T g[3];
+          g[0] = (xb + k < K1 - 1) ? right - qc[k] : (T)0;
+          g[1] = has_y ? qy[k] - qc[k] : (T)0;
+          g[2] = has_up ? qu[k] - qc[k] : (T)0;
+          T wk[3];
+#pragma unroll
+          for (int n = 0; n < 3; ++n) wk[n] = (n < nd) ? w[n][k] + step * g[n] : (T)0;
+          if (iso) {
+            T ss = wk[0] * wk[0];
+            if (nd >= 2) ss += wk[1] * wk[1];
+            if (nd >= 3) ss += wk[2] * wk[2];
+            ball(wk, ss);
+          } else {
+#pragma unroll
+            for (int n = 0; n < 3; ++n) wk[n] = clampv(wk[n], (T)-1, (T)1);
+          }
+#pragma unroll
+          for (int n = 0; n < 3; ++n) {
+            if (n < nd) {
+              const T pk = (n < nd) ? po[n][k] : (T)0;
+              const T df = wk[n] - pk;
+              acc[0] += (double)df * (double)df;
+              acc[1] += (double)pk * (double)pk;
+              po[n][k] = wk[n];
+              w[n][k] = wk[n] + mom * df;
+            }
+          }
+        }
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          if (n < nd) {
+            Vec4<T>::st(P0 + n * N + j, po[n]);
+            Vec4<T>::st(PB0 + n * N + j, w[n]);
+          }
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < 4; ++k) qc[k] = qu[k];
+    }
+  }
+}
 
 // ---------------------------------------------------------------------------
 // The persistent kernel
 // ---------------------------------------------------------------------------
 template <typename T, int R>
-__global__ void __launch_bounds__(NT, 2) wtv_prox_kernel(ProxArgs<T> A) {
+struct Cfg {
+  // light variants: 512 threads x 2 blocks/SM (64 regs); heavier ones trade
+  // block size for registers so the Newton accumulators never spill
+  static constexpr bool kLight = sizeof(T) == 4 && R <= 2;
+  static constexpr int NT = kLight ? 512 : 256;
+  static constexpr int MINB = kLight ? 1 : (R <= 2 ? 2 : 1);
+  static constexpr int TY = NT / TX;
+};
+
+template <typename T, int R>
+__global__ void __launch_bounds__(Cfg<T, R>::NT, Cfg<T, R>::MINB) wtv_prox_kernel(ProxArgs<T> A) {
+  constexpr int NT = Cfg<T, R>::NT;
+  constexpr int TY = Cfg<T, R>::TY;
   constexpr int NACC = NV<R>::acc;
   __shared__ double s_red[kMaxVals];
   __shared__ double s_bv[kMaxVals];
   __shared__ double s_scr[(NT / 32) * kMaxVals];
-  __shared__ T s_gw[BQ_MAX_RANK], s_beta[BQ_MAX_RANK];
+  __shared__ Ctl s_c;
+  __shared__ T s_gw[BQ_MAX_RANK], s_beta[BQ_MAX_RANK], s_gz[BQ_MAX_RANK];
   __shared__ T s_mom;
-  __shared__ int s_phase, s_div_src, s_abort;
+  __shared__ int s_phase, s_div_src, s_flag;
 
-  GridSync gs{A.bar, A.bar + 1, gridDim.x, 0};
-  if (threadIdx.x == 0) gs.my_gen = ld_acquire_u32(A.bar + 1);
+  unsigned my_gen = 0;
+  if (threadIdx.x == 0) my_gen = ld_acquire_u32(A.bar + 1);
 
   const long long N = A.N;
   const long long stride = (long long)gridDim.x * NT;
   const long long gtid = (long long)blockIdx.x * NT + threadIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const bool diag = A.d != nullptr;
+  const T sg = (T)A.sign;
+  const T tauT = (T)A.tau;
+  // balanced contiguous run of (tile, z) planes for the stencil phases
+  const long long seg_begin = (long long)blockIdx.x * A.tile_planes / gridDim.x;
+  const long long seg_end = (long long)(blockIdx.x + 1) * A.tile_planes / gridDim.x;
 
   int phase = PH_SETUP;
   while (true) {
@@ -402,15 +688,16 @@ __global__ void __launch_bounds__(NT, 2) wtv_prox_kernel(ProxArgs<T> A) {
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     int nv = 0;
-    Voxel<T, R> vox{A, s_gw, s_beta};
 
     if (phase == PH_SETUP) {
       // P_bar = P (dual_tv_solver.py:215) and Gram partials U^T D^-1 U
       nv = NV<R>::gram;
       const bool copy = !(A.wpm_only || A.reg == 0.0);
+      const T* __restrict__ Pin = A.p;
+      T* __restrict__ PBo = A.pb;
       for (long long j = gtid; j < N; j += stride) {
         if (copy)
-          for (int n = 0; n < A.ndim; ++n) A.pb[n * N + j] = A.p[n * N + j];
+          for (int n = 0; n < A.ndim; ++n) PBo[n * N + j] = Pin[n * N + j];
         if (R > 0) {
           T u[R > 0 ? R : 1];
 #pragma unroll
@@ -420,130 +707,177 @@ __global__ void __launch_bounds__(NT, 2) wtv_prox_kernel(ProxArgs<T> A) {
 #pragma unroll
           for (int c = 0; c < R; ++c)
 #pragma unroll
-            for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += diag ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
+            for (int c2 = 0; c2 <= c; ++c2, ++k)
+              acc[k] += diag ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
         }
       }
     } else if (phase == PH_DIV) {
       nv = R;
+      T* __restrict__ Aout = A.a;
+      const T* __restrict__ V = A.v;
       if (A.wpm_only || A.reg == 0.0) {
-        for (long long j = gtid; j < N; j += stride) A.a[j] = A.v[j];
+        for (long long j = gtid; j < N; j += stride) Aout[j] = V[j];
+      } else if (A.vx) {
+        div_vec<T, R, TY, NACC>(A, s_div_src ? A.p : A.pb, seg_begin, seg_end, lane, warp, acc);
       } else {
-        const T* __restrict__ F = s_div_src ? A.p : A.pb;
+        const T* __restrict__ F0 = s_div_src ? A.p : A.pb;
+        const T* __restrict__ F1 = F0 + N;
+        const T* __restrict__ F2 = F0 + 2 * N;
+        const T* __restrict__ Dd = A.d;
+        const T* __restrict__ Uu = A.U;
         const T reg = (T)A.reg;
-        for (int item = blockIdx.x; item < A.items; item += gridDim.x) {
-          const int tx = item % A.ntx, rest = item / A.ntx;
-          const int ty = rest % A.nty, tz = rest / A.nty;
-          const int x = tx * TX + lane, y = ty * TY + warp;
-          const int z0 = tz * A.zc, z1 = min(z0 + A.zc, A.K3);
-          if (x >= A.K1 || y >= A.K2) continue;
-          long long j = (long long)z0 * A.plane + (long long)y * A.K1 + x;
-          T prev3 = 0;
-          if (A.ndim >= 3 && z0 > 0) prev3 = F[2 * N + j - A.plane];
+        const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
+        long long pos = seg_begin;
+        while (pos < seg_end) {
+          const long long tile = pos / K3;
+          const int z0 = (int)(pos - tile * K3);
+          const int z1 = (int)min((long long)K3, z0 + (seg_end - pos));
+          pos += z1 - z0;
+          const int x = (int)(tile % A.ntx) * TX + lane;
+          const int y = (int)(tile / A.ntx) * TY + warp;
+          if (x >= K1 || y >= K2) continue;
+          long long j = (long long)z0 * A.plane + (long long)y * K1 + x;
+          T prev3 = (nd >= 3 && z0 > 0) ? F2[j - A.plane] : (T)0;
+#pragma unroll 2
           for (int z = z0; z < z1; ++z, j += A.plane) {
             // tv_ops.py:122-133 per dimension, dual_divergence :151-159 summed in order
-            const T c1 = F[j];
-            T div = (x < A.K1 - 1 ? -c1 : (T)0) + (x > 0 ? F[j - 1] : (T)0);
-            if (A.ndim >= 2) {
-              const T c2 = F[N + j];
-              div += (y < A.K2 - 1 ? -c2 : (T)0) + (y > 0 ? F[N + j - A.K1] : (T)0);
+            const T c1 = F0[j];
+            const T l1 = x > 0 ? F0[j - 1] : (T)0;
+            T dv = (x < K1 - 1 ? -c1 : (T)0) + l1;
+            if (nd >= 2) {
+              const T c2 = F1[j];
+              const T l2 = y > 0 ? F1[j - K1] : (T)0;
+              dv += (y < K2 - 1 ? -c2 : (T)0) + l2;
             }
-            if (A.ndim >= 3) {
-              const T c3 = F[2 * N + j];
-              div += (z < A.K3 - 1 ? -c3 : (T)0) + (z > 0 ? prev3 : (T)0);
+            if (nd >= 3) {
+              const T c3 = F2[j];
+              dv += (z < K3 - 1 ? -c3 : (T)0) + (z > 0 ? prev3 : (T)0);
               prev3 = c3;
             }
-            const T e = diag ? __ldg(A.d + j) : (T)A.tau;
-            const T de = div / e;
-            A.a[j] = __ldg(A.v + j) - reg * de;
+            const T e = diag ? __ldg(Dd + j) : tauT;
+            const T de = dv * rcp(e);
+            Aout[j] = __ldg(V + j) - reg * de;
 #pragma unroll
-            for (int c = 0; c < R; ++c) acc[c] += (double)__ldg(A.U + (long long)c * N + j) * (double)(diag ? de : div);
+            for (int c = 0; c < R; ++c) acc[c] += (double)__ldg(Uu + (long long)c * N + j) * (double)(diag ? de : dv);
           }
         }
       }
     } else if (phase == PH_NEWTON) {
       // phi(beta) partials U^T (wv - clamp(z)) and U_A^T D_A^-1 U_A (wpm.py:150-167)
       nv = NV<R>::newton;
-      constexpr int UN = 2;
-      for (long long j0 = gtid; j0 < N; j0 += stride * UN) {
+      const T* __restrict__ Aa = A.a;
+      auto body = [&](T av, T e, const T (&u)[R > 0 ? R : 1], T lo, T hi) {
+        T wv, z;
+        shift<T, R>(av, e, u, s_gw, s_beta, sg, wv, z);
+        const T dl = wv - clampv(z, lo, hi);
 #pragma unroll
-        for (int uu = 0; uu < UN; ++uu) {
-          const long long j = j0 + uu * stride;
-          if (j < N) {
-            T wv, z, e, u[R > 0 ? R : 1];
-            vox.eval(j, wv, z, e, u);
-            const T lo = vox.bound_lo(j), hi = vox.bound_hi(j);
-            const T dl = wv - clampv(z, lo, hi);
+        for (int c = 0; c < R; ++c) acc[c] += (double)(u[c] * dl);
+        if (z > lo && z < hi) {
+          int k = R;
 #pragma unroll
-            for (int c = 0; c < R; ++c) acc[c] += (double)(u[c] * dl);
-            if (z > lo && z < hi) {
-              int k = R;
+          for (int c = 0; c < R; ++c)
 #pragma unroll
-              for (int c = 0; c < R; ++c)
+            for (int c2 = 0; c2 <= c; ++c2, ++k)
+              acc[k] += diag ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
+        }
+      };
+      if (A.vec) {
+        const long long N4 = N >> 2;
+#pragma unroll 2
+        for (long long q4 = gtid; q4 < N4; q4 += stride) {
+          const long long j = q4 << 2;
+          T av[4], e[4], u[R > 0 ? R : 1][4], lo[4], hi[4];
+          Vec4<T>::rw(Aa + j, av);
+          if (diag) Vec4<T>::ro(A.d + j, e);
+          else e[0] = e[1] = e[2] = e[3] = tauT;
 #pragma unroll
-                for (int c2 = 0; c2 <= c; ++c2, ++k)
-                  acc[k] += diag ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
-            }
+          for (int c = 0; c < R; ++c) Vec4<T>::ro(A.U + (long long)c * N + j, u[c]);
+          if (A.lo_arr) Vec4<T>::ro(A.lo_arr + j, lo);
+          else lo[0] = lo[1] = lo[2] = lo[3] = (T)A.lo;
+          if (A.hi_arr) Vec4<T>::ro(A.hi_arr + j, hi);
+          else hi[0] = hi[1] = hi[2] = hi[3] = (T)A.hi;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            T uk[R > 0 ? R : 1];
+#pragma unroll
+            for (int c = 0; c < R; ++c) uk[c] = u[c][k];
+            body(av[k], e[k], uk, lo[k], hi[k]);
           }
+        }
+      } else {
+        for (long long j = gtid; j < N; j += stride) {
+          T u[R > 0 ? R : 1];
+#pragma unroll
+          for (int c = 0; c < R; ++c) u[c] = __ldg(A.U + (long long)c * N + j);
+          body(Aa[j], diag ? __ldg(A.d + j) : tauT, u, A.lo_arr ? __ldg(A.lo_arr + j) : (T)A.lo,
+               A.hi_arr ? __ldg(A.hi_arr + j) : (T)A.hi);
         }
       }
     } else if (phase == PH_DUAL) {
       // dual_tv_solver.py:225-239: P_next = Proj(P_bar + step D q), momentum
       nv = 2;
       const T step = (T)A.step, mom = s_mom;
-      T* __restrict__ P = A.p;
-      T* __restrict__ PB = A.pb;
-      for (int item = blockIdx.x; item < A.items; item += gridDim.x) {
-        const int tx = item % A.ntx, rest = item / A.ntx;
-        const int ty = rest % A.nty, tz = rest / A.nty;
-        const int x = tx * TX + lane, y = ty * TY + warp;
-        const int z0 = tz * A.zc, z1 = min(z0 + A.zc, A.K3);
-        if (y >= A.K2) continue;  // whole warp leaves together
-        const bool act = x < A.K1;
-        long long j = (long long)z0 * A.plane + (long long)y * A.K1 + x;
-        T qc = act ? vox.q(j) : (T)0;
+      T* __restrict__ P0 = A.p;
+      T* __restrict__ PB0 = A.pb;
+      const QEval<T, R> qv{A.a, A.d, A.U, A.lo_arr, A.hi_arr, N, tauT, (T)A.lo, (T)A.hi, sg, s_gz};
+      const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
+      const bool iso = A.mode == BQ_TV_ISO;
+      long long pos = A.vx ? seg_end : seg_begin;
+      if (A.vx) dual_vec<T, R, TY, NACC>(A, qv, step, mom, seg_begin, seg_end, lane, warp, acc);
+      while (pos < seg_end) {
+        const long long tile = pos / K3;
+        const int z0 = (int)(pos - tile * K3);
+        const int z1 = (int)min((long long)K3, z0 + (seg_end - pos));
+        pos += z1 - z0;
+        const int x = (int)(tile % A.ntx) * TX + lane;
+        const int y = (int)(tile / A.ntx) * TY + warp;
+        if (y >= K2) continue;  // whole warp leaves together
+        const bool act = x < K1;
+        const bool has_r = x < K1 - 1;
+        const bool has_y = nd >= 2 && y < K2 - 1;
+        long long j = (long long)z0 * A.plane + (long long)y * K1 + x;
+        T qc = act ? qv(j) : (T)0;
+#pragma unroll 2
         for (int z = z0; z < z1; ++z, j += A.plane) {
-          T qu = 0;
-          const bool has_up = A.ndim >= 3 && z < A.K3 - 1;
-          if (act && has_up) qu = vox.q(j + A.plane);
+          const bool has_up = nd >= 3 && z < K3 - 1;
+          const T qu = (act && has_up) ? qv(j + A.plane) : (T)0;
+          const T qy = (act && has_y) ? qv(j + K1) : (T)0;
           T qr = __shfl_down_sync(0xffffffffu, qc, 1);
-          if (!act) continue;
-          const bool has_r = x < A.K1 - 1;
-          if (has_r && lane == 31) qr = vox.q(j + 1);
-          T g[3];
-          g[0] = has_r ? qr - qc : (T)0;
-          g[1] = (A.ndim >= 2 && y < A.K2 - 1) ? vox.q(j + A.K1) - qc : (T)0;
-          g[2] = has_up ? qu - qc : (T)0;
-          T w[3], po[3];
+          if (act) {
+            if (has_r && lane == 31) qr = qv(j + 1);
+            T g[3];
+            g[0] = has_r ? qr - qc : (T)0;
+            g[1] = has_y ? qy - qc : (T)0;
+            g[2] = has_up ? qu - qc : (T)0;
+            T w[3], po[3];
 #pragma unroll
-          for (int n = 0; n < 3; ++n) {
-            if (n < A.ndim) {
-              po[n] = P[n * N + j];
-              w[n] = PB[n * N + j] + step * g[n];
-            } else {
-              po[n] = 0;
-              w[n] = 0;
+            for (int n = 0; n < 3; ++n) {
+              if (n < nd) {
+                po[n] = P0[n * N + j];
+                w[n] = PB0[n * N + j] + step * g[n];
+              } else {
+                po[n] = 0;
+                w[n] = 0;
+              }
             }
-          }
-          if (A.mode == BQ_TV_ISO) {
-            // tv_ops.py:177-179: p / max(||p_col||, 1)
-            T ss = w[0] * w[0];
-            if (A.ndim >= 2) ss += w[1] * w[1];
-            if (A.ndim >= 3) ss += w[2] * w[2];
-            const T den = fmax(sqrt(ss), (T)1);
+            if (iso) {
+              T ss = w[0] * w[0];
+              if (nd >= 2) ss += w[1] * w[1];
+              if (nd >= 3) ss += w[2] * w[2];
+              ball(w, ss);
+            } else {
 #pragma unroll
-            for (int n = 0; n < 3; ++n) w[n] = w[n] / den;
-          } else {
+              for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
+            }
 #pragma unroll
-            for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
-          }
-#pragma unroll
-          for (int n = 0; n < 3; ++n) {
-            if (n < A.ndim) {
-              const T df = w[n] - po[n];
-              acc[0] += (double)df * (double)df;
-              acc[1] += (double)po[n] * (double)po[n];
-              P[n * N + j] = w[n];
-              PB[n * N + j] = w[n] + mom * df;
+            for (int n = 0; n < 3; ++n) {
+              if (n < nd) {
+                const T df = w[n] - po[n];
+                acc[0] += (double)df * (double)df;
+                acc[1] += (double)po[n] * (double)po[n];
+                P0[n * N + j] = w[n];
+                PB0[n * N + j] = w[n] + mom * df;
+              }
             }
           }
           qc = qu;
@@ -551,41 +885,98 @@ __global__ void __launch_bounds__(NT, 2) wtv_prox_kernel(ProxArgs<T> A) {
       }
     } else if (phase == PH_FINAL) {
       nv = 0;
-      for (long long j = gtid; j < N; j += stride) A.x[j] = vox.q(j);
+      const QEval<T, R> qv{A.a, A.d, A.U, A.lo_arr, A.hi_arr, N, tauT, (T)A.lo, (T)A.hi, sg, s_gz};
+      T* __restrict__ X = A.x;
+      for (long long j = gtid; j < N; j += stride) X[j] = qv(j);
     }
 
-    // ---- barrier + fused reduction + controller --------------------------
-    if (nv > 0) block_sum_to<NT, NACC>(acc, nv, s_bv, s_scr);
+    // ---- barrier + fused deterministic reduction -------------------------
     const int cur = phase;
-    bool ok = grid_reduce_sync<NT>(gs, s_bv, nv, A.partials, s_red, s_scr, [&](const double* red) {
-      if (threadIdx.x == 0) controller<T, R>(A, cur, red);
-    });
-    if (threadIdx.x == 0) {
-      volatile ProxCtl* c = A.ctl;
-      if (!ok) {
-        c->abort = 1;
-        A.report->status = BQ_ETIMEOUT;
+    if (cur != PH_FINAL) {
+      if (nv > 0) block_sum_to<NT, NACC>(acc, nv, s_bv, s_scr);
+      if (threadIdx.x < nv) A.partials[(size_t)blockIdx.x * kMaxVals + threadIdx.x] = s_bv[threadIdx.x];
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned old = atomicAdd(A.bar, 1u);
+        s_flag = (old == gridDim.x - 1) ? 1 : 0;
+        if (s_flag) {
+          __threadfence();
+          const double t_arr = __longlong_as_double((long long)global_ns());
+          s_red[kMaxVals - 1] = t_arr;
+          __stcg(&A.red[kMaxVals - 1], t_arr);
+        }
       }
-      s_phase = c->phase;
-      s_abort = c->abort;
-      s_div_src = c->div_src;
-      s_mom = (T)c->mom;
+      __syncthreads();
+      if (s_flag == 1) {
+        // last block: fixed-order reduction over blocks, publish, release
+        for (int k = warp; k < nv; k += NT / 32) {
+          double s = 0.0;
+          for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(&A.partials[(size_t)b * kMaxVals + k]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
+          if (lane == 0) {
+            s_red[k] = s;
+            __stcg(&A.red[k], s);
+          }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          A.bar[0] = 0;
+          __threadfence();
+          atomicAdd(A.bar + 1, 1u);
+        }
+      } else {
+        if (threadIdx.x == 0) {
+          const uint64_t t0 = global_ns();
+          unsigned spins = 0;
+          while (ld_acquire_u32(A.bar + 1) == my_gen) {
+            __nanosleep(32);
+            if (((++spins) & 1023u) == 0 && global_ns() - t0 > 20ull * 1000000000ull) {
+              s_flag = -1;  // timeout
+              break;
+            }
+          }
+          __threadfence();
+        }
+        __syncthreads();
+        if (s_flag == -1) {
+          if (blockIdx.x == 0 && threadIdx.x == 0) A.report->status = BQ_ETIMEOUT;
+          break;
+        }
+        if (threadIdx.x < nv) s_red[threadIdx.x] = __ldcg(&A.red[threadIdx.x]);
+        if (threadIdx.x == NT - 1) s_red[kMaxVals - 1] = __ldcg(&A.red[kMaxVals - 1]);
+      }
+      my_gen += 1;
+      __syncthreads();
+    }
+    // ---- redundant controller on the block's shared state ----------------
+    if (threadIdx.x == 0) {
+      controller<T, R>(A, s_c, cur, s_red, blockIdx.x == 0);
+      s_phase = s_c.phase;
+      s_div_src = s_c.div_src;
+      s_mom = (T)s_c.mom;
       for (int i = 0; i < R; ++i) {
-        s_gw[i] = (T)c->gw[i];
-        s_beta[i] = (T)c->beta[i];
+        s_gw[i] = (T)s_c.gw[i];
+        s_beta[i] = (T)s_c.beta[i];
+        s_gz[i] = (T)(s_c.gw[i] - s_c.beta[i]);
       }
     }
     __syncthreads();
     phase = s_phase;
-    if (s_abort || phase == PH_DONE) break;
+    if (phase == PH_DONE) break;
   }
 }
 
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
+bool aligned16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
+
 template <typename T, int R>
 int launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t st) {
+  constexpr int NT = Cfg<T, R>::NT;
+  constexpr int TY = Cfg<T, R>::TY;
   ProxArgs<T> A{};
   A.ndim = D.ndim;
   A.mode = D.mode;
@@ -619,31 +1010,25 @@ int launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t st) {
   A.beta_io = D.beta;
   A.report = (bq_wtv_report*)D.report;
   A.partials = ctx->ws.partials;
+  A.red = (double*)ctx->ws.ctl;
   A.bar = ctx->ws.barrier;
-  A.ctl = (ProxCtl*)ctx->ws.ctl;
+  A.vec = (A.N % 4 == 0) && aligned16(D.a) && aligned16(D.d) && aligned16(D.U) && aligned16(D.lo_arr) &&
+          aligned16(D.hi_arr);
 
   auto kern = wtv_prox_kernel<T, R>;
   int per_sm = 0;
   BQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, 0));
   BQ_CHECK(per_sm > 0, BQ_ECUDA, "wtv_prox: kernel does not fit on an SM");
-  long long max_blocks = std::min<long long>((long long)per_sm * ctx->num_sms, kMaxBlocks);
+  per_sm = std::min(per_sm, Cfg<T, R>::MINB);
+  const long long max_blocks = std::min<long long>((long long)per_sm * ctx->num_sms, kMaxBlocks);
   // small problems: fewer blocks -> cheaper barriers
-  long long want = std::max<long long>(1, (A.N + 4 * NT - 1) / (4 * NT));
-  int G = (int)std::min<long long>(max_blocks, want);
-  A.ntx = (A.K1 + TX - 1) / TX;
+  const long long want = std::max<long long>(1, (A.N + 4LL * NT - 1) / (4LL * NT));
+  const int G = (int)std::min<long long>(max_blocks, want);
+  A.vx = A.vec && (A.K1 % 4 == 0) && aligned16(D.p) && aligned16(D.pb) && aligned16(D.v);
+  const int tx = A.vx ? TXV : TX;
+  A.ntx = (A.K1 + tx - 1) / tx;
   A.nty = (A.K2 + TY - 1) / TY;
-  // z-chunk: minimise the per-block critical path ceil(items/G) * (zc + 1)
-  long long nxy = (long long)A.ntx * A.nty;
-  int best_zc = A.K3;
-  long long best_cost = -1;
-  for (int zc = 1; zc <= A.K3; ++zc) {
-    long long items = nxy * ((A.K3 + zc - 1) / zc);
-    long long waves = (items + G - 1) / G;
-    long long cost = waves * (zc + 1);
-    if (best_cost < 0 || cost < best_cost) best_cost = cost, best_zc = zc;
-  }
-  A.zc = best_zc;
-  A.items = (int)(nxy * ((A.K3 + best_zc - 1) / best_zc));
+  A.tile_planes = (long long)A.ntx * A.nty * A.K3;
 
   BQ_CUDA(cudaMemsetAsync(ctx->ws.barrier, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&A};
@@ -673,6 +1058,7 @@ int validate(const bq_wtv_desc& D, bool wpm_only) {
   for (int i = 0; i < 3; ++i) BQ_CHECK(D.dims[i] >= 1, BQ_EINVAL, "dims must be positive");
   for (int i = D.ndim; i < 3; ++i) BQ_CHECK(D.dims[i] == 1, BQ_EINVAL, "dims beyond ndim must be 1");
   BQ_CHECK(D.dims[0] * D.dims[1] * D.dims[2] < (1ll << 40), BQ_EINVAL, "grid too large");
+  BQ_CHECK(D.dims[0] < (1 << 30) && D.dims[1] < (1 << 30) && D.dims[2] < (1 << 30), BQ_EINVAL, "side too large");
   BQ_CHECK(D.dtype == BQ_F32 || D.dtype == BQ_F64, BQ_EINVAL, "dtype must be BQ_F32 or BQ_F64");
   BQ_CHECK(D.sign == 1 || D.sign == -1, BQ_EINVAL, "sign must be +1 or -1, got %d", D.sign);
   BQ_CHECK(D.d != nullptr || D.tau > 0, BQ_EINVAL, "tau must be positive, got %g", D.tau);
@@ -704,11 +1090,10 @@ extern "C" int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream) {
                                : dispatch_rank<double>(ctx, *desc, 0, st);
 }
 
-extern "C" int bq_wpm_box(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign,
-                          double tau, const void* d, const void* U, const void* x, double lo,
-                          double hi, const void* lo_arr, const void* hi_arr, double* beta_inout,
-                          double newton_eps, int32_t newton_max_iter, void* x_out, void* a_scratch,
-                          void* report, void* stream) {
+extern "C" int bq_wpm_box(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign, double tau,
+                          const void* d, const void* U, const void* x, double lo, double hi, const void* lo_arr,
+                          const void* hi_arr, double* beta_inout, double newton_eps, int32_t newton_max_iter,
+                          void* x_out, void* a_scratch, void* report, void* stream) {
   using namespace bq;
   BQ_CHECK(ctx, BQ_EINVAL, "bq_wpm_box: null ctx");
   bq_wtv_desc D{};
@@ -720,10 +1105,7 @@ extern "C" int bq_wpm_box(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, i
   D.mode = BQ_TV_ISO;
   D.rank = rank;
   D.sign = sign;
-  D.accelerated = 0;
   D.tau = tau;
-  D.reg = 0.0;
-  D.step = 0.0;
   D.eps = 1.0;
   D.max_iter = 1;
   D.newton_max_iter = newton_max_iter;
