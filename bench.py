@@ -211,7 +211,7 @@ def run_ours(args):
         dist.barrier()
     step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
     last = D.read_report(wsp)
-    names = ["setup", "div", "newton", "dual", "final"]
+    names = ["setup", "div", "newton_full", "fused", "final", "newton_local"]
     phases = {nm: {"ms": last.phase_ns[i] / 1e6, "work_ms": last.phase_work_ns[i] / 1e6,
                    "visits": int(last.phase_count[i])} for i, nm in enumerate(names)}
     ms = float(np.mean(step_ms))

@@ -98,6 +98,11 @@ typedef struct {
   void* x;               /* N   out: the prox */
   double* beta;          /* rank doubles in (warm) / out (beta*) ; may be NULL if rank==0 */
   void* report;          /* device bq_wtv_report (out) */
+  /* optional scratch enabling the fused single-pass-per-iteration kernel
+   * (K1 in {4..128} dividing 128, 16-byte aligned fields): p2 = ndim x N
+   * (third slot of the P ring, with p and pb), a2 = N (ping-pong of a). */
+  void* p2;
+  void* a2;
 } bq_wtv_desc;
 
 typedef struct {

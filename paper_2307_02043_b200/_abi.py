@@ -73,6 +73,8 @@ class WtvDesc(C.Structure):
         ("x", C.c_void_p),
         ("beta", C.c_void_p),
         ("report", C.c_void_p),
+        ("p2", C.c_void_p),
+        ("a2", C.c_void_p),
     ]
 
 

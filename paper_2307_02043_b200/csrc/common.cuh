@@ -32,7 +32,7 @@ int cuda_fail(cudaError_t e, const char* where);
 
 // Max doubles one block contributes to one barrier-reduction:
 // r (phi) + r(r+1)/2 (Newton matrix) for r = 8.
-constexpr int kMaxVals = 48;
+constexpr int kMaxVals = 96;
 // Upper bound on resident blocks of any persistent kernel (148 SMs x 8).
 constexpr int kMaxBlocks = 2048;
 
@@ -51,6 +51,8 @@ struct bq_ctx {
   int num_sms = 0;
   bq::Workspace ws;
   void* fft_cache = nullptr;      // owned by views code
+  void* near_buf = nullptr;       // near-voxel lists of the fused prox kernel
+  size_t near_bytes = 0;
 };
 
 namespace bq {

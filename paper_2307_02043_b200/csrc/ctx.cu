@@ -72,6 +72,7 @@ extern "C" int bq_ctx_destroy(bq_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   fft_cache_destroy(c->fft_cache);
+  cudaFree(c->near_buf);
   cudaFree(c->ws.partials);
   cudaFree(c->ws.barrier);
   cudaFree(c->ws.ctl);

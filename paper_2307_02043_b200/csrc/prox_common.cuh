@@ -1,0 +1,211 @@
+// prox_common.cuh — device helpers shared by the prox kernels.
+#pragma once
+
+#include "common.cuh"
+
+namespace bq {
+namespace prox {
+
+template <typename T>
+__device__ __forceinline__ T clampv(T z, T lo, T hi) {
+  return fmin(fmax(z, lo), hi);  // np.clip == minimum(maximum(z, lo), hi)
+}
+
+// Reciprocal: correctly rounded MUFU-based sequence in f32 (no IEEE division
+// subroutine on the hot path); exact division in f64.
+__device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
+__device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
+
+// Isotropic dual-ball projection p / max(||p||, 1) (tv_ops.py:177-179).
+__device__ __forceinline__ void ball(float (&w)[3], float ss) {
+  if (ss > 1.0f) {
+    const float s = rsqrtf(ss);
+    w[0] *= s, w[1] *= s, w[2] *= s;
+  }
+}
+__device__ __forceinline__ void ball(double (&w)[3], double ss) {
+  const double den = fmax(sqrt(ss), 1.0);
+  w[0] /= den, w[1] /= den, w[2] /= den;
+}
+
+// 4 consecutive elements; 16-byte vector accesses (f32) / 2 x 16 (f64).
+// ro: read-only for the kernel's lifetime (non-coherent path); rw: plain.
+template <typename T>
+struct Vec4;
+template <>
+struct Vec4<float> {
+  static __device__ __forceinline__ void ro(const float* p, float (&o)[4]) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+    o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+  }
+  static __device__ __forceinline__ void rw(const float* p, float (&o)[4]) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    o[0] = v.x, o[1] = v.y, o[2] = v.z, o[3] = v.w;
+  }
+  static __device__ __forceinline__ void st(float* p, const float (&o)[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(o[0], o[1], o[2], o[3]);
+  }
+};
+template <>
+struct Vec4<double> {
+  static __device__ __forceinline__ void ro(const double* p, double (&o)[4]) {
+    const double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    const double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    o[0] = a.x, o[1] = a.y, o[2] = b.x, o[3] = b.y;
+  }
+  static __device__ __forceinline__ void rw(const double* p, double (&o)[4]) {
+    const double2 a = *reinterpret_cast<const double2*>(p);
+    const double2 b = *(reinterpret_cast<const double2*>(p) + 1);
+    o[0] = a.x, o[1] = a.y, o[2] = b.x, o[3] = b.y;
+  }
+  static __device__ __forceinline__ void st(double* p, const double (&o)[4]) {
+    reinterpret_cast<double2*>(p)[0] = make_double2(o[0], o[1]);
+    reinterpret_cast<double2*>(p)[1] = make_double2(o[2], o[3]);
+  }
+};
+
+// ---- small dense linear algebra for the controller (r <= 8), unrolled ----
+// cap/H are symmetric; packed lower index k(i, j) = i (i + 1) / 2 + j, j <= i.
+template <int R>
+__device__ __forceinline__ bool chol(double (&a)[R > 0 ? R * R : 1]) {
+#pragma unroll
+  for (int j = 0; j < R; ++j) {
+    double s = a[j * R + j];
+#pragma unroll
+    for (int k = 0; k < j; ++k) s -= a[j * R + k] * a[j * R + k];
+    if (!(s > 0.0)) return false;
+    const double l = sqrt(s);
+    a[j * R + j] = l;
+#pragma unroll
+    for (int i = j + 1; i < R; ++i) {
+      double t = a[i * R + j];
+#pragma unroll
+      for (int k = 0; k < j; ++k) t -= a[i * R + k] * a[j * R + k];
+      a[i * R + j] = t / l;
+    }
+  }
+  return true;
+}
+template <int R>
+__device__ __forceinline__ void chol_solve(const double* l, double (&b)[R > 0 ? R : 1]) {
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    double s = b[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) s -= l[i * R + k] * b[k];
+    b[i] = s / l[i * R + i];
+  }
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    double s = b[i];
+#pragma unroll
+    for (int k = i + 1; k < R; ++k) s -= l[k * R + i] * b[k];
+    b[i] = s / l[i * R + i];
+  }
+}
+// LU with partial pivoting (numpy.linalg.solve / LAPACK gesv); false on an
+// exactly-zero pivot (LinAlgError in the reference).
+template <int R>
+__device__ __forceinline__ bool lu(double (&a)[R > 0 ? R * R : 1], double (&b)[R > 0 ? R : 1]) {
+#pragma unroll
+  for (int k = 0; k < R; ++k) {
+    int piv = k;
+    double best = fabs(a[k * R + k]);
+#pragma unroll
+    for (int i = k + 1; i < R; ++i)
+      if (fabs(a[i * R + k]) > best) best = fabs(a[i * R + k]), piv = i;
+    if (best == 0.0) return false;
+    if (piv != k) {
+#pragma unroll
+      for (int j = 0; j < R; ++j) {
+        const double t = a[k * R + j];
+        a[k * R + j] = a[piv * R + j];
+        a[piv * R + j] = t;
+      }
+      const double t = b[k];
+      b[k] = b[piv];
+      b[piv] = t;
+    }
+#pragma unroll
+    for (int i = k + 1; i < R; ++i) {
+      const double f = a[i * R + k] / a[k * R + k];
+#pragma unroll
+      for (int j = k; j < R; ++j) a[i * R + j] -= f * a[k * R + j];
+      b[i] -= f * b[k];
+    }
+  }
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    double s = b[i];
+#pragma unroll
+    for (int j = i + 1; j < R; ++j) s -= a[i * R + j] * b[j];
+    b[i] = s / a[i * R + i];
+  }
+  return true;
+}
+
+// ---- device-wide barrier primitives (release/acquire, no SC fences) -------
+__device__ __forceinline__ unsigned atom_add_acqrel(unsigned* p, unsigned v) {
+  unsigned old;
+  asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(v) : "memory");
+  return old;
+}
+__device__ __forceinline__ void red_add_release(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_relaxed(unsigned* p, unsigned v) {
+  asm volatile("st.relaxed.gpu.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void fence_acq_rel() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+}  // namespace prox
+}  // namespace bq
+
+namespace bq {
+namespace prox {
+// ---- bulk async copy (TMA engine) + mbarrier, raw PTX for sm_100a ---------
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_init_fence() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// global -> shared bulk copy, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst_smem, const void* src_gmem, unsigned bytes,
+                                         unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst_smem)),
+      "l"(src_gmem), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// order earlier generic-proxy accesses before later async-proxy ones
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(unsigned long long* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// named barrier over a subset of the block's warps (ids 1..15; 0 = __syncthreads)
+__device__ __forceinline__ void named_sync(unsigned id, unsigned nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+}  // namespace prox
+}  // namespace bq

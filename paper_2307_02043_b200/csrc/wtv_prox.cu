@@ -32,6 +32,8 @@
 //    equal-length run of (tile, z) planes carrying the z-1 (DIV) / z+1 (DUAL)
 //    neighbour in registers; x+1 comes by warp shuffle, y+1 through L1.
 //  * Fields: T (f32 or f64); every reduction and scalar in f64.
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "common.cuh"
@@ -1077,6 +1079,8 @@ int validate(const bq_wtv_desc& D, bool wpm_only) {
 }
 
 }  // namespace
+bool fused_eligible(const bq_wtv_desc& D);
+int fused_dispatch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t st);
 }  // namespace bq
 
 extern "C" int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream) {
@@ -1086,6 +1090,7 @@ extern "C" int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream) {
   if (rc) return rc;
   BQ_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = (cudaStream_t)stream;
+  if (fused_eligible(*desc) && !getenv("BQ_PROX_GENERAL")) return fused_dispatch(ctx, *desc, 0, st);
   return desc->dtype == BQ_F32 ? dispatch_rank<float>(ctx, *desc, 0, st)
                                : dispatch_rank<double>(ctx, *desc, 0, st);
 }

@@ -77,7 +77,9 @@ class ProxWorkspace:
         self.grid, self.dtype, self.device = grid, dtype, device
         self.p = torch.zeros(d, n, dtype=dtype, device=device)
         self.pb = torch.empty(d, n, dtype=dtype, device=device)
+        self.p2 = torch.empty(d, n, dtype=dtype, device=device)  # third slot of the P ring (fused kernel)
         self.a = torch.empty(n, dtype=dtype, device=device)
+        self.a2 = torch.empty(n, dtype=dtype, device=device)
         self.x = torch.empty(n, dtype=dtype, device=device)
         self.beta = torch.zeros(_abi.BQ_MAX_RANK, dtype=torch.float64, device=device)
         self.report = torch.zeros(_abi.REPORT_BYTES, dtype=torch.uint8, device=device)
@@ -113,6 +115,8 @@ def _launch(prob: DualTvProblem, v: torch.Tensor, ws: ProxWorkspace, eps, max_it
     desc.p, desc.pb, desc.a, desc.x = ws.p.data_ptr(), ws.pb.data_ptr(), ws.a.data_ptr(), ws.x.data_ptr()
     desc.beta = ws.beta.data_ptr()
     desc.report = ws.report.data_ptr()
+    desc.p2 = ws.p2.data_ptr()
+    desc.a2 = ws.a2.data_ptr()
     lib = _abi.load_library()
     _abi.check(lib.bq_wtv_prox(_abi.ctx_for(ws.device), desc, _abi.stream_ptr(ws.device)), "solve")
     # keep optional temporaries alive until the stream has consumed them
