@@ -168,6 +168,29 @@ int bq_vk(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const void* cons
 int bq_tv_value(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64_t* dims, int32_t mode,
                 const void* x, double* out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * Masked-spectrum view operators (the reference forward model,
+ * forward_models.py:86-183).  Layout as above (dims[0] fastest).
+ * ------------------------------------------------------------------------ */
+/* Orthonormal DCT-II (inverse=0) or DCT-III (inverse=1) along one axis
+ * (dims[axis] <= 512); out of place. */
+int bq_dct_axis(bq_ctx* ctx, int32_t dtype, const int64_t* dims, int32_t axis, int32_t inverse,
+                const void* in, void* out, void* stream);
+/* 3-point edge-clamped mean along one axis (forward_models.py:139-150). */
+int bq_smooth_axis(bq_ctx* ctx, int32_t dtype, const int64_t* dims, int32_t axis, const void* in,
+                   void* out, void* stream);
+/* Fused subset combine over `count` (<= 64) views of one spectrum F:
+ *   r = scale * sum_i M_{v_i} (F - y_i)          (r_out may be NULL)
+ *   cost_out[i] = 1/2 || M_{v_i} F - y_i ||^2    (cost_out may be NULL; device)
+ * masks: one 64-bit view set per frequency; views_dev: device int32 ids. */
+int bq_views_combine(bq_ctx* ctx, int32_t dtype, int64_t n, const void* F, const void* const* ys,
+                     const uint64_t* masks, const int32_t* views_dev, int32_t count, double scale,
+                     void* r_out, double* cost_out, void* stream);
+/* Pointwise chain-rule helpers: op 0 out = x + s a^2; 1 out = x + 2s a b;
+ * 2 out = a b; 3 out = x + 2s b; 4 out = s x. */
+int bq_pointwise(bq_ctx* ctx, int32_t dtype, int32_t op, int64_t n, const void* x, const void* a,
+                 const void* b, double s, void* out, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

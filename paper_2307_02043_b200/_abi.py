@@ -41,6 +41,10 @@ EXPORTS = (
     "bq_sr1",
     "bq_vk",
     "bq_tv_value",
+    "bq_dct_axis",
+    "bq_smooth_axis",
+    "bq_views_combine",
+    "bq_pointwise",
 )
 
 
@@ -121,6 +125,10 @@ _SIGS = {
          _I32, _I32, _D, _P, _P, _P, _P, _P],
     ),
     "bq_tv_value": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _I32, _P, _P, _P]),
+    "bq_dct_axis": (C.c_int, [_P, _I32, C.POINTER(_I64), _I32, _I32, _P, _P, _P]),
+    "bq_smooth_axis": (C.c_int, [_P, _I32, C.POINTER(_I64), _I32, _P, _P, _P]),
+    "bq_views_combine": (C.c_int, [_P, _I32, _I64, _P, C.POINTER(_P), _P, _P, _I32, _D, _P, _P, _P]),
+    "bq_pointwise": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _D, _P, _P]),
 }
 
 _lib = None

@@ -75,7 +75,7 @@ struct FCtl {
   int single, nl_ok, pad0, pad1;
   double t, m_prev, m_cur, rel, best_res, last_res, grow;
   double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
-  double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK];
+  double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK], dmax[BQ_MAX_RANK];
   double chol[BQ_MAX_RANK * BQ_MAX_RANK];
   double K0[BQ_MAX_RANK], Cin[36], Cout[36];
   unsigned long long t_last;
@@ -118,6 +118,7 @@ struct FArgs {
   int trace_pass;             // which FUSED pass (iteration) to trace
   int trace_thread;           // which thread of block 0 records
   int dbg;                    // debug switches (timing experiments only)
+  double grow_min;            // minimum box growth factor of the near-list Newton
 };
 
 // shared, per-block copy of what the passes read
@@ -318,13 +319,15 @@ struct Ctl {
     double g[BQ_MAX_RANK > 0 ? BQ_MAX_RANK : 1];
     for (int i = 0; i < R; ++i) g[i] = c.gw[i] - c.beta[i];
     if (used_fallback) c.grow = fmin(c.grow * 4.0, 1e12);
-    else c.grow = fmax(4.0, c.grow * 0.5);
+    else c.grow = fmax(A.grow_min, c.grow * 0.5);
     double scale = 0.0;
     for (int i = 0; i < R; ++i) scale = fmax(scale, fabs(g[i]));
     for (int i = 0; i < R; ++i) {
       const double dg = c.have_hist ? g[i] - c.glast[i] : 0.0;
+      // decaying envelope of recent steps: the trajectory of gamma is not smooth
+      c.dmax[i] = c.have_hist ? fmax(0.75 * c.dmax[i], fabs(dg)) : 0.0;
       c.gc[i] = g[i] + dg;
-      c.gwid[i] = c.grow * fabs(dg) + 1e-7 * c.grow * (fabs(g[i]) + scale) + 1e-300;
+      c.gwid[i] = c.grow * (fabs(dg) + c.dmax[i]) + 1e-7 * c.grow * (fabs(g[i]) + scale) + 1e-300;
       c.glast[i] = g[i];
     }
     c.have_hist = 1;
@@ -446,7 +449,8 @@ struct Ctl {
           c.glast[i] = 0.0;
         }
         c.have_hist = 0;
-        c.grow = 4.0;
+        c.grow = A.grow_min;
+        for (int i = 0; i < R; ++i) c.dmax[i] = 0.0;
         c.t = 1.0;
         c.it = 1;
         c.newton_total = 0;
@@ -1545,6 +1549,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.trace_pass = getenv("BQ_PROX_TRACE") ? atoi(getenv("BQ_PROX_TRACE")) : 0;
   A.trace_thread = getenv("BQ_PROX_TRACE_THREAD") ? atoi(getenv("BQ_PROX_TRACE_THREAD")) : 0;
   A.dbg = getenv("BQ_PROX_DBG") ? atoi(getenv("BQ_PROX_DBG")) : 0;
+  A.grow_min = getenv("BQ_PROX_GROW") ? atof(getenv("BQ_PROX_GROW")) : 8.0;
   BQ_CUDA(cudaMemsetAsync(ctx->ws.barrier, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&A};
   BQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)G), dim3(NT), args, dyn, st));

@@ -212,6 +212,31 @@ def main():
     out["partition_equi_30_4"] = np.concatenate(solvers.partition_views(30, 4))
     out["partition_contig_30_4"] = np.concatenate(solvers.partition_views(30, 4, "contiguous"))
 
+    # ---- DCT stand-in views + BQNPM (forward_models.py, solvers.py) ------
+    for tag, strength, snr, dims in [("lin", 0.0, 30.0, (10, 9, 8)), ("nl", 0.1, 30.0, (12, 8, 6))]:
+        g = Grid(dims)
+        L = 8
+        views = (fm.make_linear_views(g, L, mask_fraction=0.5, seed=3, noise_snr_db=snr) if strength == 0.0 else
+                 fm.make_nonlinear_views(g, L, strength=strength, mask_fraction=0.5, seed=3, noise_snr_db=snr))
+        rng = np.random.default_rng(909)
+        x = 1.333 + 0.01 * rng.standard_normal(g.size)
+        out[f"views_{tag}_dims"] = np.array(dims)
+        out[f"views_{tag}_y"] = np.array([v.y for v in views])
+        out[f"views_{tag}_x"] = x
+        out[f"views_{tag}_grad_sub"] = fm.subset_gradient(views, [1, 4, 6], x)
+        out[f"views_{tag}_values"] = np.array([v.value(x) for v in views])
+        out[f"views_{tag}_fwd0"] = views[0].forward(x)
+        out[f"views_{tag}_phantom"] = fm.make_phantom(g, seed=3).values
+        cfg = solvers.SolverConfig(subsets=4, tv_weight=2e-3, max_outer=10, box=wpm.BoxSet(1.3, 1.4), seed=0)
+        xr, tr = solvers.bqnpm_run(views, g, cfg)
+        out[f"bqnpm_{tag}_x"] = xr
+        out[f"bqnpm_{tag}_cost"] = tr.column("cost")
+        out[f"bqnpm_{tag}_inner"] = tr.column("inner_iters")
+        parts = solvers.partition_views(L, 4)
+        x0 = solvers.default_initializer(views, g, wpm.BoxSet(1.3, 1.4))
+        out[f"bqnpm_{tag}_x0"] = x0
+        out[f"bqnpm_{tag}_alphas"] = solvers.estimate_subset_lipschitz(views, parts, x0, 30, 1.05, 0)
+
     np.savez_compressed(OUT / "reference_golden.npz", **out)
     print(f"wrote {OUT / 'reference_golden.npz'} ({len(out)} arrays)")
 

@@ -1,0 +1,75 @@
+"""Device SR1 estimate, slot aggregation and v_k (through the C ABI) against the
+reference golden vectors (tests/golden, made by the unmodified reference)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2307_02043_b200 import hessian_sr1 as H  # noqa: E402
+from paper_2307_02043_b200 import metric_ops as M  # noqa: E402
+
+
+def test_sr1_matches_reference_golden(golden):
+    for i in range(golden["sr1_s"].shape[0]):
+        est = H.estimate_sr1(golden["sr1_s"][i], golden["sr1_m"][i], gamma=0.8, alpha_fallback=1.7)
+        assert est.tau == pytest.approx(float(golden["sr1_tau"][i]), rel=1e-12)
+        assert (est.u is not None) == bool(golden["sr1_has_u"][i])
+        if est.u is not None:
+            assert rel_l2(est.u, golden["sr1_u"][i]) <= 1e-10
+
+
+def test_sr1_known_answers_and_errors():
+    # tests/test_hessian_sr1.py:8-31 of the reference
+    est = H.estimate_sr1(np.array([1.0, 0.0]), np.array([1.0, 0.0]), gamma=0.8, alpha_fallback=1.0)
+    assert est.tau == pytest.approx(0.8)
+    np.testing.assert_allclose(est.u, [np.sqrt(0.2), 0.0], atol=1e-14)
+    est = H.estimate_sr1(np.array([1.0]), np.array([-1.0]), gamma=0.8, alpha_fallback=7.0)
+    assert est.tau == 7.0 and est.u is None
+    est = H.estimate_sr1(np.array([1.0, 0.0]), np.array([0.0, 1.0]), gamma=0.8, alpha_fallback=3.0)
+    assert est.tau == 3.0 and est.u is None
+    with pytest.raises(ValueError):
+        H.estimate_sr1(np.zeros(4), np.ones(4))
+    with pytest.raises(ValueError):
+        H.estimate_sr1(np.ones(3), np.ones(3), gamma=1.0)
+    with pytest.raises(ValueError):
+        H.estimate_sr1(np.ones(3), np.ones(3), alpha_fallback=0.0)
+
+
+def test_sr1_secant_equation_f32():
+    rng = np.random.default_rng(3)
+    n = 4096
+    a = rng.uniform(0.5, 2.0, n)
+    s = rng.standard_normal(n)
+    m = a * s
+    st = torch.tensor(s, dtype=torch.float32, device="cuda")
+    mt = torch.tensor(m, dtype=torch.float32, device="cuda")
+    est = H.estimate_sr1(st, mt)
+    if est.u is not None:
+        bs = est.apply(st)
+        assert rel_l2(bs.cpu().numpy(), m) < 1e-4
+
+
+def test_vk_matches_reference_golden(golden):
+    slots = []
+    for t in range(4):
+        u = golden[f"vk_u{t}"] if bool(golden[f"vk_has_u{t}"]) else None
+        slots.append(M.SubsetSlot(x=golden[f"vk_x{t}"], grad=golden[f"vk_g{t}"],
+                                  hess=H.Sr1Estimate(tau=float(golden[f"vk_tau{t}"]), u=u)))
+    w = M.aggregate_metric(slots)
+    assert w.tau == pytest.approx(float(golden["vk_tau_w"]), rel=1e-15)
+    np.testing.assert_allclose(w.U, golden["vk_U_w"], rtol=0, atol=0)
+    v = M.compute_v_k(slots, w, 0.7)
+    assert rel_l2(v, golden["vk_v"]) <= 1e-12
+
+
+def test_schedule_matches_reference_golden(golden):
+    tab = np.array([[M.kappa(k, t, 4) for t in range(1, 5)] for k in range(1, 13)])
+    np.testing.assert_array_equal(tab, golden["kappa_table"])
+    np.testing.assert_array_equal(np.concatenate(M.partition_views(30, 4)), golden["partition_equi_30_4"])

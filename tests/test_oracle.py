@@ -155,3 +155,26 @@ def test_schedule_matches_reference(golden):
     np.testing.assert_array_equal(np.concatenate(O.partition_views(30, 4)), golden["partition_equi_30_4"])
     np.testing.assert_array_equal(np.concatenate(O.partition_views(30, 4, "contiguous")),
                                   golden["partition_contig_30_4"])
+
+
+# ---- masked-spectrum views (forward_models.py) ---------------------------
+@pytest.mark.parametrize("tag,strength", [("lin", 0.0), ("nl", 0.1)])
+def test_view_oracle_matches_reference(golden, tag, strength):
+    from oracle import views as OV
+
+    dims = tuple(int(v) for v in golden[f"views_{tag}_dims"])
+    ys = golden[f"views_{tag}_y"]
+    # masks are recovered from the reference's own mask law via the package helper
+    from paper_2307_02043_b200.forward_models import spectrum_masks
+    from paper_2307_02043_b200.tv_ops import Grid
+
+    masks, _ = spectrum_masks(Grid(dims), ys.shape[0], 0.5)
+    views = [OV.DctView(dims, masks[i], ys[i], strength) for i in range(ys.shape[0])]
+    x = golden[f"views_{tag}_x"]
+    assert rel_l2(views[0].forward(x), golden[f"views_{tag}_fwd0"]) < 1e-14
+    np.testing.assert_allclose([v.value(x) for v in views], golden[f"views_{tag}_values"], rtol=1e-12)
+    assert rel_l2(OV.subset_gradient(views, [1, 4, 6], x), golden[f"views_{tag}_grad_sub"]) < 1e-12
+    # the package's phantom law reproduces the reference's
+    from paper_2307_02043_b200.forward_models import make_phantom
+
+    np.testing.assert_array_equal(make_phantom(Grid(dims), seed=3).values, golden[f"views_{tag}_phantom"])

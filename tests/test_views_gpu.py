@@ -1,0 +1,76 @@
+"""Device masked-spectrum views and the GPU-resident BQNPM loop against the
+reference (golden vectors from the unmodified reference run here) and the
+scipy oracle.  fp64 <= 1e-10; reconstructions after a fixed iteration count
+<= 1e-3 (north star), checked much tighter here."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from oracle import views as OV
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+from paper_2307_02043_b200 import forward_models as FM  # noqa: E402
+from paper_2307_02043_b200 import solvers as S  # noqa: E402
+from paper_2307_02043_b200.tv_ops import Grid  # noqa: E402
+from paper_2307_02043_b200.wpm import BoxSet  # noqa: E402
+
+CASES = [("lin", 0.0, (10, 9, 8)), ("nl", 0.1, (12, 8, 6))]
+
+
+def _views(tag, strength, dims, self_check=True):
+    g = Grid(dims)
+    if strength == 0.0:
+        return g, FM.make_linear_views(g, 8, mask_fraction=0.5, seed=3, noise_snr_db=30.0, self_check=self_check)
+    return g, FM.make_nonlinear_views(g, 8, strength=strength, mask_fraction=0.5, seed=3, noise_snr_db=30.0,
+                                      self_check=self_check)
+
+
+@pytest.mark.parametrize("tag,strength,dims", CASES)
+def test_measurements_match_reference(golden, tag, strength, dims):
+    g, views = _views(tag, strength, dims)
+    ys = np.array([v.y for v in views])
+    assert rel_l2(ys, golden[f"views_{tag}_y"]) <= 1e-12
+
+
+@pytest.mark.parametrize("tag,strength,dims", CASES)
+def test_view_operators_match_reference(golden, tag, strength, dims):
+    g, views = _views(tag, strength, dims)
+    x = golden[f"views_{tag}_x"]
+    assert rel_l2(views[0].forward(x), golden[f"views_{tag}_fwd0"]) <= 1e-12
+    np.testing.assert_allclose([v.value(x) for v in views], golden[f"views_{tag}_values"], rtol=1e-10)
+    assert rel_l2(FM.subset_gradient(views, [1, 4, 6], x), golden[f"views_{tag}_grad_sub"]) <= 1e-10
+
+
+@pytest.mark.parametrize("tag,strength,dims", CASES)
+def test_jvp_vjp_adjoint_and_oracle(tag, strength, dims):
+    g, views = _views(tag, strength, dims)
+    rng = np.random.default_rng(5)
+    x, v, z = rng.standard_normal(g.size), rng.standard_normal(g.size), rng.standard_normal(g.size)
+    ov = OV.DctView(dims, views[2].viewset.masks_host[2], views[2].y, strength)
+    assert rel_l2(views[2].jacobian_vec(x, v), ov.jvp(x, v)) <= 1e-12
+    assert rel_l2(views[2].adjoint_vec(x, z), ov.vjp(x, z)) <= 1e-12
+    lhs = float(np.dot(views[2].jacobian_vec(x, v), z))
+    rhs = float(np.dot(v, views[2].adjoint_vec(x, z)))
+    assert abs(lhs - rhs) <= 1e-11 * max(1.0, abs(lhs))
+
+
+@pytest.mark.parametrize("tag,strength,dims", CASES)
+def test_bqnpm_matches_reference_run(golden, tag, strength, dims):
+    g, views = _views(tag, strength, dims)
+    box = BoxSet(1.3, 1.4)
+    x0 = S.default_initializer(views, g, box)
+    assert rel_l2(x0.cpu().numpy(), golden[f"bqnpm_{tag}_x0"]) <= 1e-12
+    parts = S.partition_views(8, 4)
+    al = S.estimate_subset_lipschitz(views, parts, x0, 30, 1.05, 0)
+    np.testing.assert_allclose(al, golden[f"bqnpm_{tag}_alphas"], rtol=1e-10)
+    cfg = S.SolverConfig(subsets=4, tv_weight=2e-3, max_outer=10, box=box, seed=0)
+    x, tr = S.bqnpm_run(views, g, cfg)
+    assert rel_l2(x, golden[f"bqnpm_{tag}_x"]) <= 1e-9
+    np.testing.assert_allclose(tr.column("cost"), golden[f"bqnpm_{tag}_cost"], rtol=1e-9)
+    np.testing.assert_array_equal(tr.column("inner_iters"), golden[f"bqnpm_{tag}_inner"])
