@@ -191,6 +191,47 @@ int bq_views_combine(bq_ctx* ctx, int32_t dtype, int64_t n, const void* F, const
 int bq_pointwise(bq_ctx* ctx, int32_t dtype, int32_t op, int64_t n, const void* x, const void* a,
                  const void* b, double s, void* out, void* stream);
 
+/* ---------------------------------------------------------------------------
+ * First-Born / Lippmann-Schwinger view batches (north star (1)(2); no
+ * reference code -- the discretisation is specified in oracle/physics.py).
+ * Complex fields are interleaved (re, im) in the field precision; B views per
+ * call; the (2n)^3 transforms are batched cuFFT plans cached in the context.
+ * ------------------------------------------------------------------------ */
+/* khat ((2n)^3 complex) = FFT of the Green kernel K(d) = h^3 e^{i kb|d|}/(4 pi |d|). */
+int bq_green_init(bq_ctx* ctx, int32_t dtype, int32_t n, double h, double kb, void* khat, void* stream);
+/* out (B x n^3 complex) = plane waves exp(i k_b . r), kvec_dev = 3B doubles (device). */
+int bq_ls_incident(bq_ctx* ctx, int32_t dtype, int32_t n, double h, int32_t B, const double* kvec_dev,
+                   void* out, void* stream);
+/* Green operator through the padded transform (pad_buf: B x (2n)^3 complex scratch):
+ *  op 0: out = alpha v + beta G_dom(f . v)        op 1: out = alpha v + beta conj(f) . G_dom^H v
+ *  op 2: out = G_det(f . v) (n^2 per view)        op 3: out = G^H P_det^T v (v: n^2 per view)
+ *  ops 0, 1, 3 add `addend` (B x N, may be NULL) to the result. */
+int bq_ls_conv(bq_ctx* ctx, int32_t dtype, int32_t n, int32_t B, int32_t op, const void* khat,
+               const void* f, const void* v, double alpha, double beta, const void* addend,
+               void* pad_buf, void* out, void* stream);
+/* out_b = f . in_b (f real, N; in/out complex B x N). */
+int bq_cscale_real(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* f, const void* in,
+                   void* out, void* stream);
+/* per-view <a_b, c_b> = sum conj(a) c -> out (2B doubles, device), deterministic. */
+int bq_cdot(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* a, const void* c, double* out,
+            void* stream);
+/* out_b = a_b + sgn * coef_b * c_b (coef_b complex at coef[coef_stride * b]); active may be NULL. */
+int bq_caxpy(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* a, const double* coef,
+             int32_t coef_stride, double sgn, const void* c, void* out, const int32_t* active, void* stream);
+/* BiCGSTAB scalar recurrences (stage 0: beta/omega from <rh,r>; 1: alpha; 2: omega). */
+int bq_bicg_scalars(bq_ctx* ctx, int32_t B, int32_t stage, const double* d0, const double* d1,
+                    double* state, double* coef, void* stream);
+int bq_bicg_p(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* r, const void* v,
+              const double* coef, void* p, const int32_t* active, void* stream);
+int bq_bicg_x(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const double* state, const void* p,
+              const void* s, const void* t, void* x, void* r, const int32_t* mode, void* stream);
+/* grad (+)= scale * sum_b Re(conj(fp u_b) w_b), views summed in order. */
+int bq_ls_grad_accum(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* fp, const void* u,
+                     const void* w, double scale, void* grad, int32_t accumulate, void* stream);
+/* scattering potential f(x) and f'(x) (born: 2 k0^2 nb x; ls: k0^2((nb+x)^2 - nb^2)). */
+int bq_ls_potential(bq_ctx* ctx, int32_t dtype, int64_t N, const void* x, double k0, double nb,
+                    int32_t born, void* f, void* fp, void* stream);
+
 #if defined(__GNUC__)
 #pragma GCC visibility pop
 #endif

@@ -45,6 +45,17 @@ EXPORTS = (
     "bq_smooth_axis",
     "bq_views_combine",
     "bq_pointwise",
+    "bq_green_init",
+    "bq_ls_incident",
+    "bq_ls_conv",
+    "bq_cdot",
+    "bq_caxpy",
+    "bq_bicg_scalars",
+    "bq_bicg_p",
+    "bq_bicg_x",
+    "bq_ls_grad_accum",
+    "bq_ls_potential",
+    "bq_cscale_real",
 )
 
 
@@ -129,6 +140,17 @@ _SIGS = {
     "bq_smooth_axis": (C.c_int, [_P, _I32, C.POINTER(_I64), _I32, _P, _P, _P]),
     "bq_views_combine": (C.c_int, [_P, _I32, _I64, _P, C.POINTER(_P), _P, _P, _I32, _D, _P, _P, _P]),
     "bq_pointwise": (C.c_int, [_P, _I32, _I32, _I64, _P, _P, _P, _D, _P, _P]),
+    "bq_green_init": (C.c_int, [_P, _I32, _I32, _D, _D, _P, _P]),
+    "bq_ls_incident": (C.c_int, [_P, _I32, _I32, _D, _I32, _P, _P, _P]),
+    "bq_ls_conv": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
+    "bq_cscale_real": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
+    "bq_cdot": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
+    "bq_caxpy": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _I32, _D, _P, _P, _P, _P]),
+    "bq_bicg_scalars": (C.c_int, [_P, _I32, _I32, _P, _P, _P, _P, _P]),
+    "bq_bicg_p": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P, _P, _P]),
+    "bq_bicg_x": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
+    "bq_ls_grad_accum": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _D, _P, _I32, _P]),
+    "bq_ls_potential": (C.c_int, [_P, _I32, _I64, _P, _D, _D, _I32, _P, _P, _P]),
 }
 
 _lib = None

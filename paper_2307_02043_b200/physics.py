@@ -1,0 +1,289 @@
+"""First-Born and Lippmann-Schwinger view batches on the device (north star (1)(2)).
+
+No reference implementation exists; the
+discretisation is specified once in ``oracle/physics.py`` (Green's kernel on
+the 2n-padded grid with a ball-averaged self term, plane-wave incidence,
+detector one voxel past the +z face, BiCGSTAB from x0 = 0 with a relative
+residual tolerance) and implemented here on libbq:
+
+* ``bq_green_init``  : FFT of the Green kernel, once per setup
+* ``bq_ls_conv``     : pad (+ contrast multiply) -> batched cuFFT -> spectral
+                       Green multiply -> inverse cuFFT -> crop / axpy or detector
+* ``bq_cdot``, ``bq_bicg_*`` : batched BiCGSTAB (per-view scalars on the device,
+                       deterministic dots, converged views masked out)
+* ``bq_ls_grad_accum`` : Re(conj(f' u) . w) summed over the views of the batch
+
+The views plug into the reference's ``ViewProblem`` contract
+(forward_models.py:25-83) with real-packed [Re; Im] detector data,
+and ``subset_gradient`` batches a whole subset.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _abi
+from ._tensors import default_device, is_torch, out_like, to_dev
+
+
+class ScatterViewSet:
+    """L plane-wave views of an n^3 grid (model 'born' or 'ls')."""
+
+    def __init__(self, n, n_views, model="ls", h=0.1, lam0=0.406, n_b=1.333, theta_deg=35.0,
+                 dtype=torch.complex64, tol=1e-6, max_iter=500, batch=8, device=None):
+        if model not in ("born", "ls"):
+            raise ValueError(f"unknown model {model!r}")
+        if dtype not in (torch.complex64, torch.complex128):
+            raise ValueError("dtype must be complex64 or complex128")
+        self.n, self.L, self.model = int(n), int(n_views), model
+        self.h, self.lam0, self.n_b, self.theta = float(h), float(lam0), float(n_b), float(theta_deg)
+        self.k0 = 2.0 * math.pi / self.lam0
+        self.kb = self.n_b * self.k0
+        self.cdtype = dtype
+        self.rdtype = torch.float32 if dtype == torch.complex64 else torch.float64
+        self.code = _abi.BQ_F32 if dtype == torch.complex64 else _abi.BQ_F64
+        self.tol, self.max_iter, self.batch = float(tol), int(max_iter), int(batch)
+        self.device = device or default_device()
+        self.N = self.n ** 3
+        self.lib = _abi.load_library()
+        self.ctx = _abi.ctx_for(self.device)
+        m = 2 * self.n
+        self.khat = torch.empty(m, m, m, dtype=dtype, device=self.device)
+        self._check(self.lib.bq_green_init(self.ctx, self.code, self.n, self.h, self.kb, self.khat.data_ptr(),
+                                           self._st()), "green_init")
+        th = math.radians(self.theta)
+        kv = []
+        for l in range(self.L):
+            ph = 2.0 * math.pi * l / self.L
+            kv.append([self.kb * math.sin(th) * math.cos(ph), self.kb * math.sin(th) * math.sin(ph),
+                       self.kb * math.cos(th)])
+        self.kvec = torch.tensor(kv, dtype=torch.float64, device=self.device)
+        self.y = torch.zeros(self.L, 2 * self.n * self.n, dtype=self.rdtype, device=self.device)
+        self._pad = {}
+        self.iters_forward = []
+        self.iters_adjoint = []
+
+    # -- plumbing ---------------------------------------------------------------
+    def _st(self):
+        return _abi.stream_ptr(self.device)
+
+    def _check(self, rc, what):
+        _abi.check(rc, what)
+
+    def _padbuf(self, B):
+        if B not in self._pad:
+            m = 2 * self.n
+            self._pad[B] = torch.empty(B, m, m, m, dtype=self.cdtype, device=self.device)
+        return self._pad[B]
+
+    def potential(self, x):
+        f = torch.empty(self.N, dtype=self.rdtype, device=self.device)
+        fp = torch.empty_like(f)
+        self._check(self.lib.bq_ls_potential(self.ctx, self.code, self.N, x.data_ptr(), self.k0, self.n_b,
+                                             int(self.model == "born"), f.data_ptr(), fp.data_ptr(), self._st()),
+                    "potential")
+        return f, fp
+
+    def incident(self, views):
+        B = len(views)
+        kv = self.kvec[list(views)].contiguous()
+        out = torch.empty(B, self.N, dtype=self.cdtype, device=self.device)
+        self._check(self.lib.bq_ls_incident(self.ctx, self.code, self.n, self.h, B, kv.data_ptr(), out.data_ptr(),
+                                            self._st()), "incident")
+        return out
+
+    def conv(self, op, f, v, alpha=0.0, beta=1.0, addend=None):
+        B = v.shape[0]
+        out_len = self.n * self.n if op == 2 else self.N
+        out = torch.empty(B, out_len, dtype=self.cdtype, device=self.device)
+        self._check(self.lib.bq_ls_conv(self.ctx, self.code, self.n, B, op, self.khat.data_ptr(), _abi.ptr(f),
+                                        v.data_ptr(), float(alpha), float(beta), _abi.ptr(addend),
+                                        self._padbuf(B).data_ptr(), out.data_ptr(), self._st()), "ls_conv")
+        return out
+
+    def cdot(self, a, c):
+        B = a.shape[0]
+        out = torch.empty(2 * B, dtype=torch.float64, device=self.device)
+        self._check(self.lib.bq_cdot(self.ctx, self.code, a.shape[1], B, a.data_ptr(), c.data_ptr(), out.data_ptr(),
+                                     self._st()), "cdot")
+        return out
+
+    def caxpy(self, a, coef, stride, sgn, c, out=None, active=None):
+        out = torch.empty_like(a) if out is None else out
+        self._check(self.lib.bq_caxpy(self.ctx, self.code, a.shape[1], a.shape[0], a.data_ptr(), coef.data_ptr(),
+                                      stride, float(sgn), c.data_ptr(), out.data_ptr(), _abi.ptr(active), self._st()),
+                    "caxpy")
+        return out
+
+    # -- batched BiCGSTAB (oracle/physics.py bicgstab) ------------------------
+    def bicgstab(self, apply_a, b):
+        B, N = b.shape
+        x = torch.zeros_like(b)
+        r = b.clone()
+        rh = r.clone()
+        p = torch.zeros_like(b)
+        v = torch.zeros_like(b)
+        state = torch.zeros(B, 8, dtype=torch.float64, device=self.device)
+        state[:, 0] = 1.0  # rho
+        state[:, 2] = 1.0  # alpha
+        state[:, 4] = 1.0  # omega
+        coef = torch.zeros(B, 4, dtype=torch.float64, device=self.device)
+        nb = torch.sqrt(self.cdot(b, b).view(B, 2)[:, 0]).cpu().numpy()
+        active_h = (nb > 0).astype(np.int32)
+        iters = np.zeros(B, dtype=np.int64)
+        res0 = np.zeros(B)
+        active = torch.from_numpy(active_h.copy()).to(self.device)
+        mode = torch.zeros(B, dtype=torch.int32, device=self.device)
+        lib, ctx, code, st = self.lib, self.ctx, self.code, self._st()
+        for it in range(1, self.max_iter + 1):
+            if not active_h.any():
+                break
+            d = self.cdot(rh, r)
+            self._check(lib.bq_bicg_scalars(ctx, B, 0, d.data_ptr(), None, state.data_ptr(), coef.data_ptr(), st), "s0")
+            self._check(lib.bq_bicg_p(ctx, code, N, B, r.data_ptr(), v.data_ptr(), coef.data_ptr(), p.data_ptr(),
+                                      active.data_ptr(), st), "bicg_p")
+            v = apply_a(p)
+            d = self.cdot(rh, v)
+            self._check(lib.bq_bicg_scalars(ctx, B, 1, d.data_ptr(), None, state.data_ptr(), coef.data_ptr(), st), "s1")
+            s = self.caxpy(r, state[:, 2:], 8, -1.0, v)  # s = r - alpha v
+            ns = torch.sqrt(self.cdot(s, s).view(B, 2)[:, 0]).cpu().numpy()
+            early = (ns <= self.tol * nb) & (active_h > 0)
+            t = apply_a(s)
+            d0 = self.cdot(t, s)
+            d1 = self.cdot(t, t)
+            self._check(lib.bq_bicg_scalars(ctx, B, 2, d0.data_ptr(), d1.data_ptr(), state.data_ptr(),
+                                            coef.data_ptr(), st), "s2")
+            md = np.where(active_h > 0, np.where(early, 1, 2), 0).astype(np.int32)
+            mode.copy_(torch.from_numpy(md))
+            self._check(lib.bq_bicg_x(ctx, code, N, B, state.data_ptr(), p.data_ptr(), s.data_ptr(), t.data_ptr(),
+                                      x.data_ptr(), r.data_ptr(), mode.data_ptr(), st), "bicg_x")
+            nr = torch.sqrt(self.cdot(r, r).view(B, 2)[:, 0]).cpu().numpy()
+            done = early | ((nr <= self.tol * nb) & (md == 2))
+            iters[(active_h > 0)] = it
+            active_h = np.where(done, 0, active_h).astype(np.int32)
+            active.copy_(torch.from_numpy(active_h.copy()))
+        return x, iters
+
+    # -- operators ---------------------------------------------------------------
+    def total_field(self, f, views):
+        uin = self.incident(views)
+        if self.model == "born":
+            return uin, np.zeros(len(views), dtype=np.int64)
+        return self.bicgstab(lambda q: self.conv(0, f, q, 1.0, -1.0), uin)
+
+    def forward_c(self, x, views):
+        f, _ = self.potential(x)
+        u, it = self.total_field(f, views)
+        self.iters_forward.extend(int(i) for i in it)
+        return self.conv(2, f, u)
+
+    @staticmethod
+    def pack(dc):
+        return torch.cat([dc.real, dc.imag], dim=1)
+
+    def unpack(self, rr):
+        nn = self.n * self.n
+        return torch.complex(rr[:, :nn].contiguous(), rr[:, nn:].contiguous()).to(self.cdtype)
+
+    def forward(self, x, views):
+        return self.pack(self.forward_c(x, views))
+
+    def vjp_from_residual(self, x, views, r_c, f, fp, u, grad, scale, accumulate):
+        w = self.conv(3, None, r_c)
+        if self.model == "ls":
+            z, it = self.bicgstab(lambda q: self.conv(1, f, q, 1.0, -1.0), self._cmul_conj_f(f, w))
+            self.iters_adjoint.extend(int(i) for i in it)
+            w = self.conv(1, None, z, 0.0, 1.0, addend=w)  # w + G_dom^H z
+        self._check(self.lib.bq_ls_grad_accum(self.ctx, self.code, self.N, len(views), fp.data_ptr(), u.data_ptr(),
+                                              w.contiguous().data_ptr(), float(scale), grad.data_ptr(),
+                                              int(accumulate), self._st()), "grad_accum")
+        return grad
+
+    def _cmul_conj_f(self, f, w):
+        # conj(f) . w with real f: a real scaling of each view
+        out = torch.empty_like(w)
+        self._check(self.lib.bq_cscale_real(self.ctx, self.code, self.N, w.shape[0], f.data_ptr(), w.data_ptr(),
+                                            out.data_ptr(), self._st()), "cscale")
+        return out
+
+    def subset_gradient(self, views, x):
+        """(1/|S|) sum_rho grad 1/2 ||H_rho(x) - y_rho||^2, views batched `batch` at a time."""
+        views = list(views)
+        grad = torch.zeros(self.N, dtype=self.rdtype, device=self.device)
+        f, fp = self.potential(x)
+        first = True
+        for i in range(0, len(views), self.batch):
+            vb = views[i:i + self.batch]
+            u, it = self.total_field(f, vb)
+            self.iters_forward.extend(int(k) for k in it)
+            H = self.conv(2, f, u)
+            r = H - self.unpack(self.y[vb])
+            self.vjp_from_residual(x, vb, r, f, fp, u, grad, 1.0 / len(views), accumulate=not first)
+            first = False
+        return grad
+
+    def costs(self, views, x):
+        views = list(views)
+        out = []
+        for i in range(0, len(views), self.batch):
+            vb = views[i:i + self.batch]
+            d = self.forward(x, vb) - self.y[vb]
+            out.append(0.5 * (d.double() ** 2).sum(dim=1))
+        return torch.cat(out)
+
+
+class ScatterView:
+    """ViewProblem-compatible single view (forward_models.py:25-83)."""
+
+    def __init__(self, vs: ScatterViewSet, v: int):
+        self.viewset, self.view_id = vs, int(v)
+
+    @property
+    def y(self):
+        return self.viewset.y[self.view_id].detach().cpu().numpy().astype(float)
+
+    def _x(self, x):
+        return to_dev(x, self.viewset.rdtype, self.viewset.device)
+
+    def forward(self, x):
+        return out_like(x, self.viewset.forward(self._x(x), [self.view_id])[0])
+
+    def gradient(self, x):
+        return out_like(x, self.viewset.subset_gradient([self.view_id], self._x(x)))
+
+    def value(self, x):
+        return float(self.viewset.costs([self.view_id], self._x(x))[0].item())
+
+    def adjoint_vec(self, x, z):
+        vs = self.viewset
+        xt = self._x(x)
+        f, fp = vs.potential(xt)
+        u, _ = vs.total_field(f, [self.view_id])
+        zt = to_dev(z, vs.rdtype, vs.device)[None, :]
+        grad = torch.zeros(vs.N, dtype=vs.rdtype, device=vs.device)
+        vs.vjp_from_residual(xt, [self.view_id], vs.unpack(zt), f, fp, u, grad, 1.0, accumulate=False)
+        return out_like(z, grad)
+
+
+def make_scatter_views(n, n_views, model="ls", x_gt=None, noise_snr_db=None, seed=0, **kw):
+    """Views with synthetic measurements y = H(x_gt) (+ complex Gaussian noise at
+    the given SNR, 20 log10(||y|| / ||e||), as forward_models.py:186-191)."""
+    vs = ScatterViewSet(n, n_views, model=model, **kw)
+    rng = np.random.default_rng(seed)
+    if x_gt is not None:
+        xt = to_dev(x_gt, vs.rdtype, vs.device)
+        for i in range(0, n_views, vs.batch):
+            vb = list(range(i, min(n_views, i + vs.batch)))
+            vs.y[vb] = vs.forward(xt, vb)
+        if noise_snr_db is not None:
+            for l in range(n_views):
+                e = rng.standard_normal(vs.y.shape[1])
+                scale = float(torch.linalg.vector_norm(vs.y[l].double()).item()) / np.linalg.norm(e)
+                vs.y[l] += to_dev(e * scale * 10.0 ** (-noise_snr_db / 20.0), vs.rdtype, vs.device)
+    return [ScatterView(vs, l) for l in range(n_views)], vs
+
+
+__all__ = ["ScatterViewSet", "ScatterView", "make_scatter_views"]
