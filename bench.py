@@ -273,6 +273,10 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
 
+    ls = None
+    if not args.no_ls and rank == 0:
+        ls = ls_measure(args, dev)
+
     if rank == 0:
         peak, peak_kind = hbm_peak()
         bpv = bytes_per_voxel_iter(4, 1, True)
@@ -305,6 +309,7 @@ def run_ours(args):
             "e2e": {"value": ws * N * iters / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
                     "h2d_bytes_per_step": 3 * N * 4, "d2h_bytes_per_step": N * 4},
             "gpu_launches": args.steps,
+            "ls": ls,
             "clocks": sampler.summary(),
             "wall_s_timed_region": wall,
             "prox_phases_last_step": phases,
@@ -316,6 +321,49 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def ls_measure(args, dev):
+    """Secondary metric (BASELINE 'views*voxels/s of LS forward+adjoint'): one
+    subset gradient of config 4 (n=128 padded to 256^3, c64, 16 of 64 views on a
+    40 deg cone, 12 ellipsoids dn~U[0.01,0.1], 25 dB) at x = x_gt / 2."""
+    import torch
+
+    from paper_2307_02043_b200 import physics as PH
+    from paper_2307_02043_b200.configs import ls_phantom
+
+    n = args.ls_n
+    xgt = ls_phantom(n, 12, 0.01, 0.1, seed=4000)
+    views, vs = PH.make_scatter_views(n, 64, model="ls", x_gt=xgt, noise_snr_db=25.0, seed=4001, theta_deg=40.0,
+                                      batch=16, max_iter=500, device=dev)
+    x = torch.tensor(0.5 * xgt, dtype=torch.float32, device=dev)
+    idx = list(range(0, 64, 4))
+    vs.subset_gradient(idx, x)  # plans, warm-up
+    times, kf, ka = [], [], []
+    for _ in range(max(1, args.ls_steps)):
+        vs.iters_forward.clear()
+        vs.iters_adjoint.clear()
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize(dev)
+        s.record()
+        vs.subset_gradient(idx, x)
+        e.record()
+        torch.cuda.synchronize(dev)
+        times.append(s.elapsed_time(e))
+        kf.append(float(np.mean(vs.iters_forward)))
+        ka.append(float(np.mean(vs.iters_adjoint)))
+    ms = float(np.median(times))
+    Kf, Ka = float(np.mean(kf)), float(np.mean(ka))
+    bpv = 952.0 * (Kf + Ka) + 92.0  # SURVEY 8d: bytes per view*voxel of the fused LS algorithm
+    vv = len(idx) * n ** 3
+    peak, _ = hbm_peak()
+    achieved = vv * bpv / (ms * 1e-3) / 1e9
+    return {"metric": "LS forward+adjoint views*voxels/s", "value": vv / (ms * 1e-3), "unit": "view*voxel/s",
+            "ms_per_subset_gradient": ms, "views": len(idx), "n": n, "padded": 2 * n, "dtype": "c64",
+            "K_f": Kf, "K_a": Ka,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "algorithmic_bytes_per_view_voxel": bpv},
+            "data": "synthetic (seeded ellipsoid phantom, 25 dB noise), x = x_gt/2"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -325,6 +373,9 @@ def main():
     ap.add_argument("--n", type=int, default=128)
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-ls", action="store_true")
+    ap.add_argument("--ls-n", type=int, default=128)
+    ap.add_argument("--ls-steps", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -40,3 +40,21 @@ def config2_inputs(n: int = 128):
     u = rm.standard_normal(N) / np.sqrt(N)
     return {"n": n, "v": v, "d": d, "u": u, "phantom": phantom, "reg": 0.05, "lo": 0.0, "hi": np.inf,
             "iters": 100, "tau_twin": 1.25}
+
+
+def ls_phantom(n: int, n_shapes: int, dn_lo: float, dn_hi: float, seed: int) -> np.ndarray:
+    """Random ellipsoids for the LS configurations: centres U[0.25,0.75]^3,
+    semi-axes U[0.08,0.25], random rotation, dn ~ U[lo, hi], later shapes overwrite."""
+    rng = np.random.default_rng(seed)
+    c = (np.arange(n) + 0.5) / n
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    pts = np.stack([x, y, z], axis=-1)
+    vol = np.zeros((n, n, n))
+    for _ in range(n_shapes):
+        ctr = rng.uniform(0.25, 0.75, 3)
+        ax = rng.uniform(0.08, 0.25, 3)
+        q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+        val = rng.uniform(dn_lo, dn_hi)
+        inside = np.sum((((pts - ctr) @ q) / ax) ** 2, axis=-1) <= 1.0
+        vol[inside] = val
+    return vol.reshape(-1)
