@@ -168,7 +168,9 @@ def load_library(path: Path | str | None = None):
     with _lock:
         if _lib is not None and path is None:
             return _lib
-        p = Path(path) if path is not None else LIB_PATH
+        import os
+
+        p = Path(path) if path is not None else Path(os.environ.get("BQ_LIB", LIB_PATH))
         if not p.exists():
             raise BqError(
                 f"{p} is missing: build it with `python -m paper_2307_02043_b200.build` "

@@ -73,7 +73,8 @@ def build(force: bool = False, verbose: bool = False, jobs: int | None = None) -
         obj = OBJDIR / (src.stem + ".o")
         objs.append(obj)
         if force or _needs(obj, [src] + _headers(src)):
-            cmd = [nvcc, *ARCH, *NVCC_FLAGS, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
+            extra = os.environ.get("BQ_NVCC_EXTRA", "").split()
+            cmd = [nvcc, *ARCH, *NVCC_FLAGS, *extra, "-I", str(INCLUDE), "-c", str(src), "-o", str(obj)]
             if verbose:
                 cmd += ["-Xptxas", "-v"]
             todo.append((src, cmd))

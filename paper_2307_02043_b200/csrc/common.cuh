@@ -53,6 +53,8 @@ struct bq_ctx {
   void* fft_cache = nullptr;      // owned by views code
   void* near_buf = nullptr;       // near-voxel lists of the fused prox kernel
   size_t near_bytes = 0;
+  void* aux_buf = nullptr;        // per-voxel 1/d of the fused prox kernel
+  size_t aux_bytes = 0;
 };
 
 namespace bq {

@@ -73,6 +73,7 @@ extern "C" int bq_ctx_destroy(bq_ctx* c) {
   cudaDeviceSynchronize();
   fft_cache_destroy(c->fft_cache);
   cudaFree(c->near_buf);
+  cudaFree(c->aux_buf);
   cudaFree(c->ws.partials);
   cudaFree(c->ws.barrier);
   cudaFree(c->ws.ctl);

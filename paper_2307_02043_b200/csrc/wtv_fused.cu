@@ -1,1567 +1,26 @@
-// wtv_fused.cu — the fast path of bq_wtv_prox: ONE persistent cooperative
-// kernel in which every FGP iteration is ONE fused streaming pass plus ONE
-// device-wide barrier.
-//
-// Reference algorithm (paths under /root/reference/pkg/src/tvqn/):
-//   dual_tv_solver.py:161-250  FGP loop: P_next = Proj(P_bar + step D q), FISTA momentum,
-//                              rel-change stop, final prox at P
-//   dual_tv_solver.py:119-135  w(P) = v - reg W^-1 div(P), q = wpm_box(w(P))
-//   tv_ops.py:107-180          stencils, divergence, dual-ball projection
-//   wpm.py:92-106, 145-253     Woodbury inverse, structured WPM semi-smooth Newton
-// with W = diag(d) + sign U U^T (d == NULL -> tau I, the reference metric).
-//
-// How one FGP iteration i maps onto the machine:
-//  * P lives in a 3-slot ring (p_i, p_{i-1}, p_{i-2}); the momentum field
-//    P_bar_{i-1} = p_{i-1} + m (p_{i-1} - p_{i-2}) is formed on the fly (the
-//    reference's stored P_bar, same arithmetic).  `a` ping-pongs between two
-//    buffers.  Nothing read in a pass is written in that pass, so halos can be
-//    recomputed by any block without races.
-//  * FUSED pass (z-march, 4 voxels per lane via 16-byte accesses, one warp per
-//    x-row of K1 <= 128 voxels): q = clamp(a_{i-1} + s.gamma) evaluated on the
-//    fly, p_i = Proj(P_bar_{i-1} + step D q), P_bar_i formed in registers,
-//    a_i = v - reg D^-1 div(P_bar_i): the x-1 neighbour comes by shuffle, the
-//    z-1 neighbour is carried in registers, the y-1 neighbour through shared
-//    memory (one extra "halo" warp recomputes the row above the block tile).
-//    The same pass accumulates ||p_i - p_{i-1}||^2, ||p_{i-1}||^2,
-//    U^T D^-1 div (Woodbury right-hand side) and the Newton aggregates below.
-//  * Semi-smooth Newton without passes: for a predicted box of the shift
-//    gamma = gw - beta, each voxel is classified as always-inside,
-//    always-clamped or "near" (clamp state may change in the box).  The pass
-//    reduces K0 = sum_out u (a - bound) + sum_near u a, Cin = sum_in u s^T,
-//    Cout = sum_out u s^T and compacts near-voxel indices per warp.  Then
-//    phi(beta) = K0 + Cout gw + Cin beta + beta - sum_near u clamp(a + s.gamma)
-//    and H = I + Cin + sum_near,inside u s^T are exact for every gamma in the
-//    box, so every block evaluates the Newton steps redundantly over the short
-//    near list: no full pass, no barrier.  If gamma leaves the box or the list
-//    overflows, the step falls back to the full-pass Newton of the reference.
-//  * Barriers: release/acquire atomics; the last block reduces the per-block
-//    partials in block order (deterministic) and publishes them; every block
-//    runs the controller on its own shared-memory copy of the state.
-#include <stdlib.h>
-
-#include <algorithm>
-
-#include "prox_common.cuh"
+// wtv_fused.cu — dispatch of the fused prox kernel (instantiations live in
+// wtv_fused_inst_*.cu so they compile in parallel).
+#include "wtv_fused_impl.cuh"
 
 namespace bq {
-namespace {
-using namespace prox;
+namespace fused {
+#define BQ_FUSED_DECL(T, R) extern template int fused_launch<T, R>(bq_ctx*, const bq_wtv_desc&, int, cudaStream_t);
+BQ_FUSED_DECL(float, 0) BQ_FUSED_DECL(float, 1) BQ_FUSED_DECL(float, 2) BQ_FUSED_DECL(float, 3)
+BQ_FUSED_DECL(float, 4) BQ_FUSED_DECL(float, 5) BQ_FUSED_DECL(float, 6) BQ_FUSED_DECL(float, 7)
+BQ_FUSED_DECL(float, 8) BQ_FUSED_DECL(double, 0) BQ_FUSED_DECL(double, 1) BQ_FUSED_DECL(double, 2)
+BQ_FUSED_DECL(double, 3) BQ_FUSED_DECL(double, 4) BQ_FUSED_DECL(double, 5) BQ_FUSED_DECL(double, 6)
+BQ_FUSED_DECL(double, 7) BQ_FUSED_DECL(double, 8)
+#undef BQ_FUSED_DECL
+}  // namespace fused
 
-enum : int { F_SETUP = 0, F_DIV = 1, F_NEWTON = 2, F_FUSED = 3, F_FINAL = 4, F_DONE = 5, F_NLOCAL = 6 };
-
-constexpr int CAPW = 64;   // near-list capacity per warp per pass
-constexpr unsigned FULLM = 0xffffffffu;
-
-template <int R>
-struct FV {
-  static constexpr int S = R * (R + 1) / 2;
-  static constexpr int RHS = 0;
-  static constexpr int K0 = R;
-  static constexpr int CIN = 2 * R;
-  static constexpr int COUT = 2 * R + S;
-  static constexpr int NRM = 2 * R + 2 * S;
-  static constexpr int OVF = NRM + 2;
-  static constexpr int PASS = OVF + 1;
-  static constexpr int NEWTON = R + S;
-  static constexpr int ACC = PASS > NEWTON ? PASS : NEWTON;
-};
-static_assert(FV<8>::PASS <= kMaxVals, "kMaxVals too small");
-
-struct FCtl {
-  int phase, it, newton_it, newton_total;
-  int converged, status, last_newton_it, last_newton_conv;
-  int final_mode, div_p, have_hist, fallbacks;
-  int slot_cur, slot_prev, a_cur, local_steps;
-  int single, nl_ok, pad0, pad1;
-  double t, m_prev, m_cur, rel, best_res, last_res, grow;
-  double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
-  double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK], dmax[BQ_MAX_RANK];
-  double chol[BQ_MAX_RANK * BQ_MAX_RANK];
-  double K0[BQ_MAX_RANK], Cin[36], Cout[36];
-  unsigned long long t_last;
-  unsigned long long phase_ns[8], phase_work_ns[8];
-  int phase_cnt[8];
-};
-
-constexpr int NSTAGE = 2;      // depth of the bulk-copy pipeline (measured best)
-
-struct StageGeo {
-  int W, SRW, nstage;           // warps used, staged rows, pipeline depth (<= NSTAGE)
-  long long slot_elems;         // SRW * K1
-  long long stage_elems;        // fields * slot_elems
-};
-
-template <typename T>
-struct FArgs {
-  int ndim, mode, sign, accelerated, max_iter, newton_max_iter, wpm_only, vec;
-  int K1, K2, K3, lpr, rpw, nty;
-  long long N, plane, tile_planes;
-  double tau, reg, step, eps, newton_eps, lo, hi;
-  const T* lo_arr;
-  const T* hi_arr;
-  const T* d;
-  const T* U;
-  const T* v;
-  T* ring[3];  // ring[0] is the caller's P (in: warm start, out: P*)
-  T* abuf[2];
-  T* x;
-  double* beta_io;
-  bq_wtv_report* report;
-  double* partials;
-  double* red;
-  unsigned* bar;
-  int* near_idx;  // [G * NW * CAPW], NW = warps per block
-  int* near_cnt;  // [G * NW]
-  StageGeo geo;   // staged FUSED pass geometry
-  long long dyn_bytes;  // dynamic shared memory of the launch
-  unsigned long long* trace;  // optional: block-0 per-step timestamps of one FUSED pass
-  int trace_pass;             // which FUSED pass (iteration) to trace
-  int trace_thread;           // which thread of block 0 records
-  int dbg;                    // debug switches (timing experiments only)
-  double grow_min;            // minimum box growth factor of the near-list Newton
-};
-
-// shared, per-block copy of what the passes read
-template <typename T>
-struct FShared {
-  T gz[BQ_MAX_RANK];   // gamma = gw - beta (shift of the clamp argument)
-  T gw[BQ_MAX_RANK];
-  T gc[BQ_MAX_RANK];   // box centre / half width for the aggregates
-  T gwid[BQ_MAX_RANK];
-  T m_prev, m_cur;
-  int phase, slot_cur, slot_prev, slot_new, a_cur, div_p, single, iter;
-};
-
-// ---------------------------------------------------------------------------
-// per-voxel helpers
-// ---------------------------------------------------------------------------
-template <typename T, int R>
-struct Fields {
-  const T* __restrict__ d;
-  const T* __restrict__ U;
-  const T* __restrict__ lo_arr;
-  const T* __restrict__ hi_arr;
-  long long N;
-  T tau, lo, hi, sg;
-
-  // q = clamp(a + s.gamma), s_c = sign u_c / e; also returns 1/e and u (4 voxels)
-  __device__ __forceinline__ void q4x(const T* __restrict__ a, long long j, const T* gz, T (&q)[4], T (&ie)[4],
-                                      T (&u)[R > 0 ? R : 1][4]) const {
-    Vec4<T>::rw(a + j, q);
-    if (R > 0) {
-      T e[4];
-      if (d) Vec4<T>::ro(d + j, e);
-      else e[0] = e[1] = e[2] = e[3] = tau;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ie[k] = rcp(e[k]);
-#pragma unroll
-      for (int c = 0; c < R; ++c) Vec4<T>::ro(U + (long long)c * N + j, u[c]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        T z = q[k];
-#pragma unroll
-        for (int c = 0; c < R; ++c) z += (sg * u[c][k] * ie[k]) * gz[c];
-        q[k] = z;
-      }
-    } else {
-      T e[4];
-      if (d) Vec4<T>::ro(d + j, e);
-      else e[0] = e[1] = e[2] = e[3] = tau;
-#pragma unroll
-      for (int k = 0; k < 4; ++k) ie[k] = rcp(e[k]);
-    }
-    T l[4], h[4];
-    bounds4(j, l, h);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = clampv(q[k], l[k], h[k]);
-  }
-  __device__ __forceinline__ void q4(const T* __restrict__ a, long long j, const T* gz, T (&q)[4]) const {
-    Vec4<T>::rw(a + j, q);
-    if (R > 0) {
-      T e[4];
-      if (d) Vec4<T>::ro(d + j, e);
-      else e[0] = e[1] = e[2] = e[3] = tau;
-      T u[R > 0 ? R : 1][4];
-#pragma unroll
-      for (int c = 0; c < R; ++c) Vec4<T>::ro(U + (long long)c * N + j, u[c]);
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const T ie = rcp(e[k]);
-        T z = q[k];
-#pragma unroll
-        for (int c = 0; c < R; ++c) z += (sg * u[c][k] * ie) * gz[c];
-        q[k] = z;
-      }
-    }
-    T l[4], h[4];
-    bounds4(j, l, h);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) q[k] = clampv(q[k], l[k], h[k]);
-  }
-  // 1/e and u only (standalone DIV pass)
-  __device__ __forceinline__ void ieu4(long long j, T (&ie)[4], T (&u)[R > 0 ? R : 1][4]) const {
-    T e[4];
-    if (d) Vec4<T>::ro(d + j, e);
-    else e[0] = e[1] = e[2] = e[3] = tau;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) ie[k] = rcp(e[k]);
-#pragma unroll
-    for (int c = 0; c < R; ++c) Vec4<T>::ro(U + (long long)c * N + j, u[c]);
-  }
-  __device__ __forceinline__ void bounds4(long long j, T (&l)[4], T (&h)[4]) const {
-    if (lo_arr) Vec4<T>::ro(lo_arr + j, l);
-    else l[0] = l[1] = l[2] = l[3] = lo;
-    if (hi_arr) Vec4<T>::ro(hi_arr + j, h);
-    else h[0] = h[1] = h[2] = h[3] = hi;
-  }
-  // scalar versions (near list, full Newton, final)
-  __device__ __forceinline__ void voxel(const T* __restrict__ a, long long j, T& av, T (&s)[R > 0 ? R : 1],
-                                        T (&u)[R > 0 ? R : 1], T& l, T& h) const {
-    av = a[j];
-    const T e = d ? __ldg(d + j) : tau;
-    const T ie = rcp(e);
-#pragma unroll
-    for (int c = 0; c < R; ++c) {
-      u[c] = __ldg(U + (long long)c * N + j);
-      s[c] = sg * u[c] * ie;
-    }
-    l = lo_arr ? __ldg(lo_arr + j) : lo;
-    h = hi_arr ? __ldg(hi_arr + j) : hi;
-  }
-};
-
-// Classify voxel (a, s, u) for the Newton aggregates of box (gc, gwid) and
-// accumulate; returns true for a "near" voxel (must go to the list).
-template <typename T, int R, int NACC, typename AccT>
-__device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], const T (&u)[R > 0 ? R : 1], T l, T h,
-                                          const T* gc, const T* gwid, AccT (&acc)[NACC]) {
-  using V = FV<R>;
-  T zc = av, rho = 0;
-#pragma unroll
-  for (int c = 0; c < R; ++c) {
-    zc += s[c] * gc[c];
-    rho += fabs(s[c]) * gwid[c];
-  }
-  // safety margin for rounding of a + s.gamma anywhere in the box
-  const T eps = (sizeof(T) == 4) ? (T)1e-5 : (T)1e-13;
-  rho = rho * ((T)1 + eps) + (fabs(zc) + fabs(av)) * eps;
-  const bool inside = (zc - rho > l) && (zc + rho < h);
-  int k = 0;
-  if (inside) {
-#pragma unroll
-    for (int c = 0; c < R; ++c)
-#pragma unroll
-      for (int c2 = 0; c2 <= c; ++c2, ++k) acc[V::CIN + k] += (AccT)u[c] * (AccT)s[c2];
-    return false;
-  }
-#pragma unroll
-  for (int c = 0; c < R; ++c)
-#pragma unroll
-    for (int c2 = 0; c2 <= c; ++c2, ++k) acc[V::COUT + k] += (AccT)u[c] * (AccT)s[c2];
-  if (zc + rho <= l) {
-#pragma unroll
-    for (int c = 0; c < R; ++c) acc[V::K0 + c] += (AccT)u[c] * (AccT)(av - l);
-    return false;
-  }
-  if (zc - rho >= h) {
-#pragma unroll
-    for (int c = 0; c < R; ++c) acc[V::K0 + c] += (AccT)u[c] * (AccT)(av - h);
-    return false;
-  }
-#pragma unroll
-  for (int c = 0; c < R; ++c) acc[V::K0 + c] += (AccT)u[c] * (AccT)av;
-  return true;
-}
-
-// Warp-deterministic compaction of near voxels into this warp's segment.
-__device__ __forceinline__ void near_push(bool flag, long long j, int lane, int* seg, int& cnt, bool& ovf) {
-  const unsigned m = __ballot_sync(FULLM, flag);
-  if (m == 0) return;
-  const int n = __popc(m);
-  if (cnt + n > CAPW) {
-    ovf = true;
-    cnt = CAPW;
-    return;
-  }
-  if (flag) seg[cnt + __popc(m & ((1u << lane) - 1u))] = (int)j;
-  cnt += n;
-}
-
-// ---------------------------------------------------------------------------
-// controller (thread 0 of every block, on the block's own shared state)
-// ---------------------------------------------------------------------------
-template <typename T, int R>
-struct Ctl {
-  using V = FV<R>;
-  const FArgs<T>& A;
-  FCtl& c;
-  bool writer;
-
-  __device__ bool diag() const { return A.d != nullptr; }
-  // gram-like reduced entry -> metric units (scalar metric divides by tau)
-  __device__ double gsc(double g) const { return diag() ? g : g / A.tau; }
-
-  __device__ void timeline(int phase, const double* red, bool passed_barrier) {
-    const unsigned long long now = global_ns();
-    if (phase == F_SETUP) {
-      for (int i = 0; i < 8; ++i) c.phase_ns[i] = 0, c.phase_work_ns[i] = 0, c.phase_cnt[i] = 0;
-    } else {
-      c.phase_ns[phase] += now - c.t_last;
-      const unsigned long long arrive = passed_barrier ? __double_as_longlong(red[kMaxVals - 1]) : now;
-      if (arrive > c.t_last && arrive <= now) c.phase_work_ns[phase] += arrive - c.t_last;
-      c.phase_cnt[phase] += 1;
-    }
-    c.t_last = now;
-  }
-
-  __device__ void next_box_and_continue(bool used_fallback) {
-    // predict the next gamma box from the last two Newton solutions
-    double g[BQ_MAX_RANK > 0 ? BQ_MAX_RANK : 1];
-    for (int i = 0; i < R; ++i) g[i] = c.gw[i] - c.beta[i];
-    if (used_fallback) c.grow = fmin(c.grow * 4.0, 1e12);
-    else c.grow = fmax(A.grow_min, c.grow * 0.5);
-    double scale = 0.0;
-    for (int i = 0; i < R; ++i) scale = fmax(scale, fabs(g[i]));
-    for (int i = 0; i < R; ++i) {
-      const double dg = c.have_hist ? g[i] - c.glast[i] : 0.0;
-      // decaying envelope of recent steps: the trajectory of gamma is not smooth
-      c.dmax[i] = c.have_hist ? fmax(0.75 * c.dmax[i], fabs(dg)) : 0.0;
-      c.gc[i] = g[i] + dg;
-      c.gwid[i] = c.grow * (fabs(dg) + c.dmax[i]) + 1e-7 * c.grow * (fabs(g[i]) + scale) + 1e-300;
-      c.glast[i] = g[i];
-    }
-    c.have_hist = 1;
-  }
-
-  __device__ void finish_newton(int converged) {
-    for (int i = 0; i < R; ++i) c.beta[i] = c.best_beta[i];
-    c.newton_total += c.newton_it;
-    c.last_newton_it = c.newton_it;
-    c.last_newton_conv = converged;
-    c.last_res = (R == 0) ? 0.0 : c.best_res;
-    next_box_and_continue(c.fallbacks > 0);
-    c.phase = c.final_mode ? F_FINAL : F_FUSED;
-  }
-
-  // one Newton evaluation result (phi without beta, H without I) -> decision
-  // wpm.py:207-224.  Returns the next phase.
-  __device__ void newton_step(const double* phi_part, const double* h_part) {
-    double phi[BQ_MAX_RANK > 0 ? BQ_MAX_RANK : 1];
-    double ss = 0.0;
-    for (int i = 0; i < R; ++i) {
-      phi[i] = phi_part[i] + c.beta[i];
-      ss += phi[i] * phi[i];
-    }
-    const double res = sqrt(ss);
-    if (res < c.best_res) {
-      c.best_res = res;
-      for (int i = 0; i < R; ++i) c.best_beta[i] = c.beta[i];
-    }
-    if (res <= A.newton_eps) return finish_newton(1);
-    if (c.newton_it == A.newton_max_iter) return finish_newton(0);
-    double h[R > 0 ? R * R : 1], hs[R > 0 ? R * R : 1], st[R > 0 ? R : 1];
-    int k = 0;
-    for (int i = 0; i < R; ++i)
-      for (int j = 0; j <= i; ++j, ++k) {
-        const double val = (i == j ? 1.0 : 0.0) + h_part[k];
-        h[i * R + j] = val;
-        h[j * R + i] = val;
-      }
-    for (int i = 0; i < R * R; ++i) hs[i] = h[i];
-    for (int i = 0; i < R; ++i) st[i] = phi[i];
-    if (!lu<R>(hs, st)) {
-      double ninf = 0.0;  // Levenberg fallback, wpm.py:219-223
-      for (int i = 0; i < R; ++i) {
-        double rs = 0.0;
-        for (int j = 0; j < R; ++j) rs += fabs(h[i * R + j]);
-        ninf = fmax(ninf, rs);
-      }
-      for (int i = 0; i < R * R; ++i) hs[i] = h[i];
-      for (int i = 0; i < R; ++i) hs[i * R + i] += 1e-8 * ninf, st[i] = phi[i];
-      lu<R>(hs, st);
-    }
-    for (int i = 0; i < R; ++i) c.beta[i] -= st[i];
-    c.newton_it += 1;
-    choose_newton_mode();
-  }
-
-  // local (near-list) evaluation is exact while gamma stays in the box
-  __device__ void choose_newton_mode() {
-    bool in_box = c.nl_ok != 0;
-    for (int i = 0; i < R; ++i) {
-      const double g = c.gw[i] - c.beta[i];
-      if (!(fabs(g - c.gc[i]) <= c.gwid[i])) in_box = false;
-    }
-    if (in_box) {
-      c.phase = F_NLOCAL;
-    } else {
-      if (c.phase != F_NEWTON) c.fallbacks += 1;
-      c.phase = F_NEWTON;
-    }
-  }
-
-  // after a DIV or FUSED pass: Woodbury coefficient and Newton start
-  __device__ void after_div(const double* red) {
-    double coef[R > 0 ? R : 1];
-    for (int i = 0; i < R; ++i) coef[i] = gsc(red[V::RHS + i]);
-    if (R > 0) chol_solve<R>(c.chol, coef);
-    for (int i = 0; i < R; ++i) c.gw[i] = c.single ? 0.0 : A.reg * coef[i];
-    for (int i = 0; i < R; ++i) c.K0[i] = red[V::K0 + i];
-    for (int k = 0; k < V::S; ++k) c.Cin[k] = red[V::CIN + k], c.Cout[k] = red[V::COUT + k];
-    c.nl_ok = red[V::OVF] == 0.0;
-    c.fallbacks = 0;
-    c.newton_it = 0;
-    c.best_res = INFINITY;
-    for (int i = 0; i < R; ++i) c.best_beta[i] = c.beta[i];
-    if (R == 0) {
-      c.best_res = 0.0;
-      finish_newton(1);
-      return;
-    }
-    c.phase = F_DIV;  // sentinel so a first out-of-box start is not counted twice
-    choose_newton_mode();
-  }
-
-  __device__ void run(int phase, const double* red) {
-    switch (phase) {
-      case F_SETUP: {
-        double cap[R > 0 ? R * R : 1];
-        int k = 0;
-        for (int i = 0; i < R; ++i)
-          for (int j = 0; j <= i; ++j, ++k) {
-            const double val = (i == j ? 1.0 : 0.0) + A.sign * gsc(red[k]);
-            cap[i * R + j] = val;
-            cap[j * R + i] = val;
-          }
-        c.status = 0;
-        if (R > 0 && !chol<R>(cap)) {
-          c.status = BQ_ENOTPD;
-          c.phase = F_DONE;
-          if (writer) A.report->status = BQ_ENOTPD;
-          return;
-        }
-        for (int i = 0; i < R * R; ++i) c.chol[i] = cap[i];
-        for (int i = 0; i < R; ++i) {
-          c.beta[i] = A.beta_io ? A.beta_io[i] : 0.0;
-          c.gw[i] = 0.0;
-          c.gc[i] = -c.beta[i];  // gw == 0 when the warm start is zero
-          c.gwid[i] = 0.0;       // forces one full Newton evaluation first
-          c.glast[i] = 0.0;
-        }
-        c.have_hist = 0;
-        c.grow = A.grow_min;
-        for (int i = 0; i < R; ++i) c.dmax[i] = 0.0;
-        c.t = 1.0;
-        c.it = 1;
-        c.newton_total = 0;
-        c.converged = 0;
-        c.rel = INFINITY;
-        c.last_newton_it = 0;
-        c.last_newton_conv = 1;
-        c.last_res = 0.0;
-        c.single = (A.wpm_only || A.reg == 0.0) ? 1 : 0;
-        c.final_mode = c.single;
-        c.slot_cur = 0;
-        c.slot_prev = 0;
-        c.a_cur = 1;    // the DIV pass writes abuf[1 - a_cur] = abuf[0]
-        c.m_prev = 0.0; // P_bar_0 = P_0
-        c.div_p = 1;    // DIV source: P_0 (== P_bar_0)
-        c.phase = F_DIV;
-        return;
-      }
-      case F_DIV:
-        c.a_cur ^= 1;
-        after_div(red);
-        return;
-      case F_NEWTON: {
-        // full-pass evaluation of phi and H at beta (wpm.py:150-167)
-        double hp[V::S > 0 ? V::S : 1];
-        for (int k = 0; k < V::S; ++k) hp[k] = red[R + k];
-        newton_step(red, hp);
-        return;
-      }
-      case F_FUSED: {
-        // dual_tv_solver.py:226-239 on the ring
-        const double num = sqrt(red[V::NRM]), den = sqrt(red[V::NRM + 1]);
-        const double rel = (num == 0.0) ? 0.0 : (den > 0.0 ? num / den : INFINITY);
-        c.rel = rel;
-        const int slot_new = (c.slot_cur == c.slot_prev) ? (c.slot_cur + 1) % 3 : 3 - c.slot_cur - c.slot_prev;
-        c.slot_prev = c.slot_cur;
-        c.slot_cur = slot_new;
-        c.a_cur ^= 1;
-        if (rel < A.eps) {
-          c.converged = 1;
-          c.final_mode = 1;
-          if (!c.div_p) {
-            // a was built from P_bar_i; the final prox needs div(p_i)
-            c.div_p = 1;
-            c.m_prev = 0.0;
-            c.slot_prev = c.slot_cur;
-            c.phase = F_DIV;
-            return;
-          }
-        } else {
-          c.t = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c.t * c.t));
-          if (c.div_p) c.final_mode = 1;  // that was the last iteration
-          else c.it += 1;
-        }
-        c.m_prev = c.m_cur;
-        after_div(red);
-        return;
-      }
-      case F_FINAL: {
-        if (writer) {
-          bq_wtv_report* rp = A.report;
-          rp->iterations = c.single ? 1 : c.it;
-          rp->converged = c.single ? 1 : c.converged;
-          rp->rel_change = c.single ? 0.0 : c.rel;
-          rp->newton_iterations = c.newton_total;
-          rp->status = 0;
-          rp->newton_residual = c.last_res;
-          rp->last_newton_iterations = c.last_newton_it;
-          rp->last_newton_converged = c.last_newton_conv;
-          if (A.beta_io)
-            for (int i = 0; i < R; ++i) A.beta_io[i] = c.beta[i];
-          for (int i = 0; i < 6; ++i) {
-            const int src = (i == 5) ? F_NLOCAL : i;  // [setup, div, newton (full pass), fused, final, newton (local)]
-            rp->phase_ns[i] = (double)c.phase_ns[src];
-            rp->phase_work_ns[i] = (double)c.phase_work_ns[src];
-            rp->phase_count[i] = c.phase_cnt[src];
-          }
-        }
-        c.phase = F_DONE;
-        return;
-      }
-      default:
-        c.phase = F_DONE;
-    }
-  }
-
-  // before a FUSED pass: momentum coefficients and the div source
-  __device__ void prepare_fused() {
-    const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c.t * c.t));
-    c.m_cur = A.accelerated ? (c.t - 1.0) / tn : 0.0;
-    c.div_p = (c.it >= A.max_iter) ? 1 : 0;
-  }
-};
-
-// ---------------------------------------------------------------------------
-// FUSED pass with bulk-async staging (TMA engine): per plane-step one thread
-// copies the block's contiguous row ranges of every input field into a
-// double-buffered shared-memory stage (mbarrier completion); all warps compute
-// from shared memory.  Stage of step k: q-inputs (a, d, U, bounds) of plane
-// k+1 and P_{i-1}, P_{i-2}, v of plane k.  Staged rows y_base .. y_base+W*rpw:
-// warp 0 owns the halo rows above the tile, the last staged row is the row
-// below it (its q is computed by warp 0 too).
-// ---------------------------------------------------------------------------
-
-struct StepIter {
-  int pos, seg_end, tile;
-  int z0, z1, zs, k, K3, nd;
-  bool valid;
-  __device__ void init(long long b, long long e, int K3_, int nd_) {
-    pos = (int)b, seg_end = (int)e, K3 = K3_, nd = nd_;
-    next_segment();
-  }
-  __device__ void next_segment() {
-    valid = pos < seg_end;
-    if (!valid) return;
-    tile = pos / K3;
-    z0 = pos - tile * K3;
-    z1 = min(K3, z0 + (seg_end - pos));
-    pos += z1 - z0;
-    zs = (z0 > 0 && nd >= 3) ? z0 - 1 : z0;
-    k = zs - 1;  // pre-step: q-inputs of plane zs only
-  }
-  __device__ void advance() {
-    if (++k > z1 - 1) next_segment();
-  }
-  __device__ bool has_qin() const { return k + 1 < K3; }
-  __device__ bool has_pin() const { return k >= zs; }
-};
-
-template <int R>
-struct StageMap {
-  int A, D, U0, LO, HI, V, PC0, PP0, nfield;  // field slots (-1: absent)
-  __host__ __device__ void make(bool diag, bool lo_arr, bool hi_arr, int nd, bool need_pp) {
-    int f = 0;
-    A = f++;
-    D = diag ? f++ : -1;
-    U0 = f;
-    f += R;
-    LO = lo_arr ? f++ : -1;
-    HI = hi_arr ? f++ : -1;
-    V = f++;
-    PC0 = f;
-    f += nd;
-    PP0 = need_pp ? f : -1;
-    if (need_pp) f += nd;
-    nfield = f;
-  }
-};
-
-// Issue the bulk copies of one step.  Called by all 32 lanes of the producer
-// warp: copy i is issued by lane i (descriptor math in parallel), lane 0 arms
-// the mbarrier with the total byte count.
-template <typename T, int R>
-__device__ __forceinline__ void issue_step(const FArgs<T>& A, const StepIter& it, const StageMap<R>& M,
-                                           const StageGeo& g, T* stage, unsigned long long* bar, const T* Pc,
-                                           const T* Pp, const T* Ain, int lane) {
-  const int K1 = A.K1, K2 = A.K2, rpw = A.rpw;
-  const long long N = A.N, plane = A.plane;
-  const int TYe = (g.W - 1) * rpw;
-  const int y0 = (int)it.tile * TYe;
-  const int y_base = y0 - rpw;
-  // enumerate copies: index -> (slot, base, plane, row range)
-  int slot = -1, ya = 0, yb = 0;
-  const T* base = nullptr;
-  long long zp = 0;
-  int idx = 0;
-  auto pick = [&](int sl, const T* bs, long long z, int a, int b) {
-    if (sl < 0) return;
-    if (idx == lane) slot = sl, base = bs, zp = z, ya = a, yb = b;
-    ++idx;
-  };
-  if (it.has_qin()) {
-    const long long zq = it.k + 1;
-    pick(M.A, Ain, zq, y_base, y_base + g.SRW);
-    pick(M.D, A.d, zq, y_base, y_base + g.SRW);
-    for (int c = 0; c < R; ++c) pick(M.U0 + c, A.U + (long long)c * N, zq, y_base, y_base + g.SRW);
-    pick(M.LO, A.lo_arr, zq, y_base, y_base + g.SRW);
-    pick(M.HI, A.hi_arr, zq, y_base, y_base + g.SRW);
-  }
-  if (it.has_pin()) {
-    const long long zk = it.k;
-    pick(M.V, A.v, zk, y0, y0 + TYe);
-    for (int n = 0; n < A.ndim; ++n) {
-      pick(M.PC0 + n, Pc + n * N, zk, y_base, y_base + g.W * rpw);
-      if (M.PP0 >= 0) pick(M.PP0 + n, Pp + n * N, zk, y_base, y_base + g.W * rpw);
-    }
-  }
-  unsigned bytes = 0;
-  if (slot >= 0) {
-    ya = max(ya, 0);
-    yb = min(yb, K2);
-    if (yb > ya) bytes = (unsigned)((long long)(yb - ya) * K1 * (long long)sizeof(T));
-  }
-  unsigned total = bytes;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) total += __shfl_xor_sync(FULLM, total, o);
-  if (lane == 0) {
-    fence_proxy_async_smem();
-    mbar_expect_tx(bar, total);
-  }
-  __syncwarp();
-  if (bytes)
-    bulk_g2s(stage + slot * g.slot_elems + (long long)(ya - y_base) * K1, base + zp * plane + (long long)ya * K1,
-             bytes, bar);
-}
-
-template <typename T, int R, int NACC>
-__device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>& sh, const StageGeo& g,
-                                             long long seg_begin, long long seg_end, T* dyn,
-                                             unsigned long long* full, unsigned long long* empty,
-                                             unsigned (&uses)[NSTAGE], double (&acc)[NACC], int* near_seg,
-                                             int& ncnt, bool& ovf) {
-  using V = FV<R>;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const long long N = A.N;
-  const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
-  const int lpr = A.lpr, rpw = A.rpw;
-  const int xr = lane % lpr, yr = lane / lpr, xb = 4 * xr;
-  const int W = g.W;
-  const int TYe = (W - 1) * rpw;
-  const bool used = warp < W;
-  const bool halo = warp == 0;
-  const int sr = warp * rpw + yr;  // staged row of this thread
-  const T* __restrict__ Pc = A.ring[sh.slot_cur];
-  const T* __restrict__ Pp = A.ring[sh.slot_prev];
-  T* __restrict__ Pn = A.ring[sh.slot_new];
-  const T* __restrict__ Ain = A.abuf[sh.a_cur];
-  T* __restrict__ Aout = A.abuf[sh.a_cur ^ 1];
-  const T m_prev = sh.m_prev, m_cur = sh.m_cur;
-  const bool div_p = sh.div_p;
-  const T step = (T)A.step, reg = (T)A.reg, sg = (T)A.sign, tauT = (T)A.tau;
-  const bool iso = A.mode == BQ_TV_ISO;
-  const bool diag = A.d != nullptr;
-  StageMap<R> M;
-  M.make(diag, A.lo_arr != nullptr, A.hi_arr != nullptr, nd, m_prev != (T)0);
-  const int NS = g.nstage;
-  T* const qbuf = dyn + NS * g.stage_elems;   // [2][SRW][K1]
-  T* const srcbuf = qbuf + 2 * g.slot_elems;  // [2][SRW][K1]
-  const T lo_s = (T)A.lo, hi_s = (T)A.hi;
-
-  // ---- producer warp (warp W): issues the bulk copies, 2 stages ahead ----
-  if (warp == W) {
-    fence_proxy_async_global();  // this pass reads data written before the grid barrier
-    StepIter prod;
-    prod.init(seg_begin, seg_end, K3, nd);
-    unsigned pu0 = uses[0], pu1 = uses[1];
-    int ps = 0;
-    while (prod.valid) {
-      const int b = ps & 1;
-      if (ps >= 2) mbar_wait(&empty[b], ((b ? pu1 : pu0) - 1) & 1u);  // consumers released it
-      issue_step<T, R>(A, prod, M, g, dyn + b * g.stage_elems, &full[b], Pc, Pp, Ain, lane);
-      if (b) ++pu1;
-      else ++pu0;
-      prod.advance();
-      ++ps;
-    }
-    uses[0] = pu0, uses[1] = pu1;  // in step with the consumers
-    return;
-  }
-  if (warp > W) {
-    StepIter cnt;
-    cnt.init(seg_begin, seg_end, K3, nd);
-    int ps = 0;
-    while (cnt.valid) {
-      if (ps & 1) uses[1] += 1;
-      else uses[0] += 1;
-      cnt.advance();
-      ++ps;
-    }
-    return;
-  }
-  StepIter cons;
-  cons.init(seg_begin, seg_end, K3, nd);
-  T qc[4] = {0, 0, 0, 0}, iec[4] = {1, 1, 1, 1}, uc[R > 0 ? R : 1][4];
-  T f3prev[4] = {0, 0, 0, 0};
-#pragma unroll
-  for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][0] = uc[c][1] = uc[c][2] = uc[c][3] = 0;
-  int s = 0;
-  while (cons.valid) {
-    const int b = s & 1;
-    T* const stg = dyn + b * g.stage_elems;
-    unsigned long long t_a = 0, t_b = 0;
-    const bool tr = A.trace && blockIdx.x == 0 && threadIdx.x == A.trace_thread && sh.iter == A.trace_pass && s < 60;
-    if (tr) t_a = global_ns();
-    mbar_wait(&full[b], (b ? uses[1] : uses[0]) & 1u);
-    if (tr) t_b = global_ns();
-    if (b) uses[1] += 1;
-    else uses[0] += 1;
-    const int k = cons.k;
-    const int y0 = (int)cons.tile * TYe;
-    const int y = y0 - rpw + sr;
-    const bool act = used && y >= 0 && y < K2;
-    const bool real = act && !halo;
-    const bool warm = k < cons.z0;
-    const bool pin = cons.has_pin();
-    if (k == cons.zs - 1) f3prev[0] = f3prev[1] = f3prev[2] = f3prev[3] = 0;
-    const long long rowoff = (long long)sr * K1 + xb;
-    // per-step partial sums in the field type (one f64 conversion per step)
-    T fa[NACC];
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) fa[q] = 0;
-
-    // ---- q(k+1) of this row (+ the row below the tile, by warp 0) -------
-    T qn4[4] = {0, 0, 0, 0}, ien[4] = {1, 1, 1, 1}, un[R > 0 ? R : 1][4];
-#pragma unroll
-    for (int c = 0; c < (R > 0 ? R : 1); ++c) un[c][0] = un[c][1] = un[c][2] = un[c][3] = 0;
-    if (cons.has_qin()) {
-      auto qrow = [&](long long off, T (&q)[4], T (&ie)[4], T (&u)[R > 0 ? R : 1][4]) {
-        T e[4], l[4], h[4];
-        Vec4<T>::rw(stg + M.A * g.slot_elems + off, q);
-        if (diag) Vec4<T>::rw(stg + M.D * g.slot_elems + off, e);
-        else e[0] = e[1] = e[2] = e[3] = tauT;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) ie[v] = rcp(e[v]);
-#pragma unroll
-        for (int c = 0; c < R; ++c) Vec4<T>::rw(stg + (M.U0 + c) * g.slot_elems + off, u[c]);
-        if (M.LO >= 0) Vec4<T>::rw(stg + M.LO * g.slot_elems + off, l);
-        else l[0] = l[1] = l[2] = l[3] = lo_s;
-        if (M.HI >= 0) Vec4<T>::rw(stg + M.HI * g.slot_elems + off, h);
-        else h[0] = h[1] = h[2] = h[3] = hi_s;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          T z = q[v];
-#pragma unroll
-          for (int c = 0; c < R; ++c) z += (sg * u[c][v] * ie[v]) * sh.gz[c];
-          q[v] = clampv(z, l[v], h[v]);
-        }
-      };
-      T* qdst = qbuf + (long long)((k + 1) & 1) * g.slot_elems;
-      if (act) {
-        qrow(rowoff, qn4, ien, un);
-        Vec4<T>::st(qdst + rowoff, qn4);
-      }
-      if (halo && yr == 0 && y0 + TYe < K2) {
-        const long long off = (long long)(W * rpw) * K1 + xb;
-        T qb[4], ib[4], ub[R > 0 ? R : 1][4];
-        qrow(off, qb, ib, ub);
-        Vec4<T>::st(qdst + off, qb);
-      }
-    }
-
-    // ---- dual update at plane k (dual_tv_solver.py:225-235) -------------
-    const T qright = __shfl_down_sync(FULLM, qc[0], 1);  // x+1 of element 3
-    T src[3][4];
-    T vv[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int n = 0; n < 3; ++n) src[n][0] = src[n][1] = src[n][2] = src[n][3] = 0;
-    if (pin && act) {
-      const bool has_y = nd >= 2 && y < K2 - 1;
-      const bool has_up = nd >= 3 && k < K3 - 1;
-      T qy[4] = {0, 0, 0, 0};
-      if (has_y) Vec4<T>::rw(qbuf + (long long)(k & 1) * g.slot_elems + rowoff + K1, qy);
-      T pc4[3][4], pp4[3][4];
-#pragma unroll
-      for (int n = 0; n < 3; ++n) {
-        pc4[n][0] = pc4[n][1] = pc4[n][2] = pc4[n][3] = 0;
-        if (n < nd) Vec4<T>::rw(stg + (M.PC0 + n) * g.slot_elems + rowoff, pc4[n]);
-        if (n < nd && M.PP0 >= 0) Vec4<T>::rw(stg + (M.PP0 + n) * g.slot_elems + rowoff, pp4[n]);
-      }
-      T pn[3][4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        T gr[3];
-        const T right = (v < 3) ? qc[v + 1] : qright;
-        gr[0] = (xb + v < K1 - 1) ? right - qc[v] : (T)0;
-        gr[1] = has_y ? qy[v] - qc[v] : (T)0;
-        gr[2] = has_up ? qn4[v] - qc[v] : (T)0;
-        T w[3], pc3[3];
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          pc3[n] = pc4[n][v];
-          T pb = pc3[n];
-          if (M.PP0 >= 0 && n < nd) pb = pc3[n] + m_prev * (pc3[n] - pp4[n][v]);  // P_bar_{i-1} (:235)
-          w[n] = (n < nd) ? pb + step * gr[n] : (T)0;
-        }
-        if (iso) {
-          T ss = w[0] * w[0];
-          if (nd >= 2) ss += w[1] * w[1];
-          if (nd >= 3) ss += w[2] * w[2];
-          ball(w, ss);
-        } else {
-#pragma unroll
-          for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
-        }
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          pn[n][v] = w[n];
-          if (real && !warm && n < nd) {
-            const T df = w[n] - pc3[n];
-            fa[V::NRM] += df * df;
-            fa[V::NRM + 1] += pc3[n] * pc3[n];
-          }
-          src[n][v] = div_p ? w[n] : w[n] + m_cur * (w[n] - pc3[n]);
-        }
-      }
-      if (real && !warm) {
-        const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
-        if (!(A.dbg & 1)) {
-#pragma unroll
-          for (int n = 0; n < 3; ++n)
-            if (n < nd) Vec4<T>::st(Pn + n * N + j, pn[n]);
-        }
-        Vec4<T>::rw(stg + M.V * g.slot_elems + rowoff, vv);
-      }
-      if (nd >= 2) {
-        Vec4<T>::st(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff, src[1]);
-      }
-    }
-    const unsigned long long t_c = tr ? global_ns() : 0;
-    named_sync(1, W * 32);  // q(k+1), div-source rows published; stage b fully read
-    if (threadIdx.x == 0) mbar_arrive(&empty[b]);
-    if (tr) {
-      A.trace[4 * s + 0] = t_a;
-      A.trace[4 * s + 1] = t_b;
-      A.trace[4 * s + 2] = t_c;
-      A.trace[4 * s + 3] = global_ns();
-    }
-
-    // ---- a_i = v - reg D^-1 div(src) at plane k + Newton aggregates -----
-    const T left1 = __shfl_up_sync(FULLM, src[0][3], 1);
-    if (pin && !warm && used && !halo && !(A.dbg & 2)) {
-      T av[4] = {0, 0, 0, 0};
-      const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
-      if (real) {
-        T up[4] = {0, 0, 0, 0};
-        if (y > 0) Vec4<T>::rw(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff - K1, up);
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          if (sh.single) {
-            av[v] = vv[v];
-            continue;
-          }
-          const T lk = (v == 0) ? left1 : src[0][v - 1];
-          T dv = (xb + v < K1 - 1 ? -src[0][v] : (T)0) + (xb + v > 0 ? lk : (T)0);
-          if (nd >= 2) dv += (y < K2 - 1 ? -src[1][v] : (T)0) + (y > 0 ? up[v] : (T)0);
-          if (nd >= 3) dv += (k < K3 - 1 ? -src[2][v] : (T)0) + (k > 0 ? f3prev[v] : (T)0);
-          const T de = dv * iec[v];
-          av[v] = vv[v] - reg * de;
-#pragma unroll
-          for (int c = 0; c < R; ++c) fa[V::RHS + c] += uc[c][v] * (diag ? de : dv);
-        }
-        Vec4<T>::st(Aout + j, av);
-      }
-      T l[4], h[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) l[v] = lo_s, h[v] = hi_s;
-      if (real) {
-        if (A.lo_arr) Vec4<T>::ro(A.lo_arr + j, l);
-        if (A.hi_arr) Vec4<T>::ro(A.hi_arr + j, h);
-      }
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        bool nr = false;
-        if (real && R > 0) {
-          T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
-#pragma unroll
-          for (int c = 0; c < R; ++c) {
-            uv[c] = uc[c][v];
-            sv[c] = sg * uv[c] * iec[v];
-          }
-          nr = aggregate<T, R, NACC, T>(av[v], sv, uv, l[v], h[v], sh.gc, sh.gwid, fa);
-        }
-        near_push(nr, j + v, lane, near_seg, ncnt, ovf);
-      }
-    }
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) acc[q] += (double)fa[q];
-    // ---- carries -------------------------------------------------------
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      f3prev[v] = src[2][v];
-      qc[v] = qn4[v];
-      iec[v] = ien[v];
-#pragma unroll
-      for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][v] = un[c][v];
-    }
-    cons.advance();
-    ++s;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// The kernel
-// ---------------------------------------------------------------------------
-template <typename T, int R>
-struct FCfg {
-  static constexpr bool kLight = sizeof(T) == 4 && R <= 2;
-  // 11 row warps + 1 halo/producer warp = 384 threads -> ~168 registers
-  static constexpr int RW = kLight ? 11 : 7;
-  static constexpr int NT = (RW + 1) * 32;    // + 1 halo warp
-};
-
-template <typename T, int R>
-__global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A) {
-  using V = FV<R>;
-  constexpr int RW = FCfg<T, R>::RW;
-  constexpr int NT = FCfg<T, R>::NT;
-  constexpr int NACC = V::ACC;
-  constexpr int ROWS = 32 * (RW + 1);  // >= (RW + 1) * rpw rows of <= 128 voxels
-  __shared__ double s_red[kMaxVals];
-  __shared__ double s_bv[kMaxVals];
-  __shared__ double s_scr[(NT / 32) * kMaxVals];
-  __shared__ FCtl s_c;
-  __shared__ FShared<T> sh;
-  __shared__ int s_flag;
-  extern __shared__ __align__(16) unsigned char s_dyn[];
-  T* rows = reinterpret_cast<T*>(s_dyn);  // [2][ROWS_used][K1] y-exchange of the div source
-
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  __shared__ __align__(8) unsigned long long s_full[NSTAGE];
-  __shared__ __align__(8) unsigned long long s_empty[NSTAGE];
-  unsigned my_gen = 0;
-  if (threadIdx.x == 0) {
-    my_gen = ld_acquire_u32(A.bar + 1);
-    for (int i = 0; i < NSTAGE; ++i) {
-      mbar_init(&s_full[i], 1);
-      mbar_init(&s_empty[i], 1);
-    }
-    mbar_init_fence();
-  }
-  __syncthreads();
-  unsigned uses[NSTAGE] = {0u, 0u};
-
-  const long long N = A.N, plane = A.plane;
-  const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
-  const long long stride = (long long)gridDim.x * NT;
-  const long long gtid = (long long)blockIdx.x * NT + threadIdx.x;
-  const long long seg_begin = (long long)blockIdx.x * A.tile_planes / gridDim.x;
-  const long long seg_end = (long long)(blockIdx.x + 1) * A.tile_planes / gridDim.x;
-  const long long tp_s = (long long)((A.K2 + (A.geo.W - 1) * A.rpw - 1) / ((A.geo.W - 1) * A.rpw)) * A.K3;
-  const long long seg_begin_s = (long long)blockIdx.x * tp_s / gridDim.x;
-  const long long seg_end_s = (long long)(blockIdx.x + 1) * tp_s / gridDim.x;
-  const Fields<T, R> F{A.d, A.U, A.lo_arr, A.hi_arr, N, (T)A.tau, (T)A.lo, (T)A.hi, (T)A.sign};
-  const int lpr = A.lpr, rpw = A.rpw;
-  const int xr = lane % lpr, yr = lane / lpr, xb = 4 * xr;
-  const bool halo = warp == RW;
-  const int slot = halo ? yr : rpw + warp * rpw + yr;
-  const int TYe = RW * rpw;
-  const int rows_used = (RW + 1) * rpw;
-  (void)ROWS;
-  constexpr int NW = NT / 32;
-  int* my_seg = A.near_idx + ((long long)blockIdx.x * NW + warp) * CAPW;
-
-  int phase = F_SETUP;
-  while (true) {
-    double acc[NACC];
-#pragma unroll
-    for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
-    int nv = 0;
-
-    if (phase == F_SETUP) {
-      // gram partials U^T D^-1 U (wpm.py:50-56)
-      nv = V::S;
-      if (R > 0) {
-        for (long long j = gtid; j < N; j += stride) {
-          T u[R > 0 ? R : 1];
-#pragma unroll
-          for (int c = 0; c < R; ++c) u[c] = __ldg(A.U + (long long)c * N + j);
-          const T e = A.d ? __ldg(A.d + j) : (T)1;
-          int k = 0;
-#pragma unroll
-          for (int c = 0; c < R; ++c)
-#pragma unroll
-            for (int c2 = 0; c2 <= c; ++c2, ++k)
-              acc[k] += A.d ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
-        }
-      }
-    } else if (phase == F_FUSED) {
-      nv = V::PASS;
-      int ncnt = 0;
-      bool ovf = false;
-      fused_staged<T, R, NACC>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full, s_empty,
-                               uses, acc, my_seg, ncnt, ovf);
-      if (lane == 0) A.near_cnt[blockIdx.x * NW + warp] = ncnt;
-      if (ovf) acc[V::OVF] += 1.0;
-    } else if (phase == F_DIV) {
-      nv = V::PASS;
-      const bool fused = false;
-      const T* __restrict__ Pc = A.ring[sh.slot_cur];
-      const T* __restrict__ Pp = A.ring[sh.slot_prev];
-      T* __restrict__ Pn = A.ring[sh.slot_new];
-      const T* __restrict__ Ain = A.abuf[sh.a_cur];
-      T* __restrict__ Aout = A.abuf[sh.a_cur ^ 1];
-      const T m_prev = sh.m_prev, m_cur = sh.m_cur;
-      const bool div_p = sh.div_p;
-      const T step = (T)A.step, reg = (T)A.reg;
-      const bool iso = A.mode == BQ_TV_ISO;
-      const bool single = sh.single;
-      int ncnt = 0;
-      bool ovf = false;
-      int buf = 0;
-      long long pos = seg_begin;
-      while (pos < seg_end) {
-        const long long tile = pos / K3;
-        const int z0 = (int)(pos - tile * K3);
-        const int z1 = (int)min((long long)K3, z0 + (seg_end - pos));
-        pos += z1 - z0;
-        const int y0 = (int)tile * TYe;
-        const int y = halo ? (y0 - rpw + yr) : (y0 + warp * rpw + yr);
-        const bool act = y >= 0 && y < K2;
-        const bool has_y = nd >= 2 && y < K2 - 1;
-        const int zs = (z0 > 0 && nd >= 3) ? z0 - 1 : z0;
-        long long j = (long long)zs * plane + (long long)y * K1 + xb;
-        T qc[4] = {0, 0, 0, 0}, iec[4] = {1, 1, 1, 1}, uc[R > 0 ? R : 1][4];
-#pragma unroll
-        for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][0] = uc[c][1] = uc[c][2] = uc[c][3] = 0;
-        if (act) {
-          if (fused) F.q4x(Ain, j, sh.gz, qc, iec, uc);
-          else if (!halo) F.ieu4(j, iec, uc);
-        }
-        T f3prev[4] = {0, 0, 0, 0};
-        for (int z = zs; z < z1; ++z, j += plane) {
-          const bool warm = z < z0;
-          const bool has_up = nd >= 3 && z < K3 - 1;
-          T qu[4] = {0, 0, 0, 0}, ieu[4] = {1, 1, 1, 1}, uu[R > 0 ? R : 1][4];
-#pragma unroll
-          for (int c = 0; c < (R > 0 ? R : 1); ++c) uu[c][0] = uu[c][1] = uu[c][2] = uu[c][3] = 0;
-          T src[3][4];
-          T pcur[3][4];
-          if (fused) {
-            // ---- dual update at plane z (dual_tv_solver.py:225) ----------
-            T qy[4] = {0, 0, 0, 0};
-            if (act && has_up) F.q4x(Ain, j + plane, sh.gz, qu, ieu, uu);
-            if (act && has_y) F.q4(Ain, j + K1, sh.gz, qy);
-            const T qn = __shfl_down_sync(FULLM, qc[0], 1);
-            T pprev[3][4];
-#pragma unroll
-            for (int n = 0; n < 3; ++n) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) pcur[n][k] = 0, pprev[n][k] = 0;
-              if (act && n < nd) {
-                Vec4<T>::rw(Pc + n * N + j, pcur[n]);
-                if (m_prev != (T)0) Vec4<T>::rw(Pp + n * N + j, pprev[n]);
-              }
-            }
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              const T right = (k < 3) ? qc[k + 1] : qn;
-              T g[3];
-              g[0] = (xb + k < K1 - 1) ? right - qc[k] : (T)0;
-              g[1] = has_y ? qy[k] - qc[k] : (T)0;
-              g[2] = has_up ? qu[k] - qc[k] : (T)0;
-              T w[3];
-#pragma unroll
-              for (int n = 0; n < 3; ++n) {
-                // P_bar_{i-1} = p_{i-1} + m (p_{i-1} - p_{i-2})  (dual_tv_solver.py:235)
-                const T pb = (m_prev != (T)0) ? pcur[n][k] + m_prev * (pcur[n][k] - pprev[n][k]) : pcur[n][k];
-                w[n] = (n < nd) ? pb + step * g[n] : (T)0;
-              }
-              if (iso) {
-                T ss = w[0] * w[0];
-                if (nd >= 2) ss += w[1] * w[1];
-                if (nd >= 3) ss += w[2] * w[2];
-                ball(w, ss);
-              } else {
-#pragma unroll
-                for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
-              }
-#pragma unroll
-              for (int n = 0; n < 3; ++n) {
-                if (!halo && !warm && act && n < nd) {
-                  const T df = w[n] - pcur[n][k];
-                  acc[V::NRM] += (double)df * (double)df;
-                  acc[V::NRM + 1] += (double)pcur[n][k] * (double)pcur[n][k];
-                }
-                // div source: P_bar_i (or p_i on the last iteration)
-                src[n][k] = div_p ? w[n] : w[n] + m_cur * (w[n] - pcur[n][k]);
-                pprev[n][k] = w[n];  // reuse as p_i storage
-              }
-            }
-            if (!halo && !warm && act) {
-#pragma unroll
-              for (int n = 0; n < 3; ++n)
-                if (n < nd) Vec4<T>::st(Pn + n * N + j, pprev[n]);
-            }
-          } else {
-            // ---- standalone DIV: source P_bar = p + m (p - p_prev) read ----
-            if (!halo && act && has_up) F.ieu4(j + plane, ieu, uu);
-#pragma unroll
-            for (int n = 0; n < 3; ++n) {
-#pragma unroll
-              for (int k = 0; k < 4; ++k) src[n][k] = 0;
-              if (act && n < nd && !single) {
-                T pc4[4], pp4[4];
-                Vec4<T>::rw(Pc + n * N + j, pc4);
-                if (m_prev != (T)0) Vec4<T>::rw(Pp + n * N + j, pp4);
-#pragma unroll
-                for (int k = 0; k < 4; ++k)
-                  src[n][k] = (m_prev != (T)0) ? pc4[k] + m_prev * (pc4[k] - pp4[k]) : pc4[k];
-              }
-            }
-          }
-          // ---- y-exchange of the div source (component 2) through smem ----
-          if (nd >= 2) {
-#pragma unroll
-            for (int k = 0; k < 4; ++k) rows[((long long)buf * rows_used + slot) * K1 + xb + k] = src[1][k];
-          }
-          __syncthreads();
-          const T left1 = __shfl_up_sync(FULLM, src[0][3], 1);
-          if (!halo && !warm && act) {
-            // ---- a_i = v - reg D^-1 div(src)  (tv_ops.py:122-159) -------
-            T av[4], vv[4];
-            if (single) {
-              Vec4<T>::ro(A.v + j, av);
-            } else {
-              Vec4<T>::ro(A.v + j, vv);
-#pragma unroll
-              for (int k = 0; k < 4; ++k) {
-                const T lk = (k == 0) ? left1 : src[0][k - 1];
-                T dv = (xb + k < K1 - 1 ? -src[0][k] : (T)0) + (xb + k > 0 ? lk : (T)0);
-                if (nd >= 2) {
-                  const T up = (y > 0) ? rows[((long long)buf * rows_used + slot - 1) * K1 + xb + k] : (T)0;
-                  dv += (y < K2 - 1 ? -src[1][k] : (T)0) + up;
-                }
-                if (nd >= 3) dv += (z < K3 - 1 ? -src[2][k] : (T)0) + (z > 0 ? f3prev[k] : (T)0);
-                const T de = dv * iec[k];
-                av[k] = vv[k] - reg * de;
-#pragma unroll
-                for (int c = 0; c < R; ++c) acc[V::RHS + c] += (double)uc[c][k] * (double)(A.d ? de : dv);
-              }
-            }
-            Vec4<T>::st(Aout + j, av);
-            // ---- Newton aggregates + near list for the next Newton ------
-            T l[4], h[4];
-            F.bounds4(j, l, h);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-              T s[R > 0 ? R : 1], u[R > 0 ? R : 1];
-#pragma unroll
-              for (int c = 0; c < R; ++c) {
-                u[c] = uc[c][k];
-                s[c] = F.sg * u[c] * iec[k];
-              }
-              const bool nr = (R > 0) ? aggregate<T, R, NACC, double>(av[k], s, u, l[k], h[k], sh.gc, sh.gwid, acc) : false;
-              near_push(nr, j + k, lane, my_seg, ncnt, ovf);
-            }
-          } else if (!halo) {
-            // keep the warp's ballots aligned with the active lanes' calls
-#pragma unroll
-            for (int k = 0; k < 4; ++k) near_push(false, 0, lane, my_seg, ncnt, ovf);
-          }
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            f3prev[k] = src[2][k];
-            qc[k] = qu[k];
-            iec[k] = ieu[k];
-#pragma unroll
-            for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][k] = uu[c][k];
-          }
-          buf ^= 1;
-        }
-      }
-      if (lane == 0) A.near_cnt[blockIdx.x * NW + warp] = ncnt;
-      if (ovf) acc[V::OVF] += 1.0;
-    } else if (phase == F_NEWTON) {
-      // full-pass phi(beta) and generalized Jacobian partials (wpm.py:150-167)
-      nv = V::NEWTON;
-      const T* __restrict__ Ain = A.abuf[sh.a_cur];
-      for (long long j = gtid; j < N; j += stride) {
-        T av, s[R > 0 ? R : 1], u[R > 0 ? R : 1], l, h;
-        F.voxel(Ain, j, av, s, u, l, h);
-        T wv = av, z = av;
-#pragma unroll
-        for (int c = 0; c < R; ++c) {
-          wv += s[c] * sh.gw[c];
-          z += s[c] * sh.gz[c];
-        }
-        const T dl = wv - clampv(z, l, h);
-#pragma unroll
-        for (int c = 0; c < R; ++c) acc[c] += (double)u[c] * (double)dl;
-        if (z > l && z < h) {
-          int k = R;
-#pragma unroll
-          for (int c = 0; c < R; ++c)
-#pragma unroll
-            for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += (double)u[c] * (double)s[c2];
-        }
-      }
-    } else if (phase == F_FINAL) {
-      // x = clamp(a + s.gamma*) and P* back into the caller's buffer
-      const T* __restrict__ Ain = A.abuf[sh.a_cur];
-      T* __restrict__ X = A.x;
-      const T* __restrict__ Pfin = A.ring[sh.slot_cur];
-      const bool copy = !sh.single && sh.slot_cur != 0;
-      for (long long j = gtid; j < N; j += stride) {
-        T av, s[R > 0 ? R : 1], u[R > 0 ? R : 1], l, h;
-        F.voxel(Ain, j, av, s, u, l, h);
-        T z = av;
-#pragma unroll
-        for (int c = 0; c < R; ++c) z += s[c] * sh.gz[c];
-        X[j] = clampv(z, l, h);
-        if (copy)
-          for (int n = 0; n < nd; ++n) A.ring[0][n * N + j] = Pfin[n * N + j];
-      }
-    }
-
-    // ---- barrier with fused deterministic reduction ----------------------
-    const int cur = phase;
-    const bool barrier = cur != F_FINAL;
-    if (barrier) {
-      block_sum_to<NT, NACC>(acc, nv, s_bv, s_scr);
-      if (threadIdx.x < nv) A.partials[(size_t)blockIdx.x * kMaxVals + threadIdx.x] = s_bv[threadIdx.x];
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const unsigned old = atom_add_acqrel(A.bar, 1u);
-        s_flag = (old == gridDim.x - 1) ? 1 : 0;
-        if (s_flag) {
-          const double t_arr = __longlong_as_double((long long)global_ns());
-          s_red[kMaxVals - 1] = t_arr;
-        }
-      }
-      __syncthreads();
-      if (s_flag == 1) {
-        for (int k = warp; k < nv; k += NT / 32) {
-          double s = 0.0;
-          for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(&A.partials[(size_t)b * kMaxVals + k]);
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(FULLM, s, o);
-          if (lane == 0) {
-            s_red[k] = s;
-            __stcg(&A.red[k], s);
-          }
-        }
-        if (threadIdx.x == 0) __stcg(&A.red[kMaxVals - 1], s_red[kMaxVals - 1]);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          st_relaxed(A.bar, 0u);
-          red_add_release(A.bar + 1, 1u);
-        }
-      } else {
-        if (threadIdx.x == 0) {
-          const uint64_t t0 = global_ns();
-          unsigned spins = 0;
-          while (ld_acquire_u32(A.bar + 1) == my_gen) {
-            if (((++spins) & 4095u) == 0 && global_ns() - t0 > 20ull * 1000000000ull) {
-              s_flag = -1;
-              break;
-            }
-          }
-          fence_acq_rel();
-        }
-        __syncthreads();
-        if (s_flag == -1) {
-          if (blockIdx.x == 0 && threadIdx.x == 0) A.report->status = BQ_ETIMEOUT;
-          break;
-        }
-        if (threadIdx.x < nv) s_red[threadIdx.x] = __ldcg(&A.red[threadIdx.x]);
-        if (threadIdx.x == NT - 1) s_red[kMaxVals - 1] = __ldcg(&A.red[kMaxVals - 1]);
-      }
-      my_gen += 1;
-      __syncthreads();
-    }
-
-    // ---- controller (+ block-local Newton over the near list) ------------
-    if (threadIdx.x == 0) {
-      Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
-      ctl.timeline(cur, s_red, barrier);
-      ctl.run(cur, s_red);
-    }
-    __syncthreads();
-    // ---- stage the near list (usually tiny) into shared memory once ------
-    int n_near = 0;
-    bool near_in_smem = false;
-    constexpr int EW = 3 + 2 * (R > 0 ? R : 1);  // av, l, h, u[R], s[R]
-    T* ne = reinterpret_cast<T*>(s_dyn);
-    if (s_c.phase == F_NLOCAL) {
-      const int nseg = gridDim.x * NW;
-      const T* __restrict__ Ain = A.abuf[s_c.a_cur];
-      int mine = 0;
-      for (int sidx = threadIdx.x; sidx < nseg; sidx += NT) mine += __ldcg(&A.near_cnt[sidx]);
-      // block exclusive scan of `mine` (warp shuffles + smem, fixed order)
-      __shared__ int s_wsum[NT / 32];
-      int incl = mine;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int t = __shfl_up_sync(FULLM, incl, o);
-        if (lane >= o) incl += t;
-      }
-      if (lane == 31) s_wsum[warp] = incl;
-      __syncthreads();
-      int wbase = 0, total = 0;
-      for (int w2 = 0; w2 < NT / 32; ++w2) {
-        if (w2 < warp) wbase += s_wsum[w2];
-        total += s_wsum[w2];
-      }
-      n_near = total;
-      near_in_smem = (long long)total * EW * (long long)sizeof(T) <= (long long)A.dyn_bytes;
-      if (near_in_smem) {
-        int o = wbase + incl - mine;
-        for (int sidx = threadIdx.x; sidx < nseg; sidx += NT) {
-          const int cnt = __ldcg(&A.near_cnt[sidx]);
-          const int* seg = A.near_idx + (long long)sidx * CAPW;
-          for (int e = 0; e < cnt; ++e, ++o) {
-            T av, sv[R > 0 ? R : 1], uv[R > 0 ? R : 1], l, h;
-            F.voxel(Ain, (long long)__ldcg(&seg[e]), av, sv, uv, l, h);
-            T* d = ne + (long long)o * EW;
-            d[0] = av, d[1] = l, d[2] = h;
-#pragma unroll
-            for (int c = 0; c < R; ++c) d[3 + c] = uv[c], d[3 + R + c] = sv[c];
-          }
-        }
-      }
-      __syncthreads();
-    }
-    while (s_c.phase == F_NLOCAL) {
-      // phi(beta) = K0 + Cout gw + Cin beta + beta - sum_near u clamp(a + s.gamma)
-      double nacc[V::NEWTON > 0 ? V::NEWTON : 1];
-#pragma unroll
-      for (int k = 0; k < V::NEWTON; ++k) nacc[k] = 0.0;
-      T gz[R > 0 ? R : 1];
-#pragma unroll
-      for (int c = 0; c < R; ++c) gz[c] = (T)(s_c.gw[c] - s_c.beta[c]);
-      auto near_term = [&](T av, const T (&sv)[R > 0 ? R : 1], const T (&uv)[R > 0 ? R : 1], T l, T h) {
-        T z = av;
-#pragma unroll
-        for (int c = 0; c < R; ++c) z += sv[c] * gz[c];
-        const T cz = clampv(z, l, h);
-#pragma unroll
-        for (int c = 0; c < R; ++c) nacc[c] += (double)uv[c] * (double)cz;
-        if (z > l && z < h) {
-          int k = R;
-#pragma unroll
-          for (int c = 0; c < R; ++c)
-#pragma unroll
-            for (int c2 = 0; c2 <= c; ++c2, ++k) nacc[k] += (double)uv[c] * (double)sv[c2];
-        }
-      };
-      if (near_in_smem) {
-        for (int e = threadIdx.x; e < n_near; e += NT) {
-          const T* d = ne + (long long)e * EW;
-          T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
-#pragma unroll
-          for (int c = 0; c < R; ++c) uv[c] = d[3 + c], sv[c] = d[3 + R + c];
-          near_term(d[0], sv, uv, d[1], d[2]);
-        }
-      } else {
-        const T* __restrict__ Ain = A.abuf[s_c.a_cur];
-        const int nseg = gridDim.x * NW;
-        for (int sidx = threadIdx.x; sidx < nseg; sidx += NT) {
-          const int cnt = __ldcg(&A.near_cnt[sidx]);
-          const int* seg = A.near_idx + (long long)sidx * CAPW;
-          for (int e = 0; e < cnt; ++e) {
-            T av, sv[R > 0 ? R : 1], uv[R > 0 ? R : 1], l, h;
-            F.voxel(Ain, (long long)__ldcg(&seg[e]), av, sv, uv, l, h);
-            near_term(av, sv, uv, l, h);
-          }
-        }
-      }
-      block_sum_to<NT, (V::NEWTON > 0 ? V::NEWTON : 1)>(nacc, V::NEWTON, s_bv, s_scr);
-      if (threadIdx.x == 0) {
-        Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
-        double phi[R > 0 ? R : 1], hp[V::S > 0 ? V::S : 1];
-        for (int i = 0; i < R; ++i) {
-          double cw = 0.0, cb = 0.0;
-          for (int k2 = 0; k2 < R; ++k2) {
-            const int kk = i >= k2 ? i * (i + 1) / 2 + k2 : k2 * (k2 + 1) / 2 + i;
-            cw += s_c.Cout[kk] * s_c.gw[k2];
-            cb += s_c.Cin[kk] * s_c.beta[k2];
-          }
-          phi[i] = s_c.K0[i] + cw + cb - s_bv[i];
-        }
-        for (int k = 0; k < V::S; ++k) hp[k] = s_c.Cin[k] + s_bv[R + k];
-        ctl.timeline(F_NLOCAL, s_red, false);
-        s_c.local_steps += 1;
-        ctl.newton_step(phi, hp);
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      if (s_c.phase == F_FUSED) {
-        Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
-        ctl.prepare_fused();
-      }
-      sh.phase = s_c.phase;
-      sh.slot_cur = s_c.slot_cur;
-      sh.slot_prev = s_c.slot_prev;
-      sh.slot_new = (s_c.slot_cur == s_c.slot_prev) ? (s_c.slot_cur + 1) % 3 : 3 - s_c.slot_cur - s_c.slot_prev;
-      sh.a_cur = s_c.a_cur;
-      sh.iter = s_c.it;
-      sh.div_p = s_c.div_p;
-      sh.single = s_c.single;
-      sh.m_prev = (T)s_c.m_prev;
-      sh.m_cur = (T)s_c.m_cur;
-      for (int i = 0; i < R; ++i) {
-        sh.gw[i] = (T)s_c.gw[i];
-        sh.gz[i] = (T)(s_c.gw[i] - s_c.beta[i]);
-        sh.gc[i] = (T)s_c.gc[i];
-        sh.gwid[i] = (T)s_c.gwid[i];
-      }
-    }
-    __syncthreads();
-    phase = sh.phase;
-    if (phase == F_DONE) break;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// host side
-// ---------------------------------------------------------------------------
-bool al16(const void* p) { return p == nullptr || ((uintptr_t)p & 15u) == 0; }
-
-template <typename T, int R>
-int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t st) {
-  constexpr int RW = FCfg<T, R>::RW;
-  constexpr int NT = FCfg<T, R>::NT;
-  FArgs<T> A{};
-  A.ndim = D.ndim;
-  A.mode = D.mode;
-  A.sign = D.sign;
-  A.accelerated = D.accelerated;
-  A.max_iter = D.max_iter;
-  A.newton_max_iter = D.newton_max_iter;
-  A.wpm_only = wpm_only;
-  A.K1 = (int)D.dims[0];
-  A.K2 = (int)D.dims[1];
-  A.K3 = (int)D.dims[2];
-  A.N = D.dims[0] * D.dims[1] * D.dims[2];
-  A.plane = D.dims[0] * D.dims[1];
-  A.tau = D.tau;
-  A.reg = D.reg;
-  A.step = D.step;
-  A.eps = D.eps;
-  A.newton_eps = D.newton_eps;
-  A.lo = D.lo;
-  A.hi = D.hi;
-  A.lo_arr = (const T*)D.lo_arr;
-  A.hi_arr = (const T*)D.hi_arr;
-  A.d = (const T*)D.d;
-  A.U = (const T*)D.U;
-  A.v = (const T*)D.v;
-  A.ring[0] = (T*)D.p;
-  A.ring[1] = (T*)D.pb;
-  A.ring[2] = (T*)D.p2;
-  A.abuf[0] = (T*)D.a;
-  A.abuf[1] = (T*)D.a2;
-  A.x = (T*)D.x;
-  A.beta_io = D.beta;
-  A.report = (bq_wtv_report*)D.report;
-  A.partials = ctx->ws.partials;
-  A.red = (double*)ctx->ws.ctl;
-  A.bar = ctx->ws.barrier;
-  A.lpr = A.K1 / 4;
-  A.rpw = 32 / A.lpr;
-  const int TYe = RW * A.rpw;
-  A.nty = (A.K2 + TYe - 1) / TYe;
-  A.tile_planes = (long long)A.nty * A.K3;
-
-  auto kern = wtv_fused_kernel<T, R>;
-  // staged FUSED pass: widest tile whose double-buffered stage fits in smem
-  StageMap<R> M;
-  M.make(D.d != nullptr, D.lo_arr != nullptr, D.hi_arr != nullptr, D.ndim, true);
-  const size_t smem_cap = 200 * 1024;
-  int W = NT / 32 - 1;  // + 1 producer warp
-  const char* ns_env = getenv("BQ_PROX_STAGES");
-  const int nst = ns_env ? std::max(2, std::min(NSTAGE, atoi(ns_env))) : 2;
-  auto staged_bytes = [&](int w) {
-    const long long srw = (long long)w * A.rpw + 1;
-    return (size_t)(nst * M.nfield + 4) * srw * A.K1 * sizeof(T);
-  };
-  const char* w_env = getenv("BQ_PROX_WARPS");
-  if (w_env) W = std::max(2, std::min(W, atoi(w_env)));
-  while (W > 2 && staged_bytes(W) > smem_cap) --W;
-  BQ_CHECK(staged_bytes(W) <= smem_cap, BQ_EINVAL, "wtv_fused: stage does not fit in shared memory");
-  A.geo.W = W;
-  A.geo.nstage = nst;
-  A.geo.SRW = W * A.rpw + 1;
-  A.geo.slot_elems = (long long)A.geo.SRW * A.K1;
-  A.geo.stage_elems = (long long)M.nfield * A.geo.slot_elems;
-  const size_t dyn = std::max<size_t>(2ull * (RW + 1) * A.rpw * A.K1 * sizeof(T), staged_bytes(W));
-  BQ_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn + 1024));
-  int per_sm = 0;
-  BQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, dyn));
-  BQ_CHECK(per_sm > 0, BQ_ECUDA, "wtv_fused: kernel does not fit on an SM");
-  // one block per SM; small problems use fewer (cheaper barriers, enough work)
-  long long G = std::min<long long>(ctx->num_sms, A.tile_planes);
-  G = std::max<long long>(1, std::min<long long>(G, (A.N + 2047) / 2048));
-  {
-    const long long tp_s = (long long)((A.K2 + (W - 1) * A.rpw - 1) / ((W - 1) * A.rpw)) * A.K3;
-    G = std::min<long long>(G, tp_s);
-  }
-  G = std::min<long long>(G, kMaxBlocks);
-  // near-list workspace
-  const size_t need = (size_t)G * (NT / 32) * CAPW * sizeof(int) + (size_t)G * (NT / 32) * sizeof(int);
-  if (ctx->near_bytes < need) {
-    cudaFree(ctx->near_buf);
-    ctx->near_buf = nullptr;
-    ctx->near_bytes = 0;
-    BQ_CUDA(cudaMalloc(&ctx->near_buf, need));
-    ctx->near_bytes = need;
-  }
-  A.near_idx = (int*)ctx->near_buf;
-  A.near_cnt = A.near_idx + (size_t)G * (NT / 32) * CAPW;
-
-  A.dyn_bytes = (long long)dyn;
-  A.trace = getenv("BQ_PROX_TRACE") ? (unsigned long long*)ctx->ws.scratch : nullptr;
-  A.trace_pass = getenv("BQ_PROX_TRACE") ? atoi(getenv("BQ_PROX_TRACE")) : 0;
-  A.trace_thread = getenv("BQ_PROX_TRACE_THREAD") ? atoi(getenv("BQ_PROX_TRACE_THREAD")) : 0;
-  A.dbg = getenv("BQ_PROX_DBG") ? atoi(getenv("BQ_PROX_DBG")) : 0;
-  A.grow_min = getenv("BQ_PROX_GROW") ? atof(getenv("BQ_PROX_GROW")) : 8.0;
-  BQ_CUDA(cudaMemsetAsync(ctx->ws.barrier, 0, 2 * sizeof(unsigned), st));
-  void* args[] = {&A};
-  BQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)G), dim3(NT), args, dyn, st));
-  return BQ_OK;
-}
-
-}  // namespace
+using fused::al16;
+using fused::fused_launch;
 
 // Fast-path eligibility: 16-byte-aligned fields, K1 in {4, 8, ..., 128}
 // dividing 128, ring/ping-pong scratch supplied.
 bool fused_eligible(const bq_wtv_desc& D) {
   const long long K1 = D.dims[0];
+  if (D.ndim != 3) return false;
   if (!(K1 >= 4 && K1 <= 128 && K1 % 4 == 0 && 128 % K1 == 0)) return false;
   if (!D.p2 || !D.a2 || !D.pb || !D.p) return false;
   const void* ptrs[] = {D.p, D.pb, D.p2, D.a, D.a2, D.v, D.x, D.d, D.U, D.lo_arr, D.hi_arr};

@@ -1,0 +1,10 @@
+// explicit instantiations of the fused prox kernel (parallel compilation)
+#include "wtv_fused_impl.cuh"
+
+namespace bq {
+namespace fused {
+template int fused_launch<double, 0>(bq_ctx*, const bq_wtv_desc&, int, cudaStream_t);
+template int fused_launch<double, 1>(bq_ctx*, const bq_wtv_desc&, int, cudaStream_t);
+template int fused_launch<double, 2>(bq_ctx*, const bq_wtv_desc&, int, cudaStream_t);
+}  // namespace fused
+}  // namespace bq
