@@ -58,3 +58,25 @@ def ls_phantom(n: int, n_shapes: int, dn_lo: float, dn_hi: float, seed: int) -> 
         inside = np.sum((((pts - ctr) @ q) / ax) ** 2, axis=-1) <= 1.0
         vol[inside] = val
     return vol.reshape(-1)
+
+
+def born_spheres_phantom(n: int, seed: int, n_spheres: int = 3, dn_lo: float = 0.01, dn_hi: float = 0.05):
+    """Config 1: 3 random spheres (centres 0.3 + 0.4 U^3, radii linspace(0.32, 0.10, 3)
+    (0.8 + 0.4 U) as box fractions -- the reference law, forward_models.py:262-263 --
+    with dn ~ U[lo, hi]); later spheres overwrite earlier ones."""
+    rng = np.random.default_rng(seed)
+    c = (np.arange(n) + 0.5) / n
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    centres = 0.3 + 0.4 * rng.random((n_spheres, 3))
+    radii = np.linspace(0.32, 0.10, n_spheres) * (0.8 + 0.4 * rng.random(n_spheres))
+    dn = rng.uniform(dn_lo, dn_hi, n_spheres)
+    vol = np.zeros((n, n, n))
+    for ctr, r, val in zip(centres, radii, dn):
+        vol[(x - ctr[0]) ** 2 + (y - ctr[1]) ** 2 + (z - ctr[2]) ** 2 <= r * r] = val
+    return vol.reshape(-1)
+
+
+def complex_noise(y: np.ndarray, snr_db: float, rng) -> np.ndarray:
+    """Real-packed [Re; Im] Gaussian noise with 20 log10(||y|| / ||e||) = snr_db."""
+    e = rng.standard_normal(y.shape[0])
+    return e * (np.linalg.norm(y) / np.linalg.norm(e)) * 10.0 ** (-snr_db / 20.0)

@@ -66,6 +66,11 @@ class ScatterViewSet:
         self.iters_forward = []
         self.iters_adjoint = []
 
+    @property
+    def dtype(self):
+        """Real field dtype of x and of the gradient (the solver loop's working type)."""
+        return self.rdtype
+
     # -- plumbing ---------------------------------------------------------------
     def _st(self):
         return _abi.stream_ptr(self.device)
@@ -224,6 +229,55 @@ class ScatterViewSet:
             self.vjp_from_residual(x, vb, r, f, fp, u, grad, 1.0 / len(views), accumulate=not first)
             first = False
         return grad
+
+    def jvp(self, views, x, dx, f=None, fp=None, u=None):
+        """J_rho dx for the views of a batch (complex detector data)."""
+        if f is None:
+            f, fp = self.potential(x)
+        if u is None:
+            u, _ = self.total_field(f, views)
+        # q = f' u dx  (dx real, one N-vector shared by the batch)
+        q = torch.empty_like(u)
+        fpdx = torch.empty_like(f)
+        self._check(self.lib.bq_pointwise(self.ctx, self.code, 2, self.N, None, fp.data_ptr(), dx.data_ptr(), 0.0,
+                                          fpdx.data_ptr(), self._st()), "pointwise")
+        self._check(self.lib.bq_cscale_real(self.ctx, self.code, self.N, u.shape[0], fpdx.data_ptr(), u.data_ptr(),
+                                            q.data_ptr(), self._st()), "cscale")
+        if self.model == "ls":
+            rhs = self.conv(0, None, q)  # G_dom q
+            z, _ = self.bicgstab(lambda v: self.conv(0, f, v, 1.0, -1.0), rhs)
+            fz = self._cmul_conj_f(f, z)  # f real: f . z
+            q = q + fz
+        return self.conv(2, None, q)
+
+    def gauss_newton_subset(self, views, x, v):
+        """(1/|S|) sum_rho J_rho^T J_rho v (solvers.py:176-181), batched."""
+        views = list(views)
+        out = torch.zeros(self.N, dtype=self.rdtype, device=self.device)
+        f, fp = self.potential(x)
+        first = True
+        for i in range(0, len(views), self.batch):
+            vb = views[i:i + self.batch]
+            u, _ = self.total_field(f, vb)
+            jv = self.jvp(vb, x, v, f, fp, u)
+            self.vjp_from_residual(x, vb, jv, f, fp, u, out, 1.0 / len(views), accumulate=not first)
+            first = False
+        return out
+
+    def mean_adjoint_measurements(self, views):
+        """(1/L) sum_rho J_rho(0)^T y_rho (solvers.py:192-199)."""
+        views = list(views)
+        x0 = torch.zeros(self.N, dtype=self.rdtype, device=self.device)
+        out = torch.zeros_like(x0)
+        f, fp = self.potential(x0)
+        first = True
+        for i in range(0, len(views), self.batch):
+            vb = views[i:i + self.batch]
+            u = self.incident(vb)  # f = 0: the total field is the incident one
+            self.vjp_from_residual(x0, vb, self.unpack(self.y[vb]), f, fp, u, out, 1.0 / len(views),
+                                   accumulate=not first)
+            first = False
+        return out
 
     def costs(self, views, x):
         views = list(views)

@@ -239,6 +239,42 @@ def main():
 
     np.savez_compressed(OUT / "reference_golden.npz", **out)
     print(f"wrote {OUT / 'reference_golden.npz'} ({len(out)} arrays)")
+    make_config1_golden(tv_ops, wpm, solvers, fm)
+
+
+def make_config1_golden(tv_ops, wpm, solvers, fm):
+    """Config 1 end to end: the REFERENCE bqnpm_run driving the builder's CPU
+    first-Born oracle (oracle/physics.py, complex128) through the reference's
+    own ViewProblem plugin type (forward_models.py:25-83)."""
+    import time
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    from oracle import physics as P
+    from paper_2307_02043_b200.configs import born_spheres_phantom, complex_noise
+
+    n, L = 32, 16
+    s = P.Setup(n=n, n_views=L, theta_deg=35.0)
+    m = P.ScatterModel(s, "born")
+    xgt = born_spheres_phantom(n, seed=1000)
+    rng = np.random.default_rng(1001)
+    ys = []
+    for l in range(L):
+        y = m.forward(xgt, l)
+        ys.append(y + complex_noise(y, 30.0, rng))
+    views = [fm.ViewProblem(lambda x, l=l: m.forward(x, l), lambda x, v, l=l: m.jvp(x, l, v),
+                            lambda x, z, l=l: m.vjp(x, l, z), ys[l], view_id=l) for l in range(L)]
+    grid = tv_ops.Grid((n, n, n))
+    box = wpm.BoxSet(0.0, 0.1)
+    t0 = time.time()
+    x0 = solvers.default_initializer(views, grid, box)
+    parts = solvers.partition_views(L, 4)
+    alphas = solvers.estimate_subset_lipschitz(views, parts, x0, 30, 1.05, 0)
+    cfg = solvers.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=20, box=box, seed=0, alphas=alphas)
+    x, tr = solvers.bqnpm_run(views, grid, cfg, x0=x0, ground_truth=xgt)
+    out = {"c1_y": np.array(ys), "c1_xgt": xgt, "c1_x0": x0, "c1_alphas": alphas, "c1_x": x,
+           "c1_cost": tr.column("cost"), "c1_inner": tr.column("inner_iters"), "c1_snr": tr.column("snr_db")}
+    np.savez_compressed(OUT / "config1_golden.npz", **out)
+    print(f"wrote config1_golden.npz in {time.time() - t0:.1f} s; final SNR {tr.column('snr_db')[-1]:.2f} dB")
 
 
 if __name__ == "__main__":

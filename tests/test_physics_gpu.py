@@ -80,3 +80,31 @@ def test_batched_equals_unbatched():
     fa = a.forward(xt, [0, 1, 2, 3, 4]).cpu().numpy()
     fb = np.concatenate([b.forward(xt, [l]).cpu().numpy() for l in range(5)])
     assert rel_l2(fa, fb) <= 1e-12
+
+
+def test_config1_bqnpm_matches_reference_loop():
+    """BASELINE config 1 end to end (first Born, 32^3, c128, L=16, K_s=4, 20 outer
+    iterations, lambda 1e-3, box [0, 0.1]): the device BQNPM loop on device Born
+    views vs the REFERENCE bqnpm_run driving the CPU Born oracle
+    (tests/golden/config1_golden.npz).  North star: reconstruction <= 1e-3."""
+    from pathlib import Path
+
+    from paper_2307_02043_b200 import solvers as S
+    from paper_2307_02043_b200.tv_ops import Grid
+    from paper_2307_02043_b200.wpm import BoxSet
+
+    z = np.load(Path(__file__).parent / "golden" / "config1_golden.npz")
+    views, vs = PH.make_scatter_views(32, 16, model="born", dtype=torch.complex128, theta_deg=35.0, batch=8)
+    vs.y.copy_(torch.tensor(z["c1_y"], device="cuda"))
+    grid = Grid((32, 32, 32))
+    box = BoxSet(0.0, 0.1)
+    x0 = S.default_initializer(views, grid, box)
+    assert rel_l2(x0.cpu().numpy(), z["c1_x0"]) <= 1e-10
+    al = S.estimate_subset_lipschitz(views, S.partition_views(16, 4), x0, 30, 1.05, 0)
+    np.testing.assert_allclose(al, z["c1_alphas"], rtol=1e-9)
+    cfg = S.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=20, box=box, seed=0, alphas=z["c1_alphas"])
+    x, tr = S.bqnpm_run(views, grid, cfg, x0=z["c1_x0"], ground_truth=z["c1_xgt"])
+    assert rel_l2(x, z["c1_x"]) <= 1e-3
+    assert rel_l2(x, z["c1_x"]) <= 1e-8  # measured: far inside the north-star bound
+    np.testing.assert_allclose(tr.column("cost"), z["c1_cost"], rtol=1e-8)
+    np.testing.assert_array_equal(tr.column("inner_iters"), z["c1_inner"])
