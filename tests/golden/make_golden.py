@@ -240,6 +240,7 @@ def main():
     np.savez_compressed(OUT / "reference_golden.npz", **out)
     print(f"wrote {OUT / 'reference_golden.npz'} ({len(out)} arrays)")
     make_config1_golden(tv_ops, wpm, solvers, fm)
+    make_config3_small_golden(tv_ops, wpm, solvers, fm)
 
 
 def make_config1_golden(tv_ops, wpm, solvers, fm):
@@ -275,6 +276,43 @@ def make_config1_golden(tv_ops, wpm, solvers, fm):
            "c1_cost": tr.column("cost"), "c1_inner": tr.column("inner_iters"), "c1_snr": tr.column("snr_db")}
     np.savez_compressed(OUT / "config1_golden.npz", **out)
     print(f"wrote config1_golden.npz in {time.time() - t0:.1f} s; final SNR {tr.column('snr_db')[-1]:.2f} dB")
+
+
+
+
+def make_config3_small_golden(tv_ops, wpm, solvers, fm):
+    """Config 3 law at reduced size (LS, n=20 padded to 40^3, L=8, K_s=4, 4 outer
+    iterations, 5 ellipsoids dn~U[0.02,0.08], 30 dB): the REFERENCE bqnpm_run
+    driving the CPU LS oracle with converged BiCGSTAB (tol 1e-12)."""
+    import time
+
+    sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
+    from oracle import physics as P
+    from paper_2307_02043_b200.configs import complex_noise, ls_phantom
+
+    n, L = 20, 8
+    s = P.Setup(n=n, n_views=L, theta_deg=35.0)
+    m = P.ScatterModel(s, "ls", tol=1e-12, max_iter=1000)
+    xgt = ls_phantom(n, 5, 0.02, 0.08, seed=3000)
+    rng = np.random.default_rng(3001)
+    ys = []
+    for l in range(L):
+        y = m.forward(xgt, l)
+        ys.append(y + complex_noise(y, 30.0, rng))
+    views = [fm.ViewProblem(lambda x, l=l: m.forward(x, l), lambda x, v, l=l: m.jvp(x, l, v),
+                            lambda x, z, l=l: m.vjp(x, l, z), ys[l], view_id=l) for l in range(L)]
+    grid = tv_ops.Grid((n, n, n))
+    box = wpm.BoxSet(0.0, 0.1)
+    t0 = time.time()
+    x0 = solvers.default_initializer(views, grid, box)
+    parts = solvers.partition_views(L, 4)
+    alphas = solvers.estimate_subset_lipschitz(views, parts, x0, 10, 1.05, 0)
+    cfg = solvers.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=4, box=box, seed=0, alphas=alphas)
+    x, tr = solvers.bqnpm_run(views, grid, cfg, x0=x0, ground_truth=xgt)
+    out = {"c3_y": np.array(ys), "c3_xgt": xgt, "c3_x0": x0, "c3_alphas": alphas, "c3_x": x,
+           "c3_cost": tr.column("cost"), "c3_inner": tr.column("inner_iters")}
+    np.savez_compressed(OUT / "config3s_golden.npz", **out)
+    print(f"wrote config3s_golden.npz in {time.time() - t0:.1f} s")
 
 
 if __name__ == "__main__":

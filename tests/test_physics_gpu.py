@@ -108,3 +108,30 @@ def test_config1_bqnpm_matches_reference_loop():
     assert rel_l2(x, z["c1_x"]) <= 1e-8  # measured: far inside the north-star bound
     np.testing.assert_allclose(tr.column("cost"), z["c1_cost"], rtol=1e-8)
     np.testing.assert_array_equal(tr.column("inner_iters"), z["c1_inner"])
+
+
+def test_config3_law_ls_bqnpm_matches_reference_loop():
+    """Config-3 law at reduced size (LS, n=20 padded to 40^3, L=8, K_s=4, 4 outer
+    iterations): the device BQNPM loop on device LS views (BiCGSTAB to 1e-12)
+    vs the REFERENCE bqnpm_run driving the CPU LS oracle."""
+    from pathlib import Path
+
+    from paper_2307_02043_b200 import solvers as S
+    from paper_2307_02043_b200.tv_ops import Grid
+    from paper_2307_02043_b200.wpm import BoxSet
+
+    z = np.load(Path(__file__).parent / "golden" / "config3s_golden.npz")
+    views, vs = PH.make_scatter_views(20, 8, model="ls", dtype=torch.complex128, theta_deg=35.0, batch=4,
+                                      tol=1e-12, max_iter=1000)
+    vs.y.copy_(torch.tensor(z["c3_y"], device="cuda"))
+    grid = Grid((20, 20, 20))
+    box = BoxSet(0.0, 0.1)
+    x0 = S.default_initializer(views, grid, box)
+    assert rel_l2(x0.cpu().numpy(), z["c3_x0"]) <= 1e-10
+    al = S.estimate_subset_lipschitz(views, S.partition_views(8, 4), x0, 10, 1.05, 0)
+    np.testing.assert_allclose(al, z["c3_alphas"], rtol=1e-8)
+    cfg = S.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=4, box=box, seed=0, alphas=z["c3_alphas"])
+    x, tr = S.bqnpm_run(views, grid, cfg, x0=z["c3_x0"])
+    assert rel_l2(x, z["c3_x"]) <= 1e-3
+    assert rel_l2(x, z["c3_x"]) <= 1e-7
+    np.testing.assert_allclose(tr.column("cost"), z["c3_cost"], rtol=1e-7)
