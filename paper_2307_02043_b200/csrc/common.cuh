@@ -46,6 +46,14 @@ struct Workspace {
 
 }  // namespace bq
 
+struct bq_ctx;
+namespace bq {
+// ls_fft.cu: padded-Green convolution as pruned line passes; returns 1 when the
+// size has no instantiation (the caller then uses the cuFFT path).
+int ls_conv_pruned(bq_ctx* ctx, int dtype, int n, int B, int op, const void* khat, const void* f, const void* v,
+                   double alpha, double beta, const void* addend, void* scratch, void* out, cudaStream_t st);
+}  // namespace bq
+
 struct bq_ctx {
   int device = 0;
   int num_sms = 0;

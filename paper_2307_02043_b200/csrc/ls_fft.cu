@@ -1,0 +1,517 @@
+// ls_fft.cu — pruned, fused padded-Green convolution for the Born/LS views.
+//
+// Computes exactly what oracle/physics.py Green.apply_full does -- the aperiodic
+// convolution of a field on the n^3 domain with the Green kernel K on the
+// (2n)^3 padded grid, via K_hat = FFT(K) -- but never materialises the padded
+// grid.  The 3-D transform is split into five batched line passes:
+//
+//   XF  rows  (z<nz_in, y<n)  : x-DFT of the n inputs (zero-padded to m)  -> Hx [z][y<n][x<m]
+//   YF  cols  (z<nz_in, x<m)  : y-DFT of the n inputs                      -> Q  [z][y<m][x<m]
+//   ZC  cols  (y<m,   x<m)    : z-DFT of the nz_in inputs, * K_hat (or conj), inverse z-DFT,
+//                               keep the nz_out output planes (in place)    -> Q
+//   YI  cols  (z<nz_out, x<m) : inverse y-DFT, keep y < n                   -> Hx
+//   XI  rows  (z<nz_out, y<n) : inverse x-DFT, keep x < n, fused epilogue   -> out
+//
+// so the zero half of every line is neither read nor transformed, the two
+// z-transforms and the spectral multiply share registers, and the padded
+// grid's 8N values are only ever touched as the 4N (y,x)-padded planes of Q.
+// HBM traffic per view drops from ~130N to ~28N complex words.
+// K is even in every axis (offsets i and m-i have the same length), so K_hat
+// is read through the folded index min(k, m-k): only its (n+1)^3 octant is
+// touched and it stays L2-resident across the views of a batch.
+//
+// Each line of length m = R1*R2 is a four-step DFT held by C threads:
+//   step 1: thread t owns n1 = t + C s; DFT-R2 over n2 of x[n1 + R1 n2] in
+//           registers, twiddle w_m^(n1 k2), exchange through shared memory;
+//   step 3: thread t owns k2 = t + C s; DFT-R1 over n1 -> X[k2 + R2 k1].
+// In ZC the forward result is exactly the register layout the inverse
+// (R1' = R2, R2' = R1) needs for its own step 1, so the spectral multiply and
+// the inverse's first DFT happen without touching shared memory.
+#include <cstdlib>
+
+#include "common.cuh"
+#include "ls_twiddle.cuh"
+
+namespace bq {
+namespace lsfft {
+
+template <typename T>
+struct CV;
+template <>
+struct CV<float> {
+  using V = float2;
+};
+template <>
+struct CV<double> {
+  using V = double2;
+};
+
+template <typename V>
+__device__ __forceinline__ V cadd(V a, V b) {
+  a.x += b.x;
+  a.y += b.y;
+  return a;
+}
+template <typename V>
+__device__ __forceinline__ V csub(V a, V b) {
+  a.x -= b.x;
+  a.y -= b.y;
+  return a;
+}
+template <typename V>
+__device__ __forceinline__ V cmul(V a, V b) {
+  V r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+
+// a * exp(DIR 2 pi i k / 32); k is a compile-time constant after unrolling
+template <int DIR, typename V>
+__device__ __forceinline__ V tw32(V a, int k) {
+  using T = decltype(a.x);
+  k &= 31;
+  if (k == 0) return a;
+  V r;
+  if (k == 16) {
+    r.x = -a.x;
+    r.y = -a.y;
+    return r;
+  }
+  if (k == 8) {  // * (DIR i)
+    r.x = DIR > 0 ? -a.y : a.y;
+    r.y = DIR > 0 ? a.x : -a.x;
+    return r;
+  }
+  if (k == 24) {  // * (-DIR i)
+    r.x = DIR > 0 ? a.y : -a.y;
+    r.y = DIR > 0 ? -a.x : a.x;
+    return r;
+  }
+  const T c = (T)cos32(k), s = (T)(DIR > 0 ? sin32(k) : -sin32(k));
+  r.x = a.x * c - a.y * s;
+  r.y = a.x * s + a.y * c;
+  return r;
+}
+
+template <int R>
+__host__ __device__ constexpr int brev(int k) {
+  int r = 0;
+  for (int b = 1; b < R; b <<= 1) {
+    r = (r << 1) | (k & 1);
+    k >>= 1;
+  }
+  return r;
+}
+
+// in-register DFT of length R (power of two <= 32), natural order in and out,
+// X[k] = sum_n a[n] exp(DIR 2 pi i n k / R)   (radix-2 decimation in frequency)
+template <int R, int DIR, typename V>
+__device__ __forceinline__ void dft(V (&a)[R]) {
+#pragma unroll
+  for (int half = R / 2; half >= 1; half >>= 1) {
+#pragma unroll
+    for (int base = 0; base < R; base += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const V u = a[base + j], v = a[base + j + half];
+        a[base + j] = cadd(u, v);
+        a[base + j + half] = tw32<DIR>(csub(u, v), j * (32 / (2 * half)));
+      }
+    }
+  }
+  V t[R];
+#pragma unroll
+  for (int k = 0; k < R; ++k) t[k] = a[brev<R>(k)];
+#pragma unroll
+  for (int k = 0; k < R; ++k) a[k] = t[k];
+}
+
+// shared-memory position of Y[n1][k2] for line l.  COL: lines are adjacent
+// columns and l is the fastest index; rows: each line's slab is padded so the
+// step-3 reads (stride R1+1) are bank-conflict free.
+template <int R1, int R2, int L, bool COL>
+__device__ __forceinline__ int spos(int l, int n1, int k2) {
+  return COL ? (k2 * R1 + n1) * L + l : l * (R2 * (R1 + 1)) + k2 * (R1 + 1) + n1;
+}
+
+template <int R1, int R2, int L, bool COL>
+constexpr int smem_elems() {
+  return COL ? R1 * R2 * L : L * R2 * (R1 + 1);
+}
+
+// step 1: a[s][n2] = x[n1 + R1 n2] (n1 = t + C s) -> smem Y[n1][k2] w_m^(DIR n1 k2)
+template <int R1, int R2, int C, int L, bool COL, int DIR, typename V>
+__device__ __forceinline__ void step1(V (&a)[R1 / C][R2], V* sm, const V* tw, int l, int t) {
+  constexpr int M = R1 * R2;
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s) {
+    dft<R2, DIR>(a[s]);
+    const int n1 = t + C * s;
+#pragma unroll
+    for (int k2 = 0; k2 < R2; ++k2) {
+      V w = tw[(n1 * k2) & (M - 1)];
+      if (DIR > 0) w.y = -w.y;
+      sm[spos<R1, R2, L, COL>(l, n1, k2)] = cmul(a[s][k2], w);
+    }
+  }
+}
+
+// step 3: b[s][k1] = X[k2 + R2 k1], k2 = t + C s
+template <int R1, int R2, int C, int L, bool COL, int DIR, typename V>
+__device__ __forceinline__ void step3(V (&b)[R2 / C][R1], const V* sm, int l, int t) {
+#pragma unroll
+  for (int s = 0; s < R2 / C; ++s) {
+    const int k2 = t + C * s;
+#pragma unroll
+    for (int n1 = 0; n1 < R1; ++n1) b[s][n1] = sm[spos<R1, R2, L, COL>(l, n1, k2)];
+    dft<R1, DIR>(b[s]);
+  }
+}
+
+template <typename V, int M>
+__device__ __forceinline__ void load_twiddles(V* tw, int tid, int nt) {
+  for (int i = tid; i < M; i += nt) {
+    const double2 w = g_tw512[i * (512 / M)];
+    V v;
+    v.x = (decltype(v.x))w.x;
+    v.y = (decltype(v.x))w.y;
+    tw[i] = v;
+  }
+}
+
+template <typename V>
+__device__ __forceinline__ V czero() {
+  V v;
+  v.x = 0;
+  v.y = 0;
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// XF: forward x pass over rows (row = z*n + y, rows = nz_in*n) of the compact
+// input (f .* v, or the detector residual plane), zero-padded to m.
+// ---------------------------------------------------------------------------
+template <typename T, int R1, int R2, int C, int L>
+__global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __restrict__ f,
+                                                  const typename CV<T>::V* __restrict__ v,
+                                                  typename CV<T>::V* __restrict__ hx) {
+  using V = typename CV<T>::V;
+  constexpr int M = R1 * R2;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* tw = (V*)smraw;
+  V* sm = tw + M;
+  const int tid = threadIdx.x, l = tid / C, t = tid % C;
+  const int b = blockIdx.x, row = blockIdx.y * L + l;
+  const bool ok = row < rows;
+  load_twiddles<V, M>(tw, tid, C * L);
+  const V* src = v + ((long long)b * rows + row) * n;
+  const T* fr = f ? f + (long long)row * n : nullptr;
+  V a[R1 / C][R2];
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+      const int e = t + C * s + R1 * n2;
+      V x = czero<V>();
+      if (ok && e < n) {
+        x = src[e];
+        if (fr) {
+          const T g = fr[e];
+          x.x *= g;
+          x.y *= g;
+        }
+      }
+      a[s][n2] = x;
+    }
+  __syncthreads();
+  step1<R1, R2, C, L, false, -1>(a, sm, tw, l, t);
+  __syncthreads();
+  V c[R2 / C][R1];
+  step3<R1, R2, C, L, false, -1>(c, sm, l, t);
+  if (ok) {
+    V* dst = hx + ((long long)b * n * n + row) * M;
+#pragma unroll
+    for (int s = 0; s < R2 / C; ++s)
+#pragma unroll
+      for (int k1 = 0; k1 < R1; ++k1) dst[t + C * s + R2 * k1] = c[s][k1];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// YF: forward y pass over columns (z < nz_in, x < m): Hx[z][y<n][x] -> Q[z][y<m][x]
+// ---------------------------------------------------------------------------
+template <typename T, int R1, int R2, int C, int L>
+__global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V* __restrict__ hx,
+                                                  typename CV<T>::V* __restrict__ q) {
+  using V = typename CV<T>::V;
+  constexpr int M = R1 * R2, XT = M / L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* tw = (V*)smraw;
+  V* sm = tw + M;
+  const int tid = threadIdx.x, l = tid % L, t = tid / L;
+  const int b = blockIdx.x, z = blockIdx.y / XT, x = (blockIdx.y % XT) * L + l;
+  load_twiddles<V, M>(tw, tid, C * L);
+  const V* src = hx + ((long long)b * n + z) * n * M + x;
+  V a[R1 / C][R2];
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+      const int e = t + C * s + R1 * n2;
+      a[s][n2] = e < n ? src[(long long)e * M] : czero<V>();
+    }
+  __syncthreads();
+  step1<R1, R2, C, L, true, -1>(a, sm, tw, l, t);
+  __syncthreads();
+  V c[R2 / C][R1];
+  step3<R1, R2, C, L, true, -1>(c, sm, l, t);
+  V* dst = q + ((long long)b * n + z) * M * M + x;
+#pragma unroll
+  for (int s = 0; s < R2 / C; ++s)
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) dst[(long long)(t + C * s + R2 * k1) * M] = c[s][k1];
+}
+
+// ---------------------------------------------------------------------------
+// ZC: z pass over columns (y < m, x < m), in place in Q:
+//   forward z-DFT of planes [z0, z0+nzi), * K_hat (conj if adj),
+//   inverse z-DFT, keep planes [zo0, zo0+nzo) -> Q slots 0..nzo-1.
+// ---------------------------------------------------------------------------
+template <typename T, int R1, int R2, int C, int L>
+__global__ void __launch_bounds__(C* L) zc_kernel(int n, int z0, int nzi, int zo0, int nzo, int adj,
+                                                  const typename CV<T>::V* __restrict__ khat,
+                                                  typename CV<T>::V* __restrict__ q) {
+  using V = typename CV<T>::V;
+  constexpr int M = R1 * R2, XT = M / L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* tw = (V*)smraw;
+  V* sm = tw + M;
+  const int tid = threadIdx.x, l = tid % L, t = tid / L;
+  const int b = blockIdx.x, y = blockIdx.y / XT, x = (blockIdx.y % XT) * L + l;
+  load_twiddles<V, M>(tw, tid, C * L);
+  V* col = q + (long long)b * n * M * M + (long long)y * M + x;
+  const long long zs = (long long)M * M;
+  V a[R1 / C][R2];
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) {
+      const int e = t + C * s + R1 * n2;
+      a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
+    }
+  __syncthreads();
+  step1<R1, R2, C, L, true, -1>(a, sm, tw, l, t);
+  __syncthreads();
+  V c[R2 / C][R1];
+  step3<R1, R2, C, L, true, -1>(c, sm, l, t);
+  // spectral multiply: c[s][k1] = X[kz], kz = k2 + R2 k1, k2 = t + C s
+  const int fy = y <= n ? y : M - y, fx = x <= n ? x : M - x;
+  const V* kcol = khat + (long long)fy * M + fx;
+#pragma unroll
+  for (int s = 0; s < R2 / C; ++s)
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int kz = t + C * s + R2 * k1;
+      const int fz = kz <= n ? kz : M - kz;
+      V k = kcol[(long long)fz * zs];
+      if (adj) k.y = -k.y;
+      c[s][k1] = cmul(c[s][k1], k);
+    }
+  __syncthreads();  // step-3 reads of sm are done before it is rewritten
+  // inverse with (R1', R2') = (R2, R1): c[s][n2'] = x'[n1' + R2 n2'], n1' = t + C s
+  step1<R2, R1, C, L, true, 1>(c, sm, tw, l, t);
+  __syncthreads();
+  V o[R1 / C][R2];
+  step3<R2, R1, C, L, true, 1>(o, sm, l, t);
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+    for (int k1 = 0; k1 < R2; ++k1) {
+      const int z = t + C * s + R1 * k1;
+      if (z >= zo0 && z < zo0 + nzo) col[(z - zo0) * zs] = o[s][k1];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// YI: inverse y pass over columns (z < nz_out, x < m): Q[z][y<m][x] -> Hx[z][y<n][x]
+// ---------------------------------------------------------------------------
+template <typename T, int R1, int R2, int C, int L>
+__global__ void __launch_bounds__(C* L) yi_kernel(int n, const typename CV<T>::V* __restrict__ q,
+                                                  typename CV<T>::V* __restrict__ hx) {
+  using V = typename CV<T>::V;
+  constexpr int M = R1 * R2, XT = M / L;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* tw = (V*)smraw;
+  V* sm = tw + M;
+  const int tid = threadIdx.x, l = tid % L, t = tid / L;
+  const int b = blockIdx.x, z = blockIdx.y / XT, x = (blockIdx.y % XT) * L + l;
+  load_twiddles<V, M>(tw, tid, C * L);
+  const V* src = q + ((long long)b * n + z) * M * M + x;
+  V a[R1 / C][R2];
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) a[s][n2] = src[(long long)(t + C * s + R1 * n2) * M];
+  __syncthreads();
+  step1<R1, R2, C, L, true, 1>(a, sm, tw, l, t);
+  __syncthreads();
+  V c[R2 / C][R1];
+  step3<R1, R2, C, L, true, 1>(c, sm, l, t);
+  V* dst = hx + ((long long)b * n + z) * n * M + x;
+#pragma unroll
+  for (int s = 0; s < R2 / C; ++s)
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int k = t + C * s + R2 * k1;
+      if (k < n) dst[(long long)k * M] = c[s][k1];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// XI: inverse x pass over rows (rows = nz_out*n), keep x < n, fused epilogue
+// (views_ls.cu crop_kernel / det_kernel semantics):
+//   out = beta * scale * (fconj .* G) + alpha * v + addend
+// ---------------------------------------------------------------------------
+template <typename T, int R1, int R2, int C, int L>
+__global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typename CV<T>::V* __restrict__ hx,
+                                                  double scale, const T* __restrict__ fconj,
+                                                  const typename CV<T>::V* __restrict__ v, double alpha, double beta,
+                                                  const typename CV<T>::V* __restrict__ addend,
+                                                  typename CV<T>::V* __restrict__ out) {
+  using V = typename CV<T>::V;
+  constexpr int M = R1 * R2;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  V* tw = (V*)smraw;
+  V* sm = tw + M;
+  const int tid = threadIdx.x, l = tid / C, t = tid % C;
+  const int b = blockIdx.x, row = blockIdx.y * L + l;
+  const bool ok = row < rows;
+  load_twiddles<V, M>(tw, tid, C * L);
+  const V* src = hx + ((long long)b * n * n + (ok ? row : 0)) * M;
+  V a[R1 / C][R2];
+#pragma unroll
+  for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+    for (int n2 = 0; n2 < R2; ++n2) a[s][n2] = ok ? src[t + C * s + R1 * n2] : czero<V>();
+  __syncthreads();
+  step1<R1, R2, C, L, false, 1>(a, sm, tw, l, t);
+  __syncthreads();
+  V c[R2 / C][R1];
+  step3<R1, R2, C, L, false, 1>(c, sm, l, t);
+  if (!ok) return;
+  const long long ob = ((long long)b * rows + row) * n;
+  const long long fb = (long long)row * n;
+  const bool use_v = v && alpha != 0.0;
+#pragma unroll
+  for (int s = 0; s < R2 / C; ++s)
+#pragma unroll
+    for (int k1 = 0; k1 < R1; ++k1) {
+      const int k = t + C * s + R2 * k1;
+      if (k < n) {
+        V p = c[s][k1];
+        p.x *= (T)scale;
+        p.y *= (T)scale;
+        if (fconj) {
+          const T g = fconj[fb + k];
+          p.x *= g;
+          p.y *= g;
+        }
+        V r;
+        r.x = (T)beta * p.x;
+        r.y = (T)beta * p.y;
+        if (use_v) {
+          const V vv = v[ob + k];
+          r.x += (T)alpha * vv.x;
+          r.y += (T)alpha * vv.y;
+        }
+        if (addend) {
+          const V ad = addend[ob + k];
+          r.x += ad.x;
+          r.y += ad.y;
+        }
+        out[ob + k] = r;
+      }
+    }
+}
+
+template <typename K>
+int prep(K kernel, size_t smem) {
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) {
+      set_error("ls_fft: cudaFuncSetAttribute(%zu B) failed: %s", smem, cudaGetErrorString(e));
+      return BQ_ECUDA;
+    }
+  }
+  return BQ_OK;
+}
+
+template <typename T, int R1, int R2, int C>
+int run(int n, int B, int op, const void* khat, const void* f, const void* v, double alpha, double beta,
+        const void* addend, void* scratch, void* out, cudaStream_t st) {
+  using V = typename CV<T>::V;
+  constexpr int M = R1 * R2;
+  constexpr int L = (256 / C) < M ? (256 / C) : M;
+  constexpr int NT = C * L;
+  const size_t sm_row = sizeof(V) * (M + smem_elems<R1, R2, L, false>());
+  const size_t sm_col = sizeof(V) * (M + smem_elems<R1, R2, L, true>());
+  const long long N = (long long)n * n * n;
+  V* q = (V*)scratch;                 // B x n x m x m
+  V* hx = q + (long long)B * 4 * N;   // B x n x n x m
+  const int nzi = op == 3 ? 1 : n, z0 = op == 3 ? n : 0;
+  const int nzo = op == 2 ? 1 : n, zo0 = op == 2 ? n : 0;
+  const bool adj = op == 1 || op == 3;
+  int rc;
+  if ((rc = prep(xf_kernel<T, R1, R2, C, L>, sm_row)) || (rc = prep(yf_kernel<T, R1, R2, C, L>, sm_col)) ||
+      (rc = prep(zc_kernel<T, R1, R2, C, L>, sm_col)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
+      (rc = prep(xi_kernel<T, R1, R2, C, L>, sm_row)))
+    return rc;
+  const int rows_in = nzi * n, rows_out = nzo * n;
+  xf_kernel<T, R1, R2, C, L><<<dim3(B, (rows_in + L - 1) / L), NT, sm_row, st>>>(
+      n, rows_in, (op == 0 || op == 2) ? (const T*)f : nullptr, (const V*)v, hx);
+  yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q);
+  zc_kernel<T, R1, R2, C, L><<<dim3(B, M * (M / L)), NT, sm_col, st>>>(n, z0, nzi, zo0, nzo, adj ? 1 : 0,
+                                                                       (const V*)khat, q);
+  yi_kernel<T, R1, R2, C, L><<<dim3(B, nzo * (M / L)), NT, sm_col, st>>>(n, q, hx);
+  const bool crop = op != 2;
+  xi_kernel<T, R1, R2, C, L><<<dim3(B, (rows_out + L - 1) / L), NT, sm_row, st>>>(
+      n, rows_out, hx, 1.0 / (8.0 * (double)N), op == 1 ? (const T*)f : nullptr,
+      (crop && op != 3) ? (const V*)v : nullptr, (crop && op != 3) ? alpha : 0.0, crop && op != 3 ? beta : 1.0,
+      crop ? (const V*)addend : nullptr, (V*)out);
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+template <typename T>
+int dispatch(int n, int B, int op, const void* khat, const void* f, const void* v, double alpha, double beta,
+             const void* addend, void* scratch, void* out, cudaStream_t st) {
+  switch (2 * n) {
+    case 16: return run<T, 4, 4, 4>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    case 32: return run<T, 8, 4, 4>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    case 64: return run<T, 8, 8, 8>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    case 128: return run<T, 16, 8, 8>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    case 256: return run<T, 16, 16, 16>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    case 512: return run<T, 32, 16, 16>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    default: return 1;  // not handled: the caller uses the cuFFT path
+  }
+}
+
+}  // namespace lsfft
+
+// Returns 1 when (n) has no pruned-pass instantiation (or BQ_LS_CUFFT=1 forces
+// the cuFFT path); otherwise a BQ status.  Scratch: 6N complex per view.
+int ls_conv_pruned(bq_ctx* ctx, int dtype, int n, int B, int op, const void* khat, const void* f, const void* v,
+                   double alpha, double beta, const void* addend, void* scratch, void* out, cudaStream_t st) {
+  (void)ctx;
+  static const bool force_cufft = [] {
+    const char* e = std::getenv("BQ_LS_CUFFT");
+    return e && e[0] == '1';
+  }();
+  if (force_cufft) return 1;
+  return dtype == BQ_F32
+             ? lsfft::dispatch<float>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st)
+             : lsfft::dispatch<double>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+}
+
+}  // namespace bq

@@ -484,7 +484,8 @@ int ls_conv_impl(bq_ctx* ctx, int dtype, int n, int B, int op, const void* khat,
   const long long M = (long long)m * m * m, N = (long long)n * n * n;
   const double scale = 1.0 / (double)M;
   const bool adj = (op == 1 || op == 3);
-  int rc;
+  int rc = ls_conv_pruned(ctx, dtype, n, B, op, khat, f, v, alpha, beta, addend, pad_buf, out, st);
+  if (rc != 1) return rc;  // handled by the pruned line passes (ls_fft.cu)
   pad_kernel<T><<<grid_for(ctx, M * B), 256, 0, st>>>(n, B, (op == 0 || op == 2) ? (const T*)f : nullptr,
                                                       (const V*)v, op == 3, (V*)pad_buf);
   BQ_CUDA(cudaGetLastError());
