@@ -116,10 +116,10 @@ struct FArgs {
   double* partials;
   double* red;
   unsigned* bar;
-  void* near_data;  // [G * NW * CAPW * EW] entries (T), NW = warps per block
+  void* near_data;  // [2][G * NW * CAPW * EW] entries (T), NW = warps per block; by pass parity
   T* ie;            // 1/d per voxel (written by the setup pass; staged instead of d)
-  int* near_cnt;  // [G * NW]
-  int* near_blk;  // [G]   per-block near-list totals of the last pass
+  int* near_cnt;  // [2][G * NW]  (pass parity: a fast block's next pass never
+                  //  overwrites lists a slow block is still gathering)
   StageGeo geo;   // staged FUSED pass geometry
   long long dyn_bytes;  // dynamic shared memory of the launch
   unsigned long long* trace;  // optional: block-0 per-step timestamps of one FUSED pass
@@ -967,7 +967,10 @@ template <typename T, int R>
 struct FCfg {
   static constexpr bool kLight = sizeof(T) == 4 && R <= 2;
   // 11 row warps + 1 halo/producer warp = 384 threads -> ~168 registers
-  static constexpr int RW = kLight ? 11 : 7;
+#ifndef BQ_FUSED_RW
+#define BQ_FUSED_RW 11
+#endif
+  static constexpr int RW = kLight ? BQ_FUSED_RW : 7;
   static constexpr int NT = (RW + 1) * 32;    // + 1 halo warp
 };
 
@@ -990,9 +993,8 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   __shared__ __align__(8) unsigned long long s_full[NSTAGE];
   __shared__ __align__(8) unsigned long long s_empty[NSTAGE];
-  unsigned my_gen = 0;
+  unsigned my_gen = 0;  // barriers completed (the counter starts at 0: memset at launch)
   if (threadIdx.x == 0) {
-    my_gen = ld_acquire_u32(A.bar + 1);
     for (int i = 0; i < NSTAGE; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 1);
@@ -1021,7 +1023,9 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   (void)ROWS;
   constexpr int NW = NT / 32;
   constexpr int EWN = 3 + 2 * (R > 0 ? R : 1);
-  T* my_seg = reinterpret_cast<T*>(A.near_data) + ((long long)blockIdx.x * NW + warp) * CAPW * EWN;
+  const long long seg_elems = (long long)gridDim.x * NW * CAPW * EWN;  // one parity's list area
+  T* my_seg0 = reinterpret_cast<T*>(A.near_data) + ((long long)blockIdx.x * NW + warp) * CAPW * EWN;
+  int npass = 0;  // DIV/FUSED passes so far (same in every block)
 
   int phase = F_SETUP;
   while (true) {
@@ -1054,9 +1058,11 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       nv = V::PASS;
       int ncnt = 0;
       bool ovf = false;
+      T* my_seg = my_seg0 + (npass & 1) * seg_elems;
       fused_staged<T, R, NACC, 0>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
                                   s_empty, uses, acc, my_seg, ncnt, ovf);
-      if (lane == 0) A.near_cnt[blockIdx.x * NW + warp] = ncnt;
+      if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
+      ++npass;
       if (ovf) acc[V::OVF] += 1.0;
       if (lane == 0) acc[V::NCNT] += (double)ncnt;
     } else if (phase == F_DIV) {
@@ -1075,6 +1081,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       int ncnt = 0;
       bool ovf = false;
       int buf = 0;
+      T* my_seg = my_seg0 + (npass & 1) * seg_elems;
       long long pos = seg_begin;
       while (pos < seg_end) {
         const long long tile = pos / K3;
@@ -1239,7 +1246,8 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
           buf ^= 1;
         }
       }
-      if (lane == 0) A.near_cnt[blockIdx.x * NW + warp] = ncnt;
+      if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
+      ++npass;
       if (ovf) acc[V::OVF] += 1.0;
       if (lane == 0) acc[V::NCNT] += (double)ncnt;
     } else if (phase == F_NEWTON) {
@@ -1285,58 +1293,56 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
     }
 
     // ---- barrier with fused deterministic reduction ----------------------
+    // Monotonic arrival counter: barrier g completes when it reaches (g+1)*G.
+    // Partials are stored transposed ([value][block]) and EVERY block reduces
+    // them itself in block order (identical sums everywhere, no float
+    // atomics), so no block has to wait for a "last block" to publish.
     const int cur = phase;
     const bool barrier = cur != F_FINAL;
     if (barrier) {
       block_sum_to<NT, NACC>(acc, nv, s_bv, s_scr);
-      if (threadIdx.x < nv) A.partials[(size_t)blockIdx.x * kMaxVals + threadIdx.x] = s_bv[threadIdx.x];
-      if ((cur == F_DIV || cur == F_FUSED) && threadIdx.x == 0) A.near_blk[blockIdx.x] = (int)s_bv[V::NCNT];
+      // [parity][kMaxVals][kMaxBlocks/2]: a fast block's next partials never
+      // land on values a slow block is still reducing
+      constexpr int PB = kMaxBlocks / 2;
+      double* __restrict__ PT = A.partials + (size_t)(my_gen & 1u) * kMaxVals * PB;
+      if (threadIdx.x < nv) PT[(size_t)threadIdx.x * PB + blockIdx.x] = s_bv[threadIdx.x];
+      if (threadIdx.x == NT - 1)
+        PT[(size_t)(kMaxVals - 1) * PB + blockIdx.x] = __longlong_as_double((long long)global_ns());
       __syncthreads();
       if (threadIdx.x == 0) {
-        const unsigned old = atom_add_acqrel(A.bar, 1u);
-        s_flag = (old == gridDim.x - 1) ? 1 : 0;
-        if (s_flag) {
-          const double t_arr = __longlong_as_double((long long)global_ns());
-          s_red[kMaxVals - 1] = t_arr;
+        atom_add_acqrel(A.bar, 1u);
+        const unsigned target = (my_gen + 1u) * gridDim.x;
+        const uint64_t t0 = global_ns();
+        unsigned spins = 0;
+        s_flag = 0;
+        while ((int)(ld_acquire_u32(A.bar) - target) < 0) {
+          if (((++spins) & 4095u) == 0 && global_ns() - t0 > 20ull * 1000000000ull) {
+            s_flag = -1;
+            break;
+          }
         }
+        fence_acq_rel();
       }
       __syncthreads();
-      if (s_flag == 1) {
-        for (int k = warp; k < nv; k += NT / 32) {
-          double s = 0.0;
-          for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(&A.partials[(size_t)b * kMaxVals + k]);
+      if (s_flag == -1) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.report->status = BQ_ETIMEOUT;
+        break;
+      }
+      for (int k = warp; k < nv; k += NT / 32) {
+        const double* col = PT + (size_t)k * PB;
+        double sum = 0.0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) sum += __ldcg(&col[b]);
 #pragma unroll
-          for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(FULLM, s, o);
-          if (lane == 0) {
-            s_red[k] = s;
-            __stcg(&A.red[k], s);
-          }
-        }
-        if (threadIdx.x == 0) __stcg(&A.red[kMaxVals - 1], s_red[kMaxVals - 1]);
-        __syncthreads();
-        if (threadIdx.x == 0) {
-          st_relaxed(A.bar, 0u);
-          red_add_release(A.bar + 1, 1u);
-        }
-      } else {
-        if (threadIdx.x == 0) {
-          const uint64_t t0 = global_ns();
-          unsigned spins = 0;
-          while (ld_acquire_u32(A.bar + 1) == my_gen) {
-            if (((++spins) & 4095u) == 0 && global_ns() - t0 > 20ull * 1000000000ull) {
-              s_flag = -1;
-              break;
-            }
-          }
-          fence_acq_rel();
-        }
-        __syncthreads();
-        if (s_flag == -1) {
-          if (blockIdx.x == 0 && threadIdx.x == 0) A.report->status = BQ_ETIMEOUT;
-          break;
-        }
-        if (threadIdx.x < nv) s_red[threadIdx.x] = __ldcg(&A.red[threadIdx.x]);
-        if (threadIdx.x == NT - 1) s_red[kMaxVals - 1] = __ldcg(&A.red[kMaxVals - 1]);
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(FULLM, sum, o);
+        if (lane == 0) s_red[k] = sum;
+      }
+      if (blockIdx.x == 0 && warp == NT / 32 - 1) {  // latest arrival (phase timeline of the report)
+        const long long* col = reinterpret_cast<const long long*>(PT + (size_t)(kMaxVals - 1) * PB);
+        long long t = 0;
+        for (unsigned b = lane; b < gridDim.x; b += 32) t = max(t, __ldcg(&col[b]));
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t = max(t, __shfl_down_sync(FULLM, t, o));
+        if (lane == 0) s_red[kMaxVals - 1] = __longlong_as_double(t);
       }
       my_gen += 1;
       __syncthreads();
@@ -1370,18 +1376,33 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         A.trace[240 + ntr_k++] = global_ns();
         A.trace[300] = (unsigned long long)total;
       }
-      if (total > 0 && in_smem) {
-        // segment-parallel gather (fixed order = deterministic sums): thread t
-        // owns segments t, t+NT, ...; one block scan places them.
-        const int nseg = gridDim.x * NW;
-        const T* __restrict__ nd = reinterpret_cast<const T*>(A.near_data);
-        constexpr int SPT = 8;  // segments per thread held in registers (G*NW <= 8*NT)
+      // exclusive prefix of the per-segment counts in segment order (block
+      // scan), then a flat gather: thread t copies entries t, t+NT, ... (each
+      // located by binary search), so no thread walks a long segment serially.
+      // The list order is fixed, so every block sums identically.
+      __shared__ int s_pref[8 * NT + 1];
+      const int nseg = gridDim.x * NW;
+      const bool indexed = nseg <= 8 * NT;
+      const int lpar = (npass - 1) & 1;  // parity of the pass that built the lists
+      const T* __restrict__ nd = reinterpret_cast<const T*>(A.near_data) + lpar * seg_elems;
+      const int* __restrict__ ncnt_l = A.near_cnt + lpar * nseg;
+      auto locate = [&](int e) -> const T* {
+        int lo = 0, hi = nseg;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (s_pref[mid] <= e) lo = mid;
+          else hi = mid;
+        }
+        return nd + ((long long)lo * CAPW + (e - s_pref[lo])) * EW;
+      };
+      if (total > 0 && indexed) {
+        constexpr int SPT = 8;
+        const int s0 = threadIdx.x * SPT;
         int cnt[SPT];
         int mine = 0;
 #pragma unroll
         for (int q = 0; q < SPT; ++q) {
-          const int sidx = threadIdx.x + q * NT;
-          cnt[q] = sidx < nseg ? __ldcg(&A.near_cnt[sidx]) : 0;
+          cnt[q] = s0 + q < nseg ? __ldcg(&ncnt_l[s0 + q]) : 0;
           mine += cnt[q];
         }
         __shared__ int s_wsum2[NT / 32];
@@ -1393,19 +1414,24 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         }
         if (lane == 31) s_wsum2[warp] = incl;
         __syncthreads();
-        int wbase = 0;
-        for (int w2 = 0; w2 < warp; ++w2) wbase += s_wsum2[w2];
-        int o2 = wbase + incl - mine;
+        int off = incl - mine;
+        for (int w2 = 0; w2 < warp; ++w2) off += s_wsum2[w2];
 #pragma unroll
         for (int q = 0; q < SPT; ++q) {
-          if (cnt[q] == 0) continue;
-          const int sidx = threadIdx.x + q * NT;
-          const T* src = nd + (long long)sidx * CAPW * EW;
-          T* dst = ne + (long long)o2 * EW;
-          for (int e = 0; e < cnt[q] * EW; ++e) dst[e] = __ldcg(&src[e]);
-          o2 += cnt[q];
+          if (s0 + q < nseg) s_pref[s0 + q] = off;
+          off += cnt[q];
         }
+        if (threadIdx.x == 0) s_pref[nseg] = total;
         __syncthreads();
+        if (in_smem) {
+          for (int e = threadIdx.x; e < total; e += NT) {
+            const T* src = locate(e);
+            T* dst = ne + (long long)e * EW;
+#pragma unroll
+            for (int f = 0; f < EW; ++f) dst[f] = __ldcg(&src[f]);
+          }
+          __syncthreads();
+        }
       }
       const bool big = total > 256;  // long lists: every warp evaluates, block reduction per step
       if (warp == 0 || big) {
@@ -1445,11 +1471,17 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
                 for (int c = 0; c < R; ++c) uv[c] = d[3 + c], sv[c] = d[3 + R + c];
                 near_term(d[0], sv, uv, d[1], d[2]);
               }
+            } else if (indexed) {
+              for (int e = t0; e < total; e += tstride) {
+                const T* d = locate(e);
+                T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
+#pragma unroll
+                for (int c = 0; c < R; ++c) uv[c] = __ldcg(&d[3 + c]), sv[c] = __ldcg(&d[3 + R + c]);
+                near_term(__ldcg(&d[0]), sv, uv, __ldcg(&d[1]), __ldcg(&d[2]));
+              }
             } else {
-              const int nseg = gridDim.x * NW;
-              const T* __restrict__ nd = reinterpret_cast<const T*>(A.near_data);
               for (int sidx = t0; sidx < nseg; sidx += tstride) {
-                const int cnt = __ldcg(&A.near_cnt[sidx]);
+                const int cnt = __ldcg(&ncnt_l[sidx]);
                 for (int e = 0; e < cnt; ++e) {
                   const T* d = nd + ((long long)sidx * CAPW + e) * EW;
                   T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
@@ -1620,11 +1652,11 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
     const long long tp_s = (long long)((A.K2 + (W - 1) * A.rpw - 1) / ((W - 1) * A.rpw)) * A.K3;
     G = std::min<long long>(G, tp_s);
   }
-  G = std::min<long long>(G, kMaxBlocks);
+  G = std::min<long long>(G, kMaxBlocks / 2);  // partials are double-buffered
   // near-list workspace
   constexpr int EWN = 3 + 2 * (R > 0 ? R : 1);
-  const size_t data_bytes = (size_t)G * (NT / 32) * CAPW * EWN * sizeof(T);
-  const size_t need = data_bytes + (size_t)G * (NT / 32) * sizeof(int) + (size_t)G * sizeof(int);
+  const size_t data_bytes = 2 * (size_t)G * (NT / 32) * CAPW * EWN * sizeof(T);
+  const size_t need = data_bytes + 2 * (size_t)G * (NT / 32) * sizeof(int);
   if (ctx->near_bytes < need) {
     cudaFree(ctx->near_buf);
     ctx->near_buf = nullptr;
@@ -1634,7 +1666,6 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   }
   A.near_data = ctx->near_buf;
   A.near_cnt = (int*)((char*)ctx->near_buf + data_bytes);
-  A.near_blk = A.near_cnt + (size_t)G * (NT / 32);
 
   A.dyn_bytes = (long long)dyn;
   A.trace = getenv("BQ_PROX_TRACE") ? (unsigned long long*)ctx->ws.scratch : nullptr;
