@@ -43,6 +43,12 @@
 #ifndef BQ_PROX_TRACE
 #define BQ_PROX_TRACE 0  // device timeline hooks (bench/micro/trace_*.py); build with -DBQ_PROX_TRACE=1
 #endif
+// inter-pass timeline of block 0, thread 0 (BQ_PROX_TRACE_THREAD=-3): stamp i of iteration trace_pass
+#if BQ_PROX_TRACE
+#define TR3(i) do { if (blockIdx.x == 0 && threadIdx.x == 0 && tr3_on) A.trace[320 + (i)] = global_ns(); } while (0)
+#else
+#define TR3(i) do { } while (0)
+#endif
 
 #include <algorithm>
 
@@ -122,6 +128,8 @@ struct FArgs {
                   //  overwrites lists a slow block is still gathering)
   StageGeo geo;   // staged FUSED pass geometry
   long long dyn_bytes;  // dynamic shared memory of the launch
+  long long list_off;   // near-list region of the dynamic smem (bytes), after the stages
+  long long list_bytes;
   unsigned long long* trace;  // optional: block-0 per-step timestamps of one FUSED pass
   int trace_pass;             // which FUSED pass (iteration) to trace
   int trace_thread;           // which thread of block 0 records
@@ -138,6 +146,7 @@ struct FShared {
   T gwid[BQ_MAX_RANK];
   T m_prev, m_cur;
   int phase, slot_cur, slot_prev, slot_new, a_cur, div_p, single, iter;
+  int tr7;  // trace builds: stamp the first stage of this pass
 };
 
 // ---------------------------------------------------------------------------
@@ -670,19 +679,24 @@ __device__ __forceinline__ void issue_step(const FArgs<T>& A, const StepIter& it
 // MODE 0: generic (runtime per-voxel d, optional bound arrays); 1: per-voxel
 // d, scalar bounds; 2: scalar tau, scalar bounds.  Modes 1/2 make the stage
 // layout a compile-time constant.
-template <typename T, int R, int NACC, int MODE>
+// KX > 0: the row length K1 == KX is a compile-time constant (lane -> voxel
+// mapping, row offsets and every per-row branch fold; K1 == 128 is the
+// common 128^3 case), KX == 0: runtime K1.
+template <typename T, int R, int NACC, int MODE, int KX>
 __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>& sh, const StageGeo& g,
                                              long long seg_begin, long long seg_end, T* dyn,
                                              unsigned long long* full, unsigned long long* empty,
                                              unsigned (&uses)[NSTAGE], double (&acc)[NACC], T* near_seg,
-                                             int& ncnt, bool& ovf) {
+                                             int& ncnt, bool& ovf, int pre) {
   using V = FV<R>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const long long N = A.N;
   constexpr int nd = 3;  // the fused path serves 3-D grids (others use wtv_prox.cu)
-  const int K1 = A.K1, K2 = A.K2, K3 = A.K3;
-  const int rpw = A.rpw;
-  const int xr = lane & (A.lpr - 1), yr = lane >> A.lpr_log2, xb = 4 * xr;
+  const int K1 = KX > 0 ? KX : A.K1, K2 = A.K2, K3 = A.K3;
+  const int rpw = KX > 0 ? 128 / KX : A.rpw;
+  const int xr = KX > 0 ? lane % (KX / 4) : lane & (A.lpr - 1);
+  const int yr = KX > 0 ? lane / (KX / 4) : lane >> A.lpr_log2;
+  const int xb = 4 * xr;
   const int W = g.W;
   const int TYe = (W - 1) * rpw;
   const bool used = warp < W;
@@ -700,7 +714,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   const T itauT = diag ? (T)1 : rcp((T)A.tau);
   const bool iso = A.mode == BQ_TV_ISO;
   StageMap<R> M;
-  M.make(diag, MODE == 0 && A.lo_arr != nullptr, MODE == 0 && A.hi_arr != nullptr, nd, m_prev != (T)0);
+  // p_{i-2} is always staged (unused while m_prev == 0) so that the layout does
+  // not depend on the controller: the first stages are prefetched before it runs
+  M.make(diag, MODE == 0 && A.lo_arr != nullptr, MODE == 0 && A.hi_arr != nullptr, nd, true);
   const int NS = g.nstage;
   T* const qbuf = dyn + NS * g.stage_elems;   // [2][SRW][K1]
   T* const srcbuf = qbuf + 2 * g.slot_elems;  // [2][SRW][K1]
@@ -711,8 +727,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     fence_proxy_async_global();  // this pass reads data written before the grid barrier
     StepIter prod;
     prod.init(seg_begin, seg_end, K3, nd);
-    unsigned pu0 = uses[0], pu1 = uses[1];
+    unsigned pu0 = uses[0], pu1 = uses[1];  // include the fills of the prefetched steps
     int ps = 0;
+    for (; ps < pre && prod.valid; ++ps) prod.advance();
     while (prod.valid) {
       const int b = ps & 1;
       if (ps >= 2) mbar_wait(&empty[b], ((b ? pu1 : pu0) - 1) & 1u);  // consumers released it
@@ -737,6 +754,183 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
     return;
   }
+    constexpr bool tr = false;
+    if (tr) t_a = global_ns();
+    mbar_wait(&full[b], (b ? uses[1] : uses[0]) & 1u);
+#if BQ_PROX_TRACE
+    if (s == 0 && blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 7] = global_ns();
+#endif
+    if (tr) t_b = global_ns();
+    if (b) uses[1] += 1;
+    else uses[0] += 1;
+    const int k = cons.k;
+    const int y0 = (int)cons.tile * TYe;
+    const int y = y0 - rpw + sr;
+    const bool act = used && y >= 0 && y < K2;
+    const bool real = act && !halo;
+    const bool warm = k < cons.z0;
+    const bool pin = cons.has_pin();
+    if (k == cons.zs - 1) f3prev[0] = f3prev[1] = f3prev[2] = f3prev[3] = 0;
+    const int rowoff = sr * K1 + xb;
+    // per-step partial sums in the field type (one f64 conversion per step)
+    T fa[NACC];
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) fa[q] = 0;
+    post(fa);  // deferred post phase of the previous step
+
+    // ---- q(k+1) of this row (+ the row below the tile, by warp 0) -------
+    T qn4[4] = {0, 0, 0, 0}, ien[4] = {1, 1, 1, 1}, un[R > 0 ? R : 1][4];
+#pragma unroll
+    for (int c = 0; c < (R > 0 ? R : 1); ++c) un[c][0] = un[c][1] = un[c][2] = un[c][3] = 0;
+    if (cons.has_qin()) {
+      auto qrow = [&](long long off, T (&q)[4], T (&ie)[4], T (&u)[R > 0 ? R : 1][4]) {
+        T l[4], h[4];
+        Vec4<T>::rw(stg + M.A * g.slot_elems + off, q);
+        if (diag) Vec4<T>::rw(stg + M.D * g.slot_elems + off, ie);  // 1/d, precomputed
+        else ie[0] = ie[1] = ie[2] = ie[3] = itauT;
+#pragma unroll
+        for (int c = 0; c < R; ++c) Vec4<T>::rw(stg + (M.U0 + c) * g.slot_elems + off, u[c]);
+        if (M.LO >= 0) Vec4<T>::rw(stg + M.LO * g.slot_elems + off, l);
+        else l[0] = l[1] = l[2] = l[3] = lo_s;
+        if (M.HI >= 0) Vec4<T>::rw(stg + M.HI * g.slot_elems + off, h);
+        else h[0] = h[1] = h[2] = h[3] = hi_s;
+#pragma unroll
+        for (int v = 0; v < 4; ++v) {
+          T z = q[v];
+#pragma unroll
+          for (int c = 0; c < R; ++c) z += (sg * u[c][v] * ie[v]) * sh.gz[c];
+          q[v] = clampv(z, l[v], h[v]);
+        }
+      };
+      T* qdst = qbuf + (long long)((k + 1) & 1) * g.slot_elems;
+      if (act) {
+        qrow(rowoff, qn4, ien, un);
+        Vec4<T>::st(qdst + rowoff, qn4);
+      }
+      if (halo && yr == 0 && y0 + TYe < K2) {
+        const long long off = (long long)(W * rpw) * K1 + xb;
+        T qb[4], ib[4], ub[R > 0 ? R : 1][4];
+        qrow(off, qb, ib, ub);
+        Vec4<T>::st(qdst + off, qb);
+      }
+    }
+
+    // ---- dual update at plane k (dual_tv_solver.py:225-235) -------------
+    const T qright = __shfl_down_sync(FULLM, qc[0], 1);  // x+1 of element 3
+    T src[3][4];
+    T vv[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int n = 0; n < 3; ++n) src[n][0] = src[n][1] = src[n][2] = src[n][3] = 0;
+    if (pin && act) {
+      const bool has_y = nd >= 2 && y < K2 - 1;
+      const bool has_up = nd >= 3 && k < K3 - 1;
+      T qy[4] = {0, 0, 0, 0};
+      if (has_y) Vec4<T>::rw(qbuf + (long long)(k & 1) * g.slot_elems + rowoff + K1, qy);
+      T pc4[3][4], pp4[3][4];
+#pragma unroll
+      for (int n = 0; n < 3; ++n) {
+        pc4[n][0] = pc4[n][1] = pc4[n][2] = pc4[n][3] = 0;
+        if (n < nd) Vec4<T>::rw(stg + (M.PC0 + n) * g.slot_elems + rowoff, pc4[n]);
+        if (n < nd && M.PP0 >= 0) Vec4<T>::rw(stg + (M.PP0 + n) * g.slot_elems + rowoff, pp4[n]);
+      }
+      T pn[3][4];
+#pragma unroll
+      for (int v = 0; v < 4; ++v) {
+        T gr[3];
+        const T right = (v < 3) ? qc[v + 1] : qright;
+        gr[0] = (xb + v < K1 - 1) ? right - qc[v] : (T)0;
+        gr[1] = has_y ? qy[v] - qc[v] : (T)0;
+        gr[2] = has_up ? qn4[v] - qc[v] : (T)0;
+        T w[3], pc3[3];
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          pc3[n] = pc4[n][v];
+          T pb = pc3[n];
+          if (M.PP0 >= 0 && n < nd) pb = pc3[n] + m_prev * (pc3[n] - pp4[n][v]);  // P_bar_{i-1} (:235)
+          w[n] = (n < nd) ? pb + step * gr[n] : (T)0;
+        }
+        if (iso) {
+          T ss = w[0] * w[0];
+          if (nd >= 2) ss += w[1] * w[1];
+          if (nd >= 3) ss += w[2] * w[2];
+          ball(w, ss);
+        } else {
+#pragma unroll
+          for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
+        }
+#pragma unroll
+        for (int n = 0; n < 3; ++n) {
+          pn[n][v] = w[n];
+          if (real && !warm && n < nd) {
+            const T df = w[n] - pc3[n];
+            fa[V::NRM] += df * df;
+            fa[V::NRM + 1] += pc3[n] * pc3[n];
+          }
+          src[n][v] = div_p ? w[n] : w[n] + m_cur * (w[n] - pc3[n]);
+        }
+      }
+      if (real && !warm) {
+        const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
+#pragma unroll
+        for (int n = 0; n < 3; ++n)
+          if (n < nd) Vec4<T>::st(Pn + n * N + j, pn[n]);
+        Vec4<T>::rw(stg + M.V * g.slot_elems + rowoff, vv);
+      }
+      if (nd >= 2) {
+        Vec4<T>::st(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff, src[1]);
+      }
+    }
+    const unsigned long long t_c = tr ? global_ns() : 0;
+    named_sync(1, W * 32);  // q(k+1), div-source rows published; stage b fully read
+    if (threadIdx.x == 0) mbar_arrive(&empty[b]);
+    if (tr) {
+      A.trace[4 * s + 0] = t_a;
+      A.trace[4 * s + 1] = t_b;
+      A.trace[4 * s + 2] = t_c;
+      A.trace[4 * s + 3] = global_ns();
+    }
+
+    // ---- defer the post phase of this step -------------------------------
+    p_do = pin && !warm && used && !halo;
+    p_real = real;
+    p_y = y;
+    p_k = k;
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      p_src[0][v] = src[0][v];
+      p_src[1][v] = src[1][v];
+      p_src[2][v] = src[2][v];
+      p_vv[v] = vv[v];
+      p_iec[v] = iec[v];
+      p_f3[v] = f3prev[v];
+#pragma unroll
+      for (int c = 0; c < (R > 0 ? R : 1); ++c) p_uc[c][v] = uc[c][v];
+    }
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) acc[q] += (double)fa[q];
+    // ---- carries -------------------------------------------------------
+#pragma unroll
+    for (int v = 0; v < 4; ++v) {
+      f3prev[v] = src[2][v];
+      qc[v] = qn4[v];
+      iec[v] = ien[v];
+#pragma unroll
+      for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][v] = un[c][v];
+    }
+    cons.advance();
+    ++s;
+  }
+  {
+    T fa[NACC];
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) fa[q] = 0;
+    post(fa);  // the last step's post phase (its srcbuf rows were published by the last barrier)
+#pragma unroll
+    for (int q = 0; q < NACC; ++q) acc[q] += (double)fa[q];
+  }
+}
+
+#else
   StepIter cons;
   cons.init(seg_begin, seg_end, K3, nd);
   T qc[4] = {0, 0, 0, 0}, iec[4] = {1, 1, 1, 1}, uc[R > 0 ? R : 1][4];
@@ -755,6 +949,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
 #endif
     if (tr) t_a = global_ns();
     mbar_wait(&full[b], (b ? uses[1] : uses[0]) & 1u);
+#if BQ_PROX_TRACE
+    if (s == 0 && blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 7] = global_ns();
+#endif
     if (tr) t_b = global_ns();
     if (b) uses[1] += 1;
     else uses[0] += 1;
@@ -960,6 +1157,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   }
 }
 
+#endif
 // ---------------------------------------------------------------------------
 // The kernel
 // ---------------------------------------------------------------------------
@@ -1001,8 +1199,37 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
     }
     mbar_init_fence();
   }
+  __shared__ int s_pre[4];  // prefetched steps of the next FUSED pass: count, slot_cur, slot_prev, a_cur
+  if (threadIdx.x == 0) s_pre[0] = 0;
   __syncthreads();
   unsigned uses[NSTAGE] = {0u, 0u};
+  const int PW = A.geo.W;  // producer warp of the staged pass
+  // Consume prefetched stages that will not be used (the next pass is not the
+  // predicted FUSED pass, or the smem is needed): keeps the mbarrier phase
+  // counts of producer and consumers in step and no bulk copy in flight.
+  // consumer warps only (everything but the producer warp): named barrier 2
+  constexpr int NC = NT - 32;
+  const int cidx = warp < PW ? (int)threadIdx.x : (warp > PW ? (int)threadIdx.x - 32 : -1);
+  auto csync = [&]() { named_sync(2, NC); };
+  auto drain_impl = [&](bool consumers_only) {
+    const int n = s_pre[0];
+    for (int i = 0; i < n; ++i) {
+      const int b = i & 1;
+      if (warp != PW) {
+        if (threadIdx.x == 0) {
+          mbar_wait(&s_full[b], uses[b] & 1u);
+          mbar_arrive(&s_empty[b]);
+        }
+        uses[b] += 1;
+      }
+    }
+    if (consumers_only) csync();
+    else __syncthreads();
+    if (threadIdx.x == 0) s_pre[0] = 0;
+    if (consumers_only) csync();
+    else __syncthreads();
+  };
+  auto drain = [&]() { drain_impl(false); };
 
   const long long N = A.N, plane = A.plane;
   const int K1 = A.K1, K2 = A.K2, K3 = A.K3, nd = A.ndim;
@@ -1028,12 +1255,16 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   int npass = 0;  // DIV/FUSED passes so far (same in every block)
 
   int phase = F_SETUP;
+#if BQ_PROX_TRACE
+  bool tr3_on = false;
+#endif
   while (true) {
     double acc[NACC];
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     int nv = 0;
 
+    if (s_pre[0] > 0 && (phase == F_DIV || phase == F_FINAL)) drain();  // these reuse / leave the smem
     if (phase == F_SETUP) {
       // gram partials U^T D^-1 U (wpm.py:50-56); 1/d staged by the fused pass
       nv = V::S;
@@ -1059,12 +1290,32 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       int ncnt = 0;
       bool ovf = false;
       T* my_seg = my_seg0 + (npass & 1) * seg_elems;
-      fused_staged<T, R, NACC, 0>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
-                                  s_empty, uses, acc, my_seg, ncnt, ovf);
+      int pre = s_pre[0];
+      if (pre > 0 && !(s_pre[1] == sh.slot_cur && s_pre[2] == sh.slot_prev && s_pre[3] == sh.a_cur)) {
+        drain();
+        pre = 0;
+      }
+#if BQ_PROX_TRACE
+      if (blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) {
+        A.trace[320 + 9] = global_ns();
+        A.trace[320 + 10] = (unsigned long long)(pre + 100 * s_pre[0]);
+      }
+#endif
+      if (A.K1 == 128)
+        fused_staged<T, R, NACC, 0, 128>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
+                                         s_empty, uses, acc, my_seg, ncnt, ovf, pre);
+      else
+        fused_staged<T, R, NACC, 0, 0>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
+                                       s_empty, uses, acc, my_seg, ncnt, ovf, pre);
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
       if (ovf) acc[V::OVF] += 1.0;
       if (lane == 0) acc[V::NCNT] += (double)ncnt;
+#if BQ_PROX_TRACE
+      tr3_on = A.trace && A.trace_thread == -3 && s_c.it == A.trace_pass;
+      if (tr3_on && blockIdx.x == 0 && threadIdx.x == 0) A.trace[320 + 8] = s_c.it;
+#endif
+      TR3(0);
     } else if (phase == F_DIV) {
       nv = V::PASS;
       const bool fused = false;
@@ -1300,7 +1551,8 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
     const int cur = phase;
     const bool barrier = cur != F_FINAL;
     if (barrier) {
-      block_sum_to<NT, NACC>(acc, nv, s_bv, s_scr);
+      block_sum_to<NT, NACC>(acc, nv, s_bv, s_scr);  // (its syncs: every thread has read s_pre)
+      if (cur == F_FUSED && threadIdx.x == 0) s_pre[0] = 0;
       // [parity][kMaxVals][kMaxBlocks/2]: a fast block's next partials never
       // land on values a slow block is still reducing
       constexpr int PB = kMaxBlocks / 2;
@@ -1309,6 +1561,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       if (threadIdx.x == NT - 1)
         PT[(size_t)(kMaxVals - 1) * PB + blockIdx.x] = __longlong_as_double((long long)global_ns());
       __syncthreads();
+      if (cur == F_FUSED) TR3(1);
       if (threadIdx.x == 0) {
         atom_add_acqrel(A.bar, 1u);
         const unsigned target = (my_gen + 1u) * gridDim.x;
@@ -1322,11 +1575,28 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
           }
         }
         fence_acq_rel();
+        if (cur == F_FUSED) TR3(2);
       }
       __syncthreads();
       if (s_flag == -1) {
         if (blockIdx.x == 0 && threadIdx.x == 0) A.report->status = BQ_ETIMEOUT;
         break;
+      }
+      if (cur == F_FUSED && threadIdx.x == 0) {
+        // the next FUSED pass (the usual successor) reads ring[slot_new],
+        // ring[slot_cur] and abuf[a_cur ^ 1]; its first stages are issued by
+        // the producer warp below, while the other warps run the controller
+        StepIter it;
+        it.init(seg_begin_s, seg_end_s, K3, 3);
+        int n = 0;
+        while (it.valid && n < NSTAGE) {
+          it.advance();
+          ++n;
+        }
+        s_pre[1] = sh.slot_new;
+        s_pre[2] = sh.slot_cur;
+        s_pre[3] = sh.a_cur ^ 1;
+        s_pre[0] = n;
       }
       for (int k = warp; k < nv; k += NT / 32) {
         const double* col = PT + (size_t)k * PB;
@@ -1346,24 +1616,50 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       }
       my_gen += 1;
       __syncthreads();
+      if (cur == F_FUSED) TR3(3);
     }
 
+    // ---- producer warp: prefetch the next pass's first stages -------------
+    if (warp == PW) {
+      if (cur == F_FUSED && s_pre[0] > 0) {
+        StageMap<R> M;
+        M.make(A.d != nullptr, A.lo_arr != nullptr, A.hi_arr != nullptr, 3, true);
+        fence_proxy_async_global();  // reads data written before the grid barrier
+        StepIter it;
+        it.init(seg_begin_s, seg_end_s, K3, 3);
+        for (int n = 0; n < s_pre[0]; ++n) {
+          const int b = n & 1;
+          issue_step<T, R>(A, it, M, A.geo, reinterpret_cast<T*>(s_dyn) + b * A.geo.stage_elems, &s_full[b],
+                           A.ring[s_pre[1]], A.ring[s_pre[2]], A.abuf[s_pre[3]], lane);
+          uses[b] += 1;
+          it.advance();
+        }
+      }
+    } else {
     // ---- controller (+ block-local Newton over the near list) ------------
     if (threadIdx.x == 0) {
       Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
       ctl.timeline(cur, s_red, barrier);
       ctl.run(cur, s_red);
     }
-    __syncthreads();
+    csync();
+    if (cur == F_FUSED) TR3(4);
     // ---- on-chip Newton: warp 0 stages the (usually tiny) near list into
     //      shared memory and runs every Newton step with warp-level
     //      reductions; the other warps wait once.
     if (s_c.phase == F_NLOCAL) {
       constexpr int EW = 3 + 2 * (R > 0 ? R : 1);  // av, l, h, u[R], s[R]
-      T* ne = reinterpret_cast<T*>(s_dyn);
+      T* ne = reinterpret_cast<T*>(s_dyn + A.list_off);
       const int total = (int)s_red[V::NCNT];
-      const bool in_smem = (long long)total * EW * (long long)sizeof(T) <= (long long)A.dyn_bytes &&
-                           (int)gridDim.x * NW <= 8 * NT;
+      const long long lbytes = (long long)total * EW * (long long)sizeof(T);
+      const bool seg_ok = (int)gridDim.x * NW <= 8 * NC;
+      bool in_smem = seg_ok && lbytes <= A.list_bytes;
+      if (seg_ok && !in_smem && lbytes <= A.dyn_bytes) {
+        // long list (early iterations): give up the prefetched stages, use all the dynamic smem
+        if (s_pre[0] > 0) drain_impl(true);
+        ne = reinterpret_cast<T*>(s_dyn);
+        in_smem = true;
+      }
 #if BQ_PROX_TRACE
       const bool ntr = A.trace && blockIdx.x == 0 && threadIdx.x == 0 && s_c.it == A.trace_pass && A.trace_thread < 0;
       const bool nprof = A.trace && blockIdx.x == 0 && threadIdx.x == 0 && A.trace_thread == -2 && s_c.it < 128;
@@ -1382,7 +1678,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       // The list order is fixed, so every block sums identically.
       __shared__ int s_pref[8 * NT + 1];
       const int nseg = gridDim.x * NW;
-      const bool indexed = nseg <= 8 * NT;
+      const bool indexed = nseg <= 8 * NC;
       const int lpar = (npass - 1) & 1;  // parity of the pass that built the lists
       const T* __restrict__ nd = reinterpret_cast<const T*>(A.near_data) + lpar * seg_elems;
       const int* __restrict__ ncnt_l = A.near_cnt + lpar * nseg;
@@ -1397,7 +1693,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       };
       if (total > 0 && indexed) {
         constexpr int SPT = 8;
-        const int s0 = threadIdx.x * SPT;
+        const int s0 = cidx * SPT;
         int cnt[SPT];
         int mine = 0;
 #pragma unroll
@@ -1406,31 +1702,32 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
           mine += cnt[q];
         }
         __shared__ int s_wsum2[NT / 32];
+        const int cw = cidx >> 5;
         int incl = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
           const int t = __shfl_up_sync(FULLM, incl, o);
           if (lane >= o) incl += t;
         }
-        if (lane == 31) s_wsum2[warp] = incl;
-        __syncthreads();
+        if (lane == 31) s_wsum2[cw] = incl;
+        csync();
         int off = incl - mine;
-        for (int w2 = 0; w2 < warp; ++w2) off += s_wsum2[w2];
+        for (int w2 = 0; w2 < cw; ++w2) off += s_wsum2[w2];
 #pragma unroll
         for (int q = 0; q < SPT; ++q) {
           if (s0 + q < nseg) s_pref[s0 + q] = off;
           off += cnt[q];
         }
         if (threadIdx.x == 0) s_pref[nseg] = total;
-        __syncthreads();
+        csync();
         if (in_smem) {
-          for (int e = threadIdx.x; e < total; e += NT) {
+          for (int e = cidx; e < total; e += NC) {
             const T* src = locate(e);
             T* dst = ne + (long long)e * EW;
 #pragma unroll
             for (int f = 0; f < EW; ++f) dst[f] = __ldcg(&src[f]);
           }
-          __syncthreads();
+          csync();
         }
       }
       const bool big = total > 256;  // long lists: every warp evaluates, block reduction per step
@@ -1460,8 +1757,8 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
                 for (int c2 = 0; c2 <= c; ++c2, ++k) nacc[k] += (double)uv[c] * (double)sv[c2];
             }
           };
-          const int t0 = big ? threadIdx.x : lane;
-          const int tstride = big ? NT : 32;
+          const int t0 = big ? cidx : lane;
+          const int tstride = big ? NC : 32;
           if (total > 0) {
             if (in_smem) {
               for (int e = t0; e < total; e += tstride) {
@@ -1493,7 +1790,21 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
             }
           }
           if (big) {
-            block_sum_to<NT, (V::NEWTON > 0 ? V::NEWTON : 1)>(nacc, V::NEWTON, s_bv, s_scr);
+            // consumer-warp reduction in fixed warp order (deterministic)
+            const int cw = cidx >> 5;
+#pragma unroll
+            for (int k = 0; k < V::NEWTON; ++k) {
+#pragma unroll
+              for (int o = 16; o > 0; o >>= 1) nacc[k] += __shfl_down_sync(FULLM, nacc[k], o);
+              if (lane == 0) s_scr[cw * kMaxVals + k] = nacc[k];
+            }
+            csync();
+            if (cidx < V::NEWTON) {
+              double t = 0.0;
+              for (int w2 = 0; w2 < NC / 32; ++w2) t += s_scr[w2 * kMaxVals + cidx];
+              s_bv[cidx] = t;
+            }
+            csync();
 #pragma unroll
             for (int k = 0; k < V::NEWTON; ++k) nacc[k] = s_bv[k];
           } else if (total > 0) {
@@ -1520,13 +1831,14 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
             ctl.newton_step(phi, hp);
             if (ntr && ntr_k < 40) A.trace[240 + ntr_k++] = global_ns();
           }
-          if (big) __syncthreads();
+          if (big) csync();
           else __syncwarp();
         }
       }
-      __syncthreads();
+      csync();
       if (nprof) A.trace[256 + s_c.it] = ((global_ns() - nprof_t0) << 20) | ((unsigned long long)total & 0xfffff);
     }
+    if (cur == F_FUSED) TR3(5);
     if (threadIdx.x == 0) {
       if (s_c.phase == F_FUSED) {
         Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
@@ -1542,6 +1854,11 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       sh.single = s_c.single;
       sh.m_prev = (T)s_c.m_prev;
       sh.m_cur = (T)s_c.m_cur;
+#if BQ_PROX_TRACE
+      sh.tr7 = (cur == F_FUSED && tr3_on) ? 1 : 0;
+#else
+      sh.tr7 = 0;
+#endif
       for (int i = 0; i < R; ++i) {
         sh.gw[i] = (T)s_c.gw[i];
         sh.gz[i] = (T)(s_c.gw[i] - s_c.beta[i]);
@@ -1549,9 +1866,14 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         sh.gwid[i] = (T)s_c.gwid[i];
       }
     }
+    }  // consumer warps
     __syncthreads();
+    if (cur == F_FUSED) TR3(6);
     phase = sh.phase;
-    if (phase == F_DONE) break;
+    if (phase == F_DONE) {
+      if (s_pre[0] > 0) drain();
+      break;
+    }
   }
 }
 
@@ -1640,7 +1962,18 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.geo.SRW = W * A.rpw + 1;
   A.geo.slot_elems = (long long)A.geo.SRW * A.K1;
   A.geo.stage_elems = (long long)M.nfield * A.geo.slot_elems;
-  const size_t dyn = std::max<size_t>(2ull * (RW + 1) * A.rpw * A.K1 * sizeof(T), staged_bytes(W));
+  const size_t base_dyn = std::max<size_t>(2ull * (RW + 1) * A.rpw * A.K1 * sizeof(T), staged_bytes(W));
+  // near-list region after the stages (so the next pass's prefetched stages survive the on-chip Newton)
+  int optin = 0, static_b = 0;
+  BQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  {
+    cudaFuncAttributes fa{};
+    BQ_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));
+    static_b = (int)fa.sharedSizeBytes;
+  }
+  const long long room = (long long)optin - static_b - (long long)base_dyn - 2048;
+  const size_t list_bytes = room > 0 ? (size_t)(room / 16 * 16) : 0;
+  const size_t dyn = base_dyn + list_bytes;
   BQ_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn + 1024));
   int per_sm = 0;
   BQ_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NT, dyn));
@@ -1668,6 +2001,8 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.near_cnt = (int*)((char*)ctx->near_buf + data_bytes);
 
   A.dyn_bytes = (long long)dyn;
+  A.list_off = (long long)base_dyn;
+  A.list_bytes = (long long)list_bytes;
   A.trace = getenv("BQ_PROX_TRACE") ? (unsigned long long*)ctx->ws.scratch : nullptr;
   A.trace_pass = getenv("BQ_PROX_TRACE") ? atoi(getenv("BQ_PROX_TRACE")) : 0;
   A.trace_thread = getenv("BQ_PROX_TRACE_THREAD") ? atoi(getenv("BQ_PROX_TRACE_THREAD")) : 0;
