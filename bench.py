@@ -352,7 +352,13 @@ def ls_measure(args, dev):
         ka.append(float(np.mean(vs.iters_adjoint)))
     ms = float(np.median(times))
     Kf, Ka = float(np.mean(kf)), float(np.mean(ka))
-    bpv = 952.0 * (Kf + Ka) + 92.0  # bytes per view*voxel of the fused LS algorithm
+    # bytes per view*voxel = (2 B_mv + 128) (K_f + K_a) + 92, with B_mv the
+    # bytes of one padded Green matvec.  SURVEY's 412 N assumes unpruned 3-D
+    # transforms; the pruned line passes (csrc/ls_fft.cu) move
+    # R 116 N + W 104 N = 220 N, so the count is lowered as 8d requires.
+    pruned = (2 * n) in (16, 32, 64, 128, 256, 512) and os.environ.get("BQ_LS_CUFFT", "0") != "1"
+    b_mv = 220.0 if pruned else 412.0
+    bpv = (2.0 * b_mv + 128.0) * (Kf + Ka) + 92.0
     vv = len(idx) * n ** 3
     peak, _ = hbm_peak()
     achieved = vv * bpv / (ms * 1e-3) / 1e9
@@ -360,7 +366,8 @@ def ls_measure(args, dev):
             "ms_per_subset_gradient": ms, "views": len(idx), "n": n, "padded": 2 * n, "dtype": "c64",
             "K_f": Kf, "K_a": Ka,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "algorithmic_bytes_per_view_voxel": bpv},
+                         "algorithmic_bytes_per_view_voxel": bpv, "bytes_per_matvec_per_voxel": b_mv,
+                         "green_path": "pruned line passes" if pruned else "padded cuFFT"},
             "data": "synthetic (seeded ellipsoid phantom, 25 dB noise), x = x_gt/2"}
 
 

@@ -56,7 +56,8 @@ def main():
         ka.append(np.mean(vs.iters_adjoint))
     ms = float(np.median(times))
     Kf, Ka = float(np.mean(kf)), float(np.mean(ka))
-    bytes_vv = 952 * (Kf + Ka) + 92
+    pruned = (2 * n) in (16, 32, 64, 128, 256, 512) and os.environ.get("BQ_LS_CUFFT", "0") != "1"
+    bytes_vv = (2.0 * (220.0 if pruned else 412.0) + 128.0) * (Kf + Ka) + 92.0  # SURVEY 8d, pruned matvec bytes (bench.py)
     vv = len(idx) * n ** 3
     out = {"metric": "LS forward+adjoint views*voxels/s", "n": n, "views_in_subset": len(idx), "ms": ms,
            "value": vv / (ms * 1e-3), "K_f": Kf, "K_a": Ka, "bytes_per_view_voxel": bytes_vv,

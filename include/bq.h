@@ -225,6 +225,14 @@ int bq_bicg_p(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* r, c
               const double* coef, void* p, const int32_t* active, void* stream);
 int bq_bicg_x(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const double* state, const void* p,
               const void* s, const void* t, void* x, void* r, const int32_t* mode, void* stream);
+/* Device-resident batched BiCGSTAB, x_b = A^-1 rhs_b from x0 = 0 to the relative residual tol
+ * (oracle/physics.py bicgstab per view): adjoint 0 solves A = I - G_dom diag f, 1 solves A^H.
+ * vec_work: 6 B N complex; conv_scratch: the bq_ls_conv pad_buf; small_work:
+ * bq_ls_bicgstab_small_bytes() bytes; iters: device, B ints.  Converged views are skipped. */
+int64_t bq_ls_bicgstab_small_bytes(bq_ctx* ctx, int32_t n, int32_t B);
+int bq_ls_bicgstab(bq_ctx* ctx, int32_t dtype, int32_t n, int32_t B, int32_t adjoint, const void* khat,
+                   const void* f, const void* rhs, void* x, double tol, int32_t max_iter, void* vec_work,
+                   void* conv_scratch, void* small_work, int32_t* iters, void* stream);
 /* grad (+)= scale * sum_b Re(conj(fp u_b) w_b), views summed in order. */
 int bq_ls_grad_accum(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* fp, const void* u,
                      const void* w, double scale, void* grad, int32_t accumulate, void* stream);

@@ -48,6 +48,8 @@ EXPORTS = (
     "bq_green_init",
     "bq_ls_incident",
     "bq_ls_conv",
+    "bq_ls_bicgstab",
+    "bq_ls_bicgstab_small_bytes",
     "bq_cdot",
     "bq_caxpy",
     "bq_bicg_scalars",
@@ -143,6 +145,8 @@ _SIGS = {
     "bq_green_init": (C.c_int, [_P, _I32, _I32, _D, _D, _P, _P]),
     "bq_ls_incident": (C.c_int, [_P, _I32, _I32, _D, _I32, _P, _P, _P]),
     "bq_ls_conv": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
+    "bq_ls_bicgstab": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _D, _I32, _P, _P, _P, _P, _P]),
+    "bq_ls_bicgstab_small_bytes": (C.c_int64, [_P, _I32, _I32]),
     "bq_cscale_real": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
     "bq_cdot": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
     "bq_caxpy": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _I32, _D, _P, _P, _P, _P]),

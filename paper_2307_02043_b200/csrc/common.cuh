@@ -50,8 +50,11 @@ struct bq_ctx;
 namespace bq {
 // ls_fft.cu: padded-Green convolution as pruned line passes; returns 1 when the
 // size has no instantiation (the caller then uses the cuFFT path).
+// Optional: active[b] == 0 skips view b; dotp != NULL writes per-block partials
+// (sum conj(da) out, sum |out|^2) as [B][*nblk][3] doubles.
 int ls_conv_pruned(bq_ctx* ctx, int dtype, int n, int B, int op, const void* khat, const void* f, const void* v,
-                   double alpha, double beta, const void* addend, void* scratch, void* out, cudaStream_t st);
+                   double alpha, double beta, const void* addend, void* scratch, void* out, cudaStream_t st,
+                   const int* active = nullptr, const void* da = nullptr, double* dotp = nullptr, int* nblk = nullptr);
 }  // namespace bq
 
 struct bq_ctx {
@@ -63,6 +66,8 @@ struct bq_ctx {
   size_t near_bytes = 0;
   void* aux_buf = nullptr;        // per-voxel 1/d of the fused prox kernel
   size_t aux_bytes = 0;
+  int* host_flags = nullptr;      // pinned: active-view counts of the device BiCGSTAB
+  cudaEvent_t flag_ev[2] = {nullptr, nullptr};
 };
 
 namespace bq {

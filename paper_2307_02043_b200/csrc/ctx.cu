@@ -74,6 +74,9 @@ extern "C" int bq_ctx_destroy(bq_ctx* c) {
   fft_cache_destroy(c->fft_cache);
   cudaFree(c->near_buf);
   cudaFree(c->aux_buf);
+  if (c->host_flags) cudaFreeHost(c->host_flags);
+  if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
+  if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
   cudaFree(c->ws.partials);
   cudaFree(c->ws.barrier);
   cudaFree(c->ws.ctl);

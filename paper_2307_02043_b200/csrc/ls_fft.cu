@@ -195,7 +195,7 @@ __device__ __forceinline__ V czero() {
 template <typename T, int R1, int R2, int C, int L>
 __global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __restrict__ f,
                                                   const typename CV<T>::V* __restrict__ v,
-                                                  typename CV<T>::V* __restrict__ hx) {
+                                                  typename CV<T>::V* __restrict__ hx, const int* __restrict__ active) {
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __re
   V* sm = tw + M;
   const int tid = threadIdx.x, l = tid / C, t = tid % C;
   const int b = blockIdx.x, row = blockIdx.y * L + l;
+  if (active && !active[b]) return;  // converged view of a batched solve: nothing to do
   const bool ok = row < rows;
   load_twiddles<V, M>(tw, tid, C * L);
   const V* src = v + ((long long)b * rows + row) * n;
@@ -243,7 +244,8 @@ __global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __re
 // ---------------------------------------------------------------------------
 template <typename T, int R1, int R2, int C, int L>
 __global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V* __restrict__ hx,
-                                                  typename CV<T>::V* __restrict__ q) {
+                                                  typename CV<T>::V* __restrict__ q, const int* __restrict__ active) {
+  if (active && !active[blockIdx.x]) return;
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2, XT = M / L;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -281,7 +283,8 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V
 template <typename T, int R1, int R2, int C, int L>
 __global__ void __launch_bounds__(C* L) zc_kernel(int n, int z0, int nzi, int zo0, int nzo, int adj,
                                                   const typename CV<T>::V* __restrict__ khat,
-                                                  typename CV<T>::V* __restrict__ q) {
+                                                  typename CV<T>::V* __restrict__ q, const int* __restrict__ active) {
+  if (active && !active[blockIdx.x]) return;
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2, XT = M / L;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -338,7 +341,8 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int z0, int nzi, int zo
 // ---------------------------------------------------------------------------
 template <typename T, int R1, int R2, int C, int L>
 __global__ void __launch_bounds__(C* L) yi_kernel(int n, const typename CV<T>::V* __restrict__ q,
-                                                  typename CV<T>::V* __restrict__ hx) {
+                                                  typename CV<T>::V* __restrict__ hx, const int* __restrict__ active) {
+  if (active && !active[blockIdx.x]) return;
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2, XT = M / L;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -378,7 +382,8 @@ __global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typenam
                                                   double scale, const T* __restrict__ fconj,
                                                   const typename CV<T>::V* __restrict__ v, double alpha, double beta,
                                                   const typename CV<T>::V* __restrict__ addend,
-                                                  typename CV<T>::V* __restrict__ out) {
+                                                  typename CV<T>::V* __restrict__ out, const int* __restrict__ active,
+                                                  const typename CV<T>::V* __restrict__ da, double* __restrict__ dotp) {
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2;
   extern __shared__ __align__(16) unsigned char smraw[];
@@ -386,6 +391,7 @@ __global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typenam
   V* sm = tw + M;
   const int tid = threadIdx.x, l = tid / C, t = tid % C;
   const int b = blockIdx.x, row = blockIdx.y * L + l;
+  if (active && !active[b]) return;
   const bool ok = row < rows;
   load_twiddles<V, M>(tw, tid, C * L);
   const V* src = hx + ((long long)b * n * n + (ok ? row : 0)) * M;
@@ -399,40 +405,69 @@ __global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typenam
   __syncthreads();
   V c[R2 / C][R1];
   step3<R1, R2, C, L, false, 1>(c, sm, l, t);
-  if (!ok) return;
-  const long long ob = ((long long)b * rows + row) * n;
-  const long long fb = (long long)row * n;
-  const bool use_v = v && alpha != 0.0;
+  // fused per-view dot partials of the result: (sum conj(da) out, sum |out|^2)
+  double dre = 0.0, dim = 0.0, dnn = 0.0;
+  if (ok) {
+    const long long ob = ((long long)b * rows + row) * n;
+    const long long fb = (long long)row * n;
+    const bool use_v = v && alpha != 0.0;
 #pragma unroll
-  for (int s = 0; s < R2 / C; ++s)
+    for (int s = 0; s < R2 / C; ++s)
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      const int k = t + C * s + R2 * k1;
-      if (k < n) {
-        V p = c[s][k1];
-        p.x *= (T)scale;
-        p.y *= (T)scale;
-        if (fconj) {
-          const T g = fconj[fb + k];
-          p.x *= g;
-          p.y *= g;
+      for (int k1 = 0; k1 < R1; ++k1) {
+        const int k = t + C * s + R2 * k1;
+        if (k < n) {
+          V p = c[s][k1];
+          p.x *= (T)scale;
+          p.y *= (T)scale;
+          if (fconj) {
+            const T g = fconj[fb + k];
+            p.x *= g;
+            p.y *= g;
+          }
+          V r;
+          r.x = (T)beta * p.x;
+          r.y = (T)beta * p.y;
+          if (use_v) {
+            const V vv = v[ob + k];
+            r.x += (T)alpha * vv.x;
+            r.y += (T)alpha * vv.y;
+          }
+          if (addend) {
+            const V ad = addend[ob + k];
+            r.x += ad.x;
+            r.y += ad.y;
+          }
+          out[ob + k] = r;
+          if (dotp) {
+            const V a = da[ob + k];
+            dre += (double)a.x * r.x + (double)a.y * r.y;
+            dim += (double)a.x * r.y - (double)a.y * r.x;
+            dnn += (double)r.x * r.x + (double)r.y * r.y;
+          }
         }
-        V r;
-        r.x = (T)beta * p.x;
-        r.y = (T)beta * p.y;
-        if (use_v) {
-          const V vv = v[ob + k];
-          r.x += (T)alpha * vv.x;
-          r.y += (T)alpha * vv.y;
-        }
-        if (addend) {
-          const V ad = addend[ob + k];
-          r.x += ad.x;
-          r.y += ad.y;
-        }
-        out[ob + k] = r;
       }
+  }
+  if (dotp) {  // fixed-order block reduction (deterministic)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      dre += __shfl_down_sync(0xffffffffu, dre, o);
+      dim += __shfl_down_sync(0xffffffffu, dim, o);
+      dnn += __shfl_down_sync(0xffffffffu, dnn, o);
     }
+    __shared__ double red[3][32];
+    const int lane = tid & 31, w = tid >> 5;
+    if (lane == 0) red[0][w] = dre, red[1][w] = dim, red[2][w] = dnn;
+    __syncthreads();
+    if (tid == 0) {
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0;
+      for (int q = 0; q < (C * L) / 32; ++q) a0 += red[0][q], a1 += red[1][q], a2 += red[2][q];
+      double* dp = dotp + ((long long)b * gridDim.y + blockIdx.y) * 3;
+      dp[0] = a0;
+      dp[1] = a1;
+      dp[2] = a2;
+    }
+  }
 }
 
 template <typename K>
@@ -449,7 +484,8 @@ int prep(K kernel, size_t smem) {
 
 template <typename T, int R1, int R2, int C>
 int run(int n, int B, int op, const void* khat, const void* f, const void* v, double alpha, double beta,
-        const void* addend, void* scratch, void* out, cudaStream_t st) {
+        const void* addend, void* scratch, void* out, const int* active, const void* da, double* dotp, int* nblk,
+        cudaStream_t st) {
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2;
   constexpr int L = (256 / C) < M ? (256 / C) : M;
@@ -469,30 +505,32 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
     return rc;
   const int rows_in = nzi * n, rows_out = nzo * n;
   xf_kernel<T, R1, R2, C, L><<<dim3(B, (rows_in + L - 1) / L), NT, sm_row, st>>>(
-      n, rows_in, (op == 0 || op == 2) ? (const T*)f : nullptr, (const V*)v, hx);
-  yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q);
+      n, rows_in, (op == 0 || op == 2) ? (const T*)f : nullptr, (const V*)v, hx, active);
+  yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q, active);
   zc_kernel<T, R1, R2, C, L><<<dim3(B, M * (M / L)), NT, sm_col, st>>>(n, z0, nzi, zo0, nzo, adj ? 1 : 0,
-                                                                       (const V*)khat, q);
-  yi_kernel<T, R1, R2, C, L><<<dim3(B, nzo * (M / L)), NT, sm_col, st>>>(n, q, hx);
+                                                                       (const V*)khat, q, active);
+  yi_kernel<T, R1, R2, C, L><<<dim3(B, nzo * (M / L)), NT, sm_col, st>>>(n, q, hx, active);
+  if (nblk) *nblk = (rows_out + L - 1) / L;
   const bool crop = op != 2;
   xi_kernel<T, R1, R2, C, L><<<dim3(B, (rows_out + L - 1) / L), NT, sm_row, st>>>(
       n, rows_out, hx, 1.0 / (8.0 * (double)N), op == 1 ? (const T*)f : nullptr,
       (crop && op != 3) ? (const V*)v : nullptr, (crop && op != 3) ? alpha : 0.0, crop && op != 3 ? beta : 1.0,
-      crop ? (const V*)addend : nullptr, (V*)out);
+      crop ? (const V*)addend : nullptr, (V*)out, active, (const V*)da, dotp);
   BQ_CUDA(cudaGetLastError());
   return BQ_OK;
 }
 
 template <typename T>
 int dispatch(int n, int B, int op, const void* khat, const void* f, const void* v, double alpha, double beta,
-             const void* addend, void* scratch, void* out, cudaStream_t st) {
+             const void* addend, void* scratch, void* out, const int* active, const void* da, double* dotp,
+             int* nblk, cudaStream_t st) {
   switch (2 * n) {
-    case 16: return run<T, 4, 4, 4>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
-    case 32: return run<T, 8, 4, 4>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
-    case 64: return run<T, 8, 8, 8>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
-    case 128: return run<T, 16, 8, 8>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
-    case 256: return run<T, 16, 16, 16>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
-    case 512: return run<T, 32, 16, 16>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+    case 16: return run<T, 4, 4, 4>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
+    case 32: return run<T, 8, 4, 4>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
+    case 64: return run<T, 8, 8, 8>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
+    case 128: return run<T, 16, 8, 8>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
+    case 256: return run<T, 16, 16, 16>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
+    case 512: return run<T, 32, 16, 16>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
     default: return 1;  // not handled: the caller uses the cuFFT path
   }
 }
@@ -502,7 +540,8 @@ int dispatch(int n, int B, int op, const void* khat, const void* f, const void* 
 // Returns 1 when (n) has no pruned-pass instantiation (or BQ_LS_CUFFT=1 forces
 // the cuFFT path); otherwise a BQ status.  Scratch: 6N complex per view.
 int ls_conv_pruned(bq_ctx* ctx, int dtype, int n, int B, int op, const void* khat, const void* f, const void* v,
-                   double alpha, double beta, const void* addend, void* scratch, void* out, cudaStream_t st) {
+                   double alpha, double beta, const void* addend, void* scratch, void* out, cudaStream_t st,
+                   const int* active, const void* da, double* dotp, int* nblk) {
   (void)ctx;
   static const bool force_cufft = [] {
     const char* e = std::getenv("BQ_LS_CUFFT");
@@ -510,8 +549,8 @@ int ls_conv_pruned(bq_ctx* ctx, int dtype, int n, int B, int op, const void* kha
   }();
   if (force_cufft) return 1;
   return dtype == BQ_F32
-             ? lsfft::dispatch<float>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st)
-             : lsfft::dispatch<double>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, st);
+             ? lsfft::dispatch<float>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st)
+             : lsfft::dispatch<double>(n, B, op, khat, f, v, alpha, beta, addend, scratch, out, active, da, dotp, nblk, st);
 }
 
 }  // namespace bq

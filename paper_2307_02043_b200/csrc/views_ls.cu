@@ -610,3 +610,335 @@ extern "C" int bq_ls_potential(bq_ctx* ctx, int32_t dtype, int64_t N, const void
   BQ_CUDA(cudaGetLastError());
   return BQ_OK;
 }
+
+// ===========================================================================
+// Device-resident batched BiCGSTAB (oracle/physics.py bicgstab, per view):
+// all scalar recurrences and stopping decisions are made on the device; the
+// dots ride in the producing kernels (the Green convolution's epilogue, the
+// s and x/r updates) as fixed-order per-block partials; converged views are
+// skipped by every kernel (the convolution passes included).  The host only
+// learns "how many views are still active" one iteration late through a
+// pinned flag, so the GPU never idles on a host round trip.
+// ===========================================================================
+namespace bq {
+namespace {
+
+// state per view (doubles): rho(2) alpha(2) omega(2) rho_new(2) nb beta(2) -> 16
+constexpr int kBS = 16;
+enum { BG_INIT = 0, BG_ALPHA = 1, BG_S = 2, BG_OMEGA = 3, BG_END = 4 };
+
+__device__ __forceinline__ void block_part3(double a, double b, double c, double* out) {
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+    c += __shfl_down_sync(0xffffffffu, c, o);
+  }
+  __shared__ double red[3][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) red[0][w] = a, red[1][w] = b, red[2][w] = c;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) s0 += red[0][q], s1 += red[1][q], s2 += red[2][q];
+    out[0] = s0, out[1] = s1, out[2] = s2;
+  }
+}
+
+template <typename T>
+__global__ void bg_init_kernel(long long N, const typename Cx<T>::V* __restrict__ rhs, typename Cx<T>::V* x,
+                               typename Cx<T>::V* r, typename Cx<T>::V* rh, typename Cx<T>::V* p,
+                               typename Cx<T>::V* v, double* part) {
+  using V = typename Cx<T>::V;
+  const int b = blockIdx.y;
+  const long long o = (long long)b * N;
+  V z;
+  z.x = 0, z.y = 0;
+  double nn = 0.0;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const V bb = rhs[o + j];
+    x[o + j] = z, r[o + j] = bb, rh[o + j] = bb, p[o + j] = z, v[o + j] = z;
+    nn += (double)bb.x * bb.x + (double)bb.y * bb.y;
+  }
+  block_part3(nn, 0.0, nn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
+}
+
+// p = r + beta (p - omega v)
+template <typename T>
+__global__ void bg_p_kernel(long long N, const typename Cx<T>::V* __restrict__ r, const typename Cx<T>::V* __restrict__ v,
+                            const double* __restrict__ state, typename Cx<T>::V* p, const int* __restrict__ active) {
+  using V = typename Cx<T>::V;
+  const int b = blockIdx.y;
+  if (!active[b]) return;
+  const double* s = state + kBS * b;
+  V beta, omega;
+  beta.x = (T)s[9], beta.y = (T)s[10];
+  omega.x = (T)s[4], omega.y = (T)s[5];
+  const long long o = (long long)b * N;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const V ov = cmul(omega, v[o + j]);
+    V q;
+    q.x = p[o + j].x - ov.x;
+    q.y = p[o + j].y - ov.y;
+    const V bq = cmul(beta, q);
+    V out;
+    out.x = r[o + j].x + bq.x;
+    out.y = r[o + j].y + bq.y;
+    p[o + j] = out;
+  }
+}
+
+// s = r - alpha v, partial ||s||^2
+template <typename T>
+__global__ void bg_s_kernel(long long N, const typename Cx<T>::V* __restrict__ r, const typename Cx<T>::V* __restrict__ v,
+                            const double* __restrict__ state, typename Cx<T>::V* __restrict__ s,
+                            const int* __restrict__ active, double* part) {
+  using V = typename Cx<T>::V;
+  const int b = blockIdx.y;
+  if (!active[b]) return;
+  V alpha;
+  alpha.x = (T)state[kBS * b + 2], alpha.y = (T)state[kBS * b + 3];
+  const long long o = (long long)b * N;
+  double nn = 0.0;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const V av = cmul(alpha, v[o + j]);
+    V q;
+    q.x = r[o + j].x - av.x;
+    q.y = r[o + j].y - av.y;
+    s[o + j] = q;
+    nn += (double)q.x * q.x + (double)q.y * q.y;
+  }
+  block_part3(nn, 0.0, nn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
+}
+
+// mode 1: x += alpha p ; mode 2: x += alpha p + omega s, r = s - omega t, partials (<rh, r>, ||r||^2)
+template <typename T>
+__global__ void bg_x_kernel(long long N, const double* __restrict__ state, const typename Cx<T>::V* __restrict__ p,
+                            const typename Cx<T>::V* __restrict__ s, const typename Cx<T>::V* __restrict__ t,
+                            const typename Cx<T>::V* __restrict__ rh, typename Cx<T>::V* x, typename Cx<T>::V* r,
+                            const int* __restrict__ mode, double* part) {
+  using V = typename Cx<T>::V;
+  const int b = blockIdx.y;
+  const int md = mode[b];
+  if (md == 0) return;
+  const double* st = state + kBS * b;
+  V alpha, omega;
+  alpha.x = (T)st[2], alpha.y = (T)st[3];
+  omega.x = (T)st[4], omega.y = (T)st[5];
+  const long long o = (long long)b * N;
+  double dre = 0.0, dim = 0.0, dnn = 0.0;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const V ap = cmul(alpha, p[o + j]);
+    V xo = x[o + j];
+    xo.x += ap.x;
+    xo.y += ap.y;
+    if (md == 2) {
+      const V sv = s[o + j];
+      const V os = cmul(omega, sv);
+      xo.x += os.x;
+      xo.y += os.y;
+      const V ot = cmul(omega, t[o + j]);
+      V rr;
+      rr.x = sv.x - ot.x;
+      rr.y = sv.y - ot.y;
+      r[o + j] = rr;
+      const V a = rh[o + j];
+      dre += (double)a.x * rr.x + (double)a.y * rr.y;
+      dim += (double)a.x * rr.y - (double)a.y * rr.x;
+      dnn += (double)rr.x * rr.x + (double)rr.y * rr.y;
+    }
+    x[o + j] = xo;
+  }
+  block_part3(dre, dim, dnn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
+}
+
+// scalar recurrences and decisions, one warp per view (fixed-order sums)
+__global__ void bg_ctl_kernel(int stage, int nblk, const double* __restrict__ part, double* state, int* mode,
+                              int* active, int* act2, int* iters, int it, double tol, int* count) {
+  const int b = blockIdx.x, lane = threadIdx.x;
+  const bool need = stage == BG_INIT || (stage == BG_OMEGA ? mode[b] == 2 : active[b] != 0);
+  double s0 = 0.0, s1 = 0.0, s2 = 0.0;
+  if (need)
+    for (int k = lane; k < nblk; k += 32) {
+      const double* q = part + ((long long)b * nblk + k) * 3;
+      s0 += q[0], s1 += q[1], s2 += q[2];
+    }
+  for (int o = 16; o > 0; o >>= 1) {
+    s0 += __shfl_down_sync(0xffffffffu, s0, o);
+    s1 += __shfl_down_sync(0xffffffffu, s1, o);
+    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  }
+  if (lane != 0) return;
+  double* s = state + kBS * b;
+  if (stage == BG_INIT) {
+    const double nb = sqrt(s2);
+    s[0] = 1.0, s[1] = 0.0, s[2] = 1.0, s[3] = 0.0, s[4] = 1.0, s[5] = 0.0;
+    s[6] = s0, s[7] = 0.0;  // rho_new = <rh, r> = ||b||^2
+    s[8] = nb;
+    s[9] = s0, s[10] = 0.0;  // beta = (rho_new / 1) (1 / 1)
+    iters[b] = 0;
+    mode[b] = 0;
+    act2[b] = 0;
+    active[b] = (nb > 0.0 && 1.0 > tol) ? 1 : 0;  // res = ||r0|| / ||b|| = 1
+    return;
+  }
+  if (!need) return;
+  if (stage == BG_ALPHA) {
+    const double2 a = cdiv(make_double2(s[6], s[7]), make_double2(s0, s1));
+    s[2] = a.x, s[3] = a.y;
+  } else if (stage == BG_S) {
+    const bool early = sqrt(s2) <= tol * s[8];
+    mode[b] = early ? 1 : 2;
+    act2[b] = early ? 0 : 1;
+  } else if (stage == BG_OMEGA) {
+    // <t, s> = sum conj(t) s = conj(sum conj(s) t)
+    const double2 om = cdiv(make_double2(s0, -s1), make_double2(s2, 0.0));
+    s[4] = om.x, s[5] = om.y;
+  } else {  // BG_END
+    iters[b] = it;
+    bool done = true;
+    if (mode[b] == 2) {
+      const double2 rho = make_double2(s[6], s[7]);  // rho = rho_new
+      s[0] = rho.x, s[1] = rho.y;
+      s[6] = s0, s[7] = s1;  // next rho_new = <rh, r>
+      done = sqrt(s2) / s[8] <= tol;
+      if (!done) {
+        const double2 beta = cmuld(cdiv(make_double2(s0, s1), rho), cdiv(make_double2(s[2], s[3]), make_double2(s[4], s[5])));
+        s[9] = beta.x, s[10] = beta.y;
+      }
+    }
+    active[b] = done ? 0 : 1;
+    mode[b] = 0;
+    act2[b] = 0;
+    if (!done) atomicAdd(count, 1);
+  }
+}
+
+// per-view (sum conj(a) c, ||c||^2) block partials (cuFFT path of the convolution)
+template <typename T>
+__global__ void bg_dot_kernel(long long N, const typename Cx<T>::V* __restrict__ a, const typename Cx<T>::V* __restrict__ c,
+                              double* part) {
+  const int b = blockIdx.y;
+  const long long o = (long long)b * N;
+  double dre = 0.0, dim = 0.0, dnn = 0.0;
+  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
+    const auto av = a[o + j];
+    const auto cv = c[o + j];
+    dre += (double)av.x * cv.x + (double)av.y * cv.y;
+    dim += (double)av.x * cv.y - (double)av.y * cv.x;
+    dnn += (double)cv.x * cv.x + (double)cv.y * cv.y;
+  }
+  block_part3(dre, dim, dnn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
+}
+
+int bg_vec_blocks(bq_ctx* ctx, long long N, int B) {
+  const long long want = std::max<long long>(1, (long long)ctx->num_sms * 8 / B);
+  return (int)std::max<long long>(1, std::min<long long>(want, (N + 255) / 256));
+}
+
+int bg_conv_blocks(int n) {
+  // rows of the XI pass / lines per block (ls_fft.cu run<>: L = min(256 / C, m))
+  const int m = 2 * n;
+  int C = 0;
+  switch (m) {
+    case 16: case 32: C = 4; break;
+    case 64: case 128: C = 8; break;
+    case 256: case 512: C = 16; break;
+    default: return 0;
+  }
+  const int L = std::min(256 / C, m);
+  return (n * n + L - 1) / L;
+}
+
+template <typename T>
+int bg_conv(bq_ctx* ctx, int dtype, int n, int B, int op, const void* khat, const void* f, const void* v, void* scratch,
+            void* out, const int* active, const void* da, double* part, int nbv, int* nblk, cudaStream_t st) {
+  int rc = ls_conv_pruned(ctx, dtype, n, B, op, khat, f, v, 1.0, -1.0, nullptr, scratch, out, st, active, da, part,
+                          nblk);
+  if (rc != 1) return rc;
+  if ((rc = ls_conv_impl<T>(ctx, dtype, n, B, op, khat, f, v, 1.0, -1.0, nullptr, scratch, out, st))) return rc;
+  const long long N = (long long)n * n * n;
+  bg_dot_kernel<T><<<dim3(nbv, B), 256, 0, st>>>(N, (const typename Cx<T>::V*)da, (const typename Cx<T>::V*)out, part);
+  *nblk = nbv;
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+template <typename T>
+int bicgstab_impl(bq_ctx* ctx, int dtype, int n, int B, int adjoint, const void* khat, const void* f, const void* rhs,
+                  void* xout, double tol, int max_iter, void* vec_work, void* conv_scratch, void* small_work,
+                  int* iters, cudaStream_t st) {
+  using V = typename Cx<T>::V;
+  const long long N = (long long)n * n * n;
+  V* r = (V*)vec_work;
+  V* rh = r + B * N;
+  V* p = rh + B * N;
+  V* v = p + B * N;
+  V* s = v + B * N;
+  V* t = s + B * N;
+  V* x = (V*)xout;
+  const int nbv = bg_vec_blocks(ctx, N, B);
+  const int pmax = std::max(nbv, bg_conv_blocks(n));
+  double* part = (double*)small_work;
+  double* state = part + (size_t)B * pmax * 3;
+  int* mode = (int*)(state + (size_t)B * kBS);
+  int* active = mode + B;
+  int* act2 = active + B;
+  int* count = act2 + B;
+  if (!ctx->host_flags) {
+    BQ_CUDA(cudaHostAlloc((void**)&ctx->host_flags, 4 * sizeof(int), cudaHostAllocDefault));
+    BQ_CUDA(cudaEventCreateWithFlags(&ctx->flag_ev[0], cudaEventDisableTiming));
+    BQ_CUDA(cudaEventCreateWithFlags(&ctx->flag_ev[1], cudaEventDisableTiming));
+  }
+  const int op = adjoint ? 1 : 0;
+  const dim3 vg(nbv, B);
+  bg_init_kernel<T><<<vg, 256, 0, st>>>(N, (const V*)rhs, x, r, rh, p, v, part);
+  bg_ctl_kernel<<<B, 32, 0, st>>>(BG_INIT, nbv, part, state, mode, active, act2, iters, 0, tol, count);
+  BQ_CUDA(cudaGetLastError());
+  int rc;
+  for (int it = 1; it <= max_iter; ++it) {
+    int nb = 0;
+    bg_p_kernel<T><<<vg, 256, 0, st>>>(N, r, v, state, p, active);
+    if ((rc = bg_conv<T>(ctx, dtype, n, B, op, khat, f, p, conv_scratch, v, active, rh, part, nbv, &nb, st))) return rc;
+    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_ALPHA, nb, part, state, mode, active, act2, iters, it, tol, count);
+    bg_s_kernel<T><<<vg, 256, 0, st>>>(N, r, v, state, s, active, part);
+    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_S, nbv, part, state, mode, active, act2, iters, it, tol, count);
+    if ((rc = bg_conv<T>(ctx, dtype, n, B, op, khat, f, s, conv_scratch, t, act2, s, part, nbv, &nb, st))) return rc;
+    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_OMEGA, nb, part, state, mode, active, act2, iters, it, tol, count);
+    BQ_CUDA(cudaMemsetAsync(count, 0, sizeof(int), st));
+    bg_x_kernel<T><<<vg, 256, 0, st>>>(N, state, p, s, t, rh, x, r, mode, part);
+    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_END, nbv, part, state, mode, active, act2, iters, it, tol, count);
+    BQ_CUDA(cudaGetLastError());
+    BQ_CUDA(cudaMemcpyAsync(&ctx->host_flags[it & 1], count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BQ_CUDA(cudaEventRecord(ctx->flag_ev[it & 1], st));
+    if (it >= 2) {  // one iteration late: the GPU already has iteration `it` queued
+      BQ_CUDA(cudaEventSynchronize(ctx->flag_ev[(it - 1) & 1]));
+      if (ctx->host_flags[(it - 1) & 1] == 0) break;
+    }
+  }
+  return BQ_OK;
+}
+
+}  // namespace
+}  // namespace bq
+
+extern "C" int64_t bq_ls_bicgstab_small_bytes(bq_ctx* ctx, int32_t n, int32_t B) {
+  if (!ctx || n < 1 || B < 1) return -1;
+  const long long N = (long long)n * n * n;
+  const int pmax = std::max(bg_vec_blocks(ctx, N, B), bg_conv_blocks(n));
+  return (int64_t)((size_t)B * pmax * 3 * sizeof(double) + (size_t)B * kBS * sizeof(double) + (3 * (size_t)B + 4) * sizeof(int));
+}
+
+// x_b = A^-1 b_b (adjoint = 0: A = I - G_dom diag f; 1: A^H = I - diag(f) G_dom^H) for the B views, BiCGSTAB from
+// x0 = 0 to the relative residual tol; iters (device, B ints) = iterations per view (oracle/physics.py bicgstab).
+extern "C" int bq_ls_bicgstab(bq_ctx* ctx, int32_t dtype, int32_t n, int32_t B, int32_t adjoint, const void* khat,
+                              const void* f, const void* rhs, void* x, double tol, int32_t max_iter, void* vec_work,
+                              void* conv_scratch, void* small_work, int32_t* iters, void* stream) {
+  BQ_CHECK(ctx && khat && f && rhs && x && vec_work && conv_scratch && small_work && iters && B >= 1 && n >= 1 &&
+               max_iter >= 0,
+           BQ_EINVAL, "bq_ls_bicgstab: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  return dtype == BQ_F32 ? bicgstab_impl<float>(ctx, dtype, n, B, adjoint, khat, f, rhs, x, tol, max_iter, vec_work,
+                                                 conv_scratch, small_work, (int*)iters, st)
+                         : bicgstab_impl<double>(ctx, dtype, n, B, adjoint, khat, f, rhs, x, tol, max_iter, vec_work,
+                                                  conv_scratch, small_work, (int*)iters, st);
+}

@@ -754,183 +754,6 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
     return;
   }
-    constexpr bool tr = false;
-    if (tr) t_a = global_ns();
-    mbar_wait(&full[b], (b ? uses[1] : uses[0]) & 1u);
-#if BQ_PROX_TRACE
-    if (s == 0 && blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 7] = global_ns();
-#endif
-    if (tr) t_b = global_ns();
-    if (b) uses[1] += 1;
-    else uses[0] += 1;
-    const int k = cons.k;
-    const int y0 = (int)cons.tile * TYe;
-    const int y = y0 - rpw + sr;
-    const bool act = used && y >= 0 && y < K2;
-    const bool real = act && !halo;
-    const bool warm = k < cons.z0;
-    const bool pin = cons.has_pin();
-    if (k == cons.zs - 1) f3prev[0] = f3prev[1] = f3prev[2] = f3prev[3] = 0;
-    const int rowoff = sr * K1 + xb;
-    // per-step partial sums in the field type (one f64 conversion per step)
-    T fa[NACC];
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) fa[q] = 0;
-    post(fa);  // deferred post phase of the previous step
-
-    // ---- q(k+1) of this row (+ the row below the tile, by warp 0) -------
-    T qn4[4] = {0, 0, 0, 0}, ien[4] = {1, 1, 1, 1}, un[R > 0 ? R : 1][4];
-#pragma unroll
-    for (int c = 0; c < (R > 0 ? R : 1); ++c) un[c][0] = un[c][1] = un[c][2] = un[c][3] = 0;
-    if (cons.has_qin()) {
-      auto qrow = [&](long long off, T (&q)[4], T (&ie)[4], T (&u)[R > 0 ? R : 1][4]) {
-        T l[4], h[4];
-        Vec4<T>::rw(stg + M.A * g.slot_elems + off, q);
-        if (diag) Vec4<T>::rw(stg + M.D * g.slot_elems + off, ie);  // 1/d, precomputed
-        else ie[0] = ie[1] = ie[2] = ie[3] = itauT;
-#pragma unroll
-        for (int c = 0; c < R; ++c) Vec4<T>::rw(stg + (M.U0 + c) * g.slot_elems + off, u[c]);
-        if (M.LO >= 0) Vec4<T>::rw(stg + M.LO * g.slot_elems + off, l);
-        else l[0] = l[1] = l[2] = l[3] = lo_s;
-        if (M.HI >= 0) Vec4<T>::rw(stg + M.HI * g.slot_elems + off, h);
-        else h[0] = h[1] = h[2] = h[3] = hi_s;
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          T z = q[v];
-#pragma unroll
-          for (int c = 0; c < R; ++c) z += (sg * u[c][v] * ie[v]) * sh.gz[c];
-          q[v] = clampv(z, l[v], h[v]);
-        }
-      };
-      T* qdst = qbuf + (long long)((k + 1) & 1) * g.slot_elems;
-      if (act) {
-        qrow(rowoff, qn4, ien, un);
-        Vec4<T>::st(qdst + rowoff, qn4);
-      }
-      if (halo && yr == 0 && y0 + TYe < K2) {
-        const long long off = (long long)(W * rpw) * K1 + xb;
-        T qb[4], ib[4], ub[R > 0 ? R : 1][4];
-        qrow(off, qb, ib, ub);
-        Vec4<T>::st(qdst + off, qb);
-      }
-    }
-
-    // ---- dual update at plane k (dual_tv_solver.py:225-235) -------------
-    const T qright = __shfl_down_sync(FULLM, qc[0], 1);  // x+1 of element 3
-    T src[3][4];
-    T vv[4] = {0, 0, 0, 0};
-#pragma unroll
-    for (int n = 0; n < 3; ++n) src[n][0] = src[n][1] = src[n][2] = src[n][3] = 0;
-    if (pin && act) {
-      const bool has_y = nd >= 2 && y < K2 - 1;
-      const bool has_up = nd >= 3 && k < K3 - 1;
-      T qy[4] = {0, 0, 0, 0};
-      if (has_y) Vec4<T>::rw(qbuf + (long long)(k & 1) * g.slot_elems + rowoff + K1, qy);
-      T pc4[3][4], pp4[3][4];
-#pragma unroll
-      for (int n = 0; n < 3; ++n) {
-        pc4[n][0] = pc4[n][1] = pc4[n][2] = pc4[n][3] = 0;
-        if (n < nd) Vec4<T>::rw(stg + (M.PC0 + n) * g.slot_elems + rowoff, pc4[n]);
-        if (n < nd && M.PP0 >= 0) Vec4<T>::rw(stg + (M.PP0 + n) * g.slot_elems + rowoff, pp4[n]);
-      }
-      T pn[3][4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        T gr[3];
-        const T right = (v < 3) ? qc[v + 1] : qright;
-        gr[0] = (xb + v < K1 - 1) ? right - qc[v] : (T)0;
-        gr[1] = has_y ? qy[v] - qc[v] : (T)0;
-        gr[2] = has_up ? qn4[v] - qc[v] : (T)0;
-        T w[3], pc3[3];
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          pc3[n] = pc4[n][v];
-          T pb = pc3[n];
-          if (M.PP0 >= 0 && n < nd) pb = pc3[n] + m_prev * (pc3[n] - pp4[n][v]);  // P_bar_{i-1} (:235)
-          w[n] = (n < nd) ? pb + step * gr[n] : (T)0;
-        }
-        if (iso) {
-          T ss = w[0] * w[0];
-          if (nd >= 2) ss += w[1] * w[1];
-          if (nd >= 3) ss += w[2] * w[2];
-          ball(w, ss);
-        } else {
-#pragma unroll
-          for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
-        }
-#pragma unroll
-        for (int n = 0; n < 3; ++n) {
-          pn[n][v] = w[n];
-          if (real && !warm && n < nd) {
-            const T df = w[n] - pc3[n];
-            fa[V::NRM] += df * df;
-            fa[V::NRM + 1] += pc3[n] * pc3[n];
-          }
-          src[n][v] = div_p ? w[n] : w[n] + m_cur * (w[n] - pc3[n]);
-        }
-      }
-      if (real && !warm) {
-        const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
-#pragma unroll
-        for (int n = 0; n < 3; ++n)
-          if (n < nd) Vec4<T>::st(Pn + n * N + j, pn[n]);
-        Vec4<T>::rw(stg + M.V * g.slot_elems + rowoff, vv);
-      }
-      if (nd >= 2) {
-        Vec4<T>::st(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff, src[1]);
-      }
-    }
-    const unsigned long long t_c = tr ? global_ns() : 0;
-    named_sync(1, W * 32);  // q(k+1), div-source rows published; stage b fully read
-    if (threadIdx.x == 0) mbar_arrive(&empty[b]);
-    if (tr) {
-      A.trace[4 * s + 0] = t_a;
-      A.trace[4 * s + 1] = t_b;
-      A.trace[4 * s + 2] = t_c;
-      A.trace[4 * s + 3] = global_ns();
-    }
-
-    // ---- defer the post phase of this step -------------------------------
-    p_do = pin && !warm && used && !halo;
-    p_real = real;
-    p_y = y;
-    p_k = k;
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      p_src[0][v] = src[0][v];
-      p_src[1][v] = src[1][v];
-      p_src[2][v] = src[2][v];
-      p_vv[v] = vv[v];
-      p_iec[v] = iec[v];
-      p_f3[v] = f3prev[v];
-#pragma unroll
-      for (int c = 0; c < (R > 0 ? R : 1); ++c) p_uc[c][v] = uc[c][v];
-    }
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) acc[q] += (double)fa[q];
-    // ---- carries -------------------------------------------------------
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      f3prev[v] = src[2][v];
-      qc[v] = qn4[v];
-      iec[v] = ien[v];
-#pragma unroll
-      for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][v] = un[c][v];
-    }
-    cons.advance();
-    ++s;
-  }
-  {
-    T fa[NACC];
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) fa[q] = 0;
-    post(fa);  // the last step's post phase (its srcbuf rows were published by the last barrier)
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) acc[q] += (double)fa[q];
-  }
-}
-
-#else
   StepIter cons;
   cons.init(seg_begin, seg_end, K3, nd);
   T qc[4] = {0, 0, 0, 0}, iec[4] = {1, 1, 1, 1}, uc[R > 0 ? R : 1][4];
@@ -1157,7 +980,6 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   }
 }
 
-#endif
 // ---------------------------------------------------------------------------
 // The kernel
 // ---------------------------------------------------------------------------

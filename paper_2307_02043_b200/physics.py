@@ -124,60 +124,36 @@ class ScatterViewSet:
         return out
 
     # -- batched BiCGSTAB (oracle/physics.py bicgstab) ------------------------
-    def bicgstab(self, apply_a, b):
+    def solve(self, adjoint, f, b):
+        """x_b = A^-1 b_b for the B views of `b` (adjoint: A^H), BiCGSTAB from x0 = 0 to
+        the relative residual `tol`, run entirely on the device (bq_ls_bicgstab:
+        scalar recurrences and stopping tests on the GPU, converged views skipped).
+        Returns (x, iterations per view)."""
         B, N = b.shape
-        x = torch.zeros_like(b)
-        r = b.clone()
-        rh = r.clone()
-        p = torch.zeros_like(b)
-        v = torch.zeros_like(b)
-        state = torch.zeros(B, 8, dtype=torch.float64, device=self.device)
-        state[:, 0] = 1.0  # rho
-        state[:, 2] = 1.0  # alpha
-        state[:, 4] = 1.0  # omega
-        coef = torch.zeros(B, 4, dtype=torch.float64, device=self.device)
-        nb = torch.sqrt(self.cdot(b, b).view(B, 2)[:, 0]).cpu().numpy()
-        active_h = (nb > 0).astype(np.int32)
-        iters = np.zeros(B, dtype=np.int64)
-        res0 = np.zeros(B)
-        active = torch.from_numpy(active_h.copy()).to(self.device)
-        mode = torch.zeros(B, dtype=torch.int32, device=self.device)
-        lib, ctx, code, st = self.lib, self.ctx, self.code, self._st()
-        for it in range(1, self.max_iter + 1):
-            if not active_h.any():
-                break
-            d = self.cdot(rh, r)
-            self._check(lib.bq_bicg_scalars(ctx, B, 0, d.data_ptr(), None, state.data_ptr(), coef.data_ptr(), st), "s0")
-            self._check(lib.bq_bicg_p(ctx, code, N, B, r.data_ptr(), v.data_ptr(), coef.data_ptr(), p.data_ptr(),
-                                      active.data_ptr(), st), "bicg_p")
-            v = apply_a(p)
-            d = self.cdot(rh, v)
-            self._check(lib.bq_bicg_scalars(ctx, B, 1, d.data_ptr(), None, state.data_ptr(), coef.data_ptr(), st), "s1")
-            s = self.caxpy(r, state[:, 2:], 8, -1.0, v)  # s = r - alpha v
-            ns = torch.sqrt(self.cdot(s, s).view(B, 2)[:, 0]).cpu().numpy()
-            early = (ns <= self.tol * nb) & (active_h > 0)
-            t = apply_a(s)
-            d0 = self.cdot(t, s)
-            d1 = self.cdot(t, t)
-            self._check(lib.bq_bicg_scalars(ctx, B, 2, d0.data_ptr(), d1.data_ptr(), state.data_ptr(),
-                                            coef.data_ptr(), st), "s2")
-            md = np.where(active_h > 0, np.where(early, 1, 2), 0).astype(np.int32)
-            mode.copy_(torch.from_numpy(md))
-            self._check(lib.bq_bicg_x(ctx, code, N, B, state.data_ptr(), p.data_ptr(), s.data_ptr(), t.data_ptr(),
-                                      x.data_ptr(), r.data_ptr(), mode.data_ptr(), st), "bicg_x")
-            nr = torch.sqrt(self.cdot(r, r).view(B, 2)[:, 0]).cpu().numpy()
-            done = early | ((nr <= self.tol * nb) & (md == 2))
-            iters[(active_h > 0)] = it
-            active_h = np.where(done, 0, active_h).astype(np.int32)
-            active.copy_(torch.from_numpy(active_h.copy()))
-        return x, iters
+        key = (B, "bicg")
+        if key not in self._pad:
+            small = int(self.lib.bq_ls_bicgstab_small_bytes(self.ctx, self.n, B))
+            if small < 0:
+                raise ValueError("bq_ls_bicgstab_small_bytes failed")
+            self._pad[key] = (torch.empty(6, B, N, dtype=self.cdtype, device=self.device),
+                              torch.empty(small, dtype=torch.uint8, device=self.device),
+                              torch.empty(B, dtype=torch.int32, device=self.device))
+        vec, small, iters = self._pad[key]
+        b = b.contiguous()
+        x = torch.empty_like(b)
+        self._check(self.lib.bq_ls_bicgstab(self.ctx, self.code, self.n, B, int(adjoint), self.khat.data_ptr(),
+                                            f.data_ptr(), b.data_ptr(), x.data_ptr(), self.tol, self.max_iter,
+                                            vec.data_ptr(), self._padbuf(B).data_ptr(), small.data_ptr(),
+                                            iters.data_ptr(), self._st()), "ls_bicgstab")
+        return x, iters.cpu().numpy().astype(np.int64)
 
+    # -- operators ---------------------------------------------------------------
     # -- operators ---------------------------------------------------------------
     def total_field(self, f, views):
         uin = self.incident(views)
         if self.model == "born":
             return uin, np.zeros(len(views), dtype=np.int64)
-        return self.bicgstab(lambda q: self.conv(0, f, q, 1.0, -1.0), uin)
+        return self.solve(False, f, uin)
 
     def forward_c(self, x, views):
         f, _ = self.potential(x)
@@ -199,7 +175,7 @@ class ScatterViewSet:
     def vjp_from_residual(self, x, views, r_c, f, fp, u, grad, scale, accumulate):
         w = self.conv(3, None, r_c)
         if self.model == "ls":
-            z, it = self.bicgstab(lambda q: self.conv(1, f, q, 1.0, -1.0), self._cmul_conj_f(f, w))
+            z, it = self.solve(True, f, self._cmul_conj_f(f, w))
             self.iters_adjoint.extend(int(i) for i in it)
             w = self.conv(1, None, z, 0.0, 1.0, addend=w)  # w + G_dom^H z
         self._check(self.lib.bq_ls_grad_accum(self.ctx, self.code, self.N, len(views), fp.data_ptr(), u.data_ptr(),
@@ -245,7 +221,7 @@ class ScatterViewSet:
                                             q.data_ptr(), self._st()), "cscale")
         if self.model == "ls":
             rhs = self.conv(0, None, q)  # G_dom q
-            z, _ = self.bicgstab(lambda v: self.conv(0, f, v, 1.0, -1.0), rhs)
+            z, _ = self.solve(False, f, rhs)
             fz = self._cmul_conj_f(f, z)  # f real: f . z
             q = q + fz
         return self.conv(2, None, q)
