@@ -186,10 +186,18 @@ def run_ours(args):
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
+    # BQ_BENCH_SHARE_GPU=1: functional check of the N>1 code path on one GPU
+    # (gloo, all ranks on device 0) -- never a measurement
+    share = os.environ.get("BQ_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
 
     import paper_2307_02043_b200 as bq
     from paper_2307_02043_b200 import dual_tv_solver as D
@@ -274,8 +282,8 @@ def run_ours(args):
         e2e = float(t.item())
 
     ls = None
-    if not args.no_ls and rank == 0:
-        ls = ls_measure(args, dev)
+    if not args.no_ls:
+        ls = ls_measure(args, dev, ws)  # collective at N > 1
 
     if rank == 0:
         peak, peak_kind = hbm_peak()
@@ -321,7 +329,7 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def ls_measure(args, dev):
+def ls_measure(args, dev, ws=1):
     """Secondary metric (BASELINE 'views*voxels/s of LS forward+adjoint'): one
     subset gradient of config 4 (n=128 padded to 256^3, c64, 16 of 64 views on a
     40 deg cone, 12 ellipsoids dn~U[0.01,0.1], 25 dB) at x = x_gt / 2."""
@@ -336,7 +344,19 @@ def ls_measure(args, dev):
                                       batch=16, max_iter=500, device=dev)
     x = torch.tensor(0.5 * xgt, dtype=torch.float32, device=dev)
     idx = list(range(0, 64, 4))
-    vs.subset_gradient(idx, x)  # plans, warm-up
+    if ws > 1:
+        # view-sharded: each rank takes a contiguous chunk of the subset,
+        # one NCCL all-reduce of the gradient; the time is the max over ranks
+        import torch.distributed as dist
+
+        from paper_2307_02043_b200 import dist as DI
+
+        def grad():
+            return DI.subset_gradient(vs, idx, x)
+    else:
+        def grad():
+            return vs.subset_gradient(idx, x)
+    grad()  # plans, warm-up
     times, kf, ka = [], [], []
     for _ in range(max(1, args.ls_steps)):
         vs.iters_forward.clear()
@@ -344,12 +364,17 @@ def ls_measure(args, dev):
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize(dev)
         s.record()
-        vs.subset_gradient(idx, x)
+        grad()
         e.record()
         torch.cuda.synchronize(dev)
-        times.append(s.elapsed_time(e))
-        kf.append(float(np.mean(vs.iters_forward)))
-        ka.append(float(np.mean(vs.iters_adjoint)))
+        t_ms = s.elapsed_time(e)
+        if ws > 1:
+            tt = torch.tensor([t_ms], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t_ms = float(tt.item())
+        times.append(t_ms)
+        kf.append(float(np.mean(vs.iters_forward)) if vs.iters_forward else 0.0)
+        ka.append(float(np.mean(vs.iters_adjoint)) if vs.iters_adjoint else 0.0)
     ms = float(np.median(times))
     Kf, Ka = float(np.mean(kf)), float(np.mean(ka))
     # bytes per view*voxel = (2 B_mv + 128) (K_f + K_a) + 92, with B_mv the
@@ -361,9 +386,11 @@ def ls_measure(args, dev):
     bpv = (2.0 * b_mv + 128.0) * (Kf + Ka) + 92.0
     vv = len(idx) * n ** 3
     peak, _ = hbm_peak()
+    peak *= ws  # whole-job bytes over ws GPUs
     achieved = vv * bpv / (ms * 1e-3) / 1e9
     return {"metric": "LS forward+adjoint views*voxels/s", "value": vv / (ms * 1e-3), "unit": "view*voxel/s",
             "ms_per_subset_gradient": ms, "views": len(idx), "n": n, "padded": 2 * n, "dtype": "c64",
+            "n_gpus": ws, "scaling": "strong", "parallelism": f"view-sharded x{ws}, one all-reduce",
             "K_f": Kf, "K_a": Ka,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "algorithmic_bytes_per_view_voxel": bpv, "bytes_per_matvec_per_voxel": b_mv,

@@ -114,3 +114,31 @@ def test_pruned_conv_512_matches_cufft_path(tmp_path, op):
         res[mode] = np.load(path)
     err = np.linalg.norm(res["pruned"] - res["cufft"]) / np.linalg.norm(res["cufft"])
     assert err < 2e-6, err
+
+
+@pytest.mark.parametrize("adjoint", [False, True])
+@pytest.mark.parametrize("n", [12, 16])
+def test_device_bicgstab_matches_oracle_iterates(adjoint, n):
+    """bq_ls_bicgstab (device recurrences, fused dots, skipped converged views) against
+    oracle/physics.py bicgstab view by view: same solution and iteration counts, for
+    A (forward) and A^H (adjoint), on the pruned (n=16) and cuFFT (n=12) paths."""
+    from paper_2307_02043_b200 import physics as PH
+
+    B = 3
+    s = P.Setup(n=n)
+    G = P.Green(s)
+    rng = np.random.default_rng(40 + n + int(adjoint))
+    f = rng.uniform(0.0, 60.0, n ** 3) * (rng.uniform(0, 1, n ** 3) < 0.4)
+    bs = rng.standard_normal((B, n ** 3)) + 1j * rng.standard_normal((B, n ** 3))
+    bs[1] = np.exp(1j * np.arange(n ** 3) * 0.01)  # a smooth right-hand side: its own convergence schedule
+    vs = PH.ScatterViewSet(n, 2, model="ls", dtype=torch.complex128, tol=1e-10, max_iter=200, batch=B)
+    x, it = vs.solve(adjoint, torch.tensor(f, device="cuda"), torch.tensor(bs, device="cuda"))
+    x = x.cpu().numpy()
+    if adjoint:
+        op = lambda v: v - f * G.dom_adj(v)  # noqa: E731
+    else:
+        op = lambda v: v - G.dom(f * v)  # noqa: E731
+    for b in range(B):
+        xr, itr, _ = P.bicgstab(op, bs[b], tol=1e-10, max_iter=200)
+        assert int(it[b]) == itr, (b, int(it[b]), itr)
+        assert np.linalg.norm(x[b] - xr) / np.linalg.norm(xr) < 1e-9
