@@ -241,6 +241,30 @@ def main():
     print(f"wrote {OUT / 'reference_golden.npz'} ({len(out)} arrays)")
     make_config1_golden(tv_ops, wpm, solvers, fm)
     make_config3_small_golden(tv_ops, wpm, solvers, fm)
+    make_baselines_golden(tv_ops, wpm, solvers, fm)
+
+
+def make_baselines_golden(tv_ops, wpm, solvers, fm):
+    """The REFERENCE aspm_run (momentum on / off) and sqnpm_run (solvers.py:320-422)
+    on the same DCT stand-in views as the bqnpm goldens."""
+    out = {}
+    for tag, strength, snr, dims in [("lin", 0.0, 30.0, (10, 9, 8)), ("nl", 0.1, 30.0, (12, 8, 6))]:
+        g = tv_ops.Grid(dims)
+        L = 8
+        views = (fm.make_linear_views(g, L, mask_fraction=0.5, seed=3, noise_snr_db=snr) if strength == 0.0 else
+                 fm.make_nonlinear_views(g, L, strength=strength, mask_fraction=0.5, seed=3, noise_snr_db=snr))
+        for name, runner, kw in [("aspm", solvers.aspm_run, dict(max_outer=10)),
+                                 ("aspm_plain", solvers.aspm_run, dict(max_outer=10, momentum=False)),
+                                 ("sqnpm", solvers.sqnpm_run, dict(max_outer=13))]:
+            cfg = solvers.SolverConfig(subsets=4, tv_weight=2e-3, box=wpm.BoxSet(1.3, 1.4), seed=0, **kw)
+            xr, tr = runner(views, g, cfg)
+            out[f"{name}_{tag}_x"] = xr
+            out[f"{name}_{tag}_cost"] = tr.column("cost")
+            out[f"{name}_{tag}_inner"] = tr.column("inner_iters")
+            out[f"{name}_{tag}_grad_evals"] = tr.column("grad_evals")
+            out[f"{name}_{tag}_full_grad_evals"] = tr.column("full_grad_evals")
+    np.savez_compressed(OUT / "baselines_golden.npz", **out)
+    print(f"wrote {OUT / 'baselines_golden.npz'} ({len(out)} arrays)")
 
 
 def make_config1_golden(tv_ops, wpm, solvers, fm):

@@ -74,3 +74,29 @@ def test_bqnpm_matches_reference_run(golden, tag, strength, dims):
     assert rel_l2(x, golden[f"bqnpm_{tag}_x"]) <= 1e-9
     np.testing.assert_allclose(tr.column("cost"), golden[f"bqnpm_{tag}_cost"], rtol=1e-9)
     np.testing.assert_array_equal(tr.column("inner_iters"), golden[f"bqnpm_{tag}_inner"])
+
+
+@pytest.fixture(scope="module")
+def baselines():
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", "baselines_golden.npz")
+    return dict(np.load(path))
+
+
+@pytest.mark.parametrize("tag,strength,dims", CASES)
+@pytest.mark.parametrize("name", ["aspm", "aspm_plain", "sqnpm"])
+def test_baselines_match_reference_runs(baselines, tag, strength, dims, name):
+    """ASPM (momentum on/off) and SQNPM on the device kernels vs the REFERENCE
+    aspm_run / sqnpm_run (solvers.py:320-422) on the same views."""
+    g, views = _views(tag, strength, dims)
+    kw = {"aspm": dict(max_outer=10), "aspm_plain": dict(max_outer=10, momentum=False),
+          "sqnpm": dict(max_outer=13)}[name]
+    cfg = S.SolverConfig(subsets=4, tv_weight=2e-3, box=BoxSet(1.3, 1.4), seed=0, **kw)
+    runner = S.RUNNERS["aspm" if name.startswith("aspm") else name]
+    x, tr = runner(views, g, cfg)
+    assert rel_l2(x, baselines[f"{name}_{tag}_x"]) <= 1e-9
+    np.testing.assert_allclose(tr.column("cost"), baselines[f"{name}_{tag}_cost"], rtol=1e-9)
+    np.testing.assert_array_equal(tr.column("inner_iters"), baselines[f"{name}_{tag}_inner"])
+    np.testing.assert_array_equal(tr.column("grad_evals"), baselines[f"{name}_{tag}_grad_evals"])
+    np.testing.assert_array_equal(tr.column("full_grad_evals"), baselines[f"{name}_{tag}_full_grad_evals"])
