@@ -37,6 +37,8 @@ for it in [int(a) for a in sys.argv[1:]] or [30, 60, 90]:
     cudart.cudaMemcpy(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(scratch), ctypes.c_size_t(400 * 8), 3)
     torch.cuda.synchronize()
     a = t.cpu().numpy()[320:331]
+    cyc = t.cpu().numpy()[340:342]
+    print("  controller cycles: timeline", cyc[0], "run", cyc[1])
     st = a[:8]
     print("  pass entry after set up:", a[9] - st[6], "ns; pre / prefetched:", a[10] % 100, a[10] // 100)
     print(f"it {it} (ctl it {a[8]}):", "  ".join(f"{names[i]} +{st[i] - st[i - 1]}" for i in range(1, 8) if st[i] and st[i - 1]))

@@ -58,7 +58,7 @@ namespace bq {
 namespace fused {
 using namespace prox;
 
-enum : int { F_SETUP = 0, F_DIV = 1, F_NEWTON = 2, F_FUSED = 3, F_FINAL = 4, F_DONE = 5, F_NLOCAL = 6 };
+enum : int { F_SETUP = 0, F_DIV = 1, F_NEWTON = 2, F_FUSED = 3, F_FINAL = 4, F_DONE = 5, F_NLOCAL = 6, F_NDIST = 7 };
 
 constexpr int CAPW = 64;   // near-list capacity per warp per pass
 constexpr unsigned FULLM = 0xffffffffu;
@@ -84,7 +84,7 @@ struct FCtl {
   int converged, status, last_newton_it, last_newton_conv;
   int final_mode, div_p, have_hist, fallbacks;
   int slot_cur, slot_prev, a_cur, local_steps;
-  int single, nl_ok, pad0, pad1;
+  int single, nl_ok, ndist, pad1;  // ndist: long near list -> distributed Newton steps
   double t, m_prev, m_cur, rel, best_res, last_res, grow;
   double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
   double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK], dmax[BQ_MAX_RANK];
@@ -135,6 +135,7 @@ struct FArgs {
   int trace_thread;           // which thread of block 0 records
   int dbg;                    // debug switches (timing experiments only)
   double grow_min;            // minimum box growth factor of the near-list Newton
+  double ndist_min;           // near lists longer than this take distributed (per-block + barrier) steps
 };
 
 // shared, per-block copy of what the passes read
@@ -412,7 +413,7 @@ struct Ctl {
       if (!(fabs(g - c.gc[i]) <= c.gwid[i])) in_box = false;
     }
     if (in_box) {
-      c.phase = F_NLOCAL;
+      c.phase = c.ndist ? F_NDIST : F_NLOCAL;
     } else {
       if (c.phase != F_NEWTON) c.fallbacks += 1;
       c.phase = F_NEWTON;
@@ -428,6 +429,7 @@ struct Ctl {
     for (int i = 0; i < R; ++i) c.K0[i] = red[V::K0 + i];
     for (int k = 0; k < V::S; ++k) c.Cin[k] = red[V::CIN + k], c.Cout[k] = red[V::COUT + k];
     c.nl_ok = red[V::OVF] == 0.0;
+    c.ndist = red[V::NCNT] > A.ndist_min ? 1 : 0;
     c.fallbacks = 0;
     c.newton_it = 0;
     c.best_res = INFINITY;
@@ -439,6 +441,21 @@ struct Ctl {
     }
     c.phase = F_DIV;  // sentinel so a first out-of-box start is not counted twice
     choose_newton_mode();
+  }
+
+  // phi(beta) = K0 + Cout gw + Cin beta - sum_near u clamp(a + s.gamma) (+ beta in newton_step),
+  // H = Cin + sum_near,inside u s^T (+ I): exact while gamma stays in the aggregates' box
+  __device__ void local_eval(const double* nacc, double* phi, double* hp) const {
+    for (int i = 0; i < R; ++i) {
+      double cw = 0.0, cb = 0.0;
+      for (int k2 = 0; k2 < R; ++k2) {
+        const int kk = i >= k2 ? i * (i + 1) / 2 + k2 : k2 * (k2 + 1) / 2 + i;
+        cw += c.Cout[kk] * c.gw[k2];
+        cb += c.Cin[kk] * c.beta[k2];
+      }
+      phi[i] = c.K0[i] + cw + cb - nacc[i];
+    }
+    for (int k = 0; k < V::S; ++k) hp[k] = c.Cin[k] + nacc[R + k];
   }
 
   __device__ void run(int phase, const double* red) {
@@ -499,6 +516,13 @@ struct Ctl {
         newton_step(red, hp);
         return;
       }
+      case F_NDIST: {
+        // box-exact evaluation, near terms summed block by block (red = sum_near u clamp, H near part)
+        double phi[R > 0 ? R : 1], hp[V::S > 0 ? V::S : 1];
+        local_eval(red, phi, hp);
+        newton_step(phi, hp);
+        return;
+      }
       case F_FUSED: {
         // dual_tv_solver.py:226-239 on the ring
         const double num = sqrt(red[V::NRM]), den = sqrt(red[V::NRM + 1]);
@@ -542,10 +566,11 @@ struct Ctl {
           if (A.beta_io)
             for (int i = 0; i < R; ++i) A.beta_io[i] = c.beta[i];
           for (int i = 0; i < 6; ++i) {
-            const int src = (i == 5) ? F_NLOCAL : i;  // [setup, div, newton (full pass), fused, final, newton (local)]
-            rp->phase_ns[i] = (double)c.phase_ns[src];
-            rp->phase_work_ns[i] = (double)c.phase_work_ns[src];
-            rp->phase_count[i] = c.phase_cnt[src];
+            // [setup, div, newton (full pass), fused, final, newton (on-chip + distributed near list)]
+            const int src = (i == 5) ? F_NLOCAL : i;
+            rp->phase_ns[i] = (double)c.phase_ns[src] + (i == 5 ? (double)c.phase_ns[F_NDIST] : 0.0);
+            rp->phase_work_ns[i] = (double)c.phase_work_ns[src] + (i == 5 ? (double)c.phase_work_ns[F_NDIST] : 0.0);
+            rp->phase_count[i] = c.phase_cnt[src] + (i == 5 ? c.phase_cnt[F_NDIST] : 0);
           }
         }
         c.phase = F_DONE;
@@ -933,8 +958,8 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
 #pragma unroll
       for (int v = 0; v < 4; ++v) l[v] = lo_s, h[v] = hi_s;
       if (real) {
-        if (A.lo_arr) Vec4<T>::ro(A.lo_arr + j, l);
-        if (A.hi_arr) Vec4<T>::ro(A.hi_arr + j, h);
+        if (MODE == 0 && A.lo_arr) Vec4<T>::ro(A.lo_arr + j, l);
+        if (MODE == 0 && A.hi_arr) Vec4<T>::ro(A.hi_arr + j, h);
       }
       bool nrv[4] = {false, false, false, false};
       bool any = false;
@@ -1075,6 +1100,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   const long long seg_elems = (long long)gridDim.x * NW * CAPW * EWN;  // one parity's list area
   T* my_seg0 = reinterpret_cast<T*>(A.near_data) + ((long long)blockIdx.x * NW + warp) * CAPW * EWN;
   int npass = 0;  // DIV/FUSED passes so far (same in every block)
+  int my_cnt = 0;  // this warp's near entries in the last pass
 
   int phase = F_SETUP;
 #if BQ_PROX_TRACE
@@ -1131,6 +1157,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
                                        s_empty, uses, acc, my_seg, ncnt, ovf, pre);
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
+      my_cnt = ncnt;
       if (ovf) acc[V::OVF] += 1.0;
       if (lane == 0) acc[V::NCNT] += (double)ncnt;
 #if BQ_PROX_TRACE
@@ -1321,8 +1348,32 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       }
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
+      my_cnt = ncnt;
       if (ovf) acc[V::OVF] += 1.0;
       if (lane == 0) acc[V::NCNT] += (double)ncnt;
+    } else if (phase == F_NDIST) {
+      // one Newton evaluation over a long near list: every warp sums the
+      // entries it pushed in the last pass (no gather), the barrier reduces
+      nv = V::NEWTON;
+      constexpr int EW = 3 + 2 * (R > 0 ? R : 1);
+      const T* seg = my_seg0 + ((npass - 1) & 1) * seg_elems;
+      for (int e = lane; e < my_cnt; e += 32) {
+        const T* d = seg + (long long)e * EW;
+        T z = d[0];
+#pragma unroll
+        for (int c = 0; c < R; ++c) z += d[3 + R + c] * sh.gz[c];
+        const T l = d[1], h = d[2];
+        const T cz = clampv(z, l, h);
+#pragma unroll
+        for (int c = 0; c < R; ++c) acc[c] += (double)d[3 + c] * (double)cz;
+        if (z > l && z < h) {
+          int k = R;
+#pragma unroll
+          for (int c = 0; c < R; ++c)
+#pragma unroll
+            for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += (double)d[3 + c] * (double)d[3 + R + c2];
+        }
+      }
     } else if (phase == F_NEWTON) {
       // full-pass phi(beta) and generalized Jacobian partials (wpm.py:150-167)
       nv = V::NEWTON;
@@ -1461,8 +1512,21 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
     // ---- controller (+ block-local Newton over the near list) ------------
     if (threadIdx.x == 0) {
       Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
+#if BQ_PROX_TRACE
+      const long long c0 = clock64();
+#endif
       ctl.timeline(cur, s_red, barrier);
+#if BQ_PROX_TRACE
+      const long long c1 = clock64();
+#endif
       ctl.run(cur, s_red);
+#if BQ_PROX_TRACE
+      const long long c2 = clock64();
+      if (cur == F_FUSED && blockIdx.x == 0 && tr3_on) {
+        A.trace[340] = (unsigned long long)(c1 - c0);
+        A.trace[341] = (unsigned long long)(c2 - c1);
+      }
+#endif
     }
     csync();
     if (cur == F_FUSED) TR3(4);
@@ -1638,16 +1702,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
           if (threadIdx.x == 0) {
             Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
             double phi[R > 0 ? R : 1], hp[V::S > 0 ? V::S : 1];
-            for (int i = 0; i < R; ++i) {
-              double cw = 0.0, cb = 0.0;
-              for (int k2 = 0; k2 < R; ++k2) {
-                const int kk = i >= k2 ? i * (i + 1) / 2 + k2 : k2 * (k2 + 1) / 2 + i;
-                cw += s_c.Cout[kk] * s_c.gw[k2];
-                cb += s_c.Cin[kk] * s_c.beta[k2];
-              }
-              phi[i] = s_c.K0[i] + cw + cb - nacc[i];
-            }
-            for (int k = 0; k < V::S; ++k) hp[k] = s_c.Cin[k] + nacc[R + k];
+            ctl.local_eval(nacc, phi, hp);
             ctl.timeline(F_NLOCAL, s_red, false);
             s_c.local_steps += 1;
             ctl.newton_step(phi, hp);
@@ -1830,6 +1885,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.trace_thread = getenv("BQ_PROX_TRACE_THREAD") ? atoi(getenv("BQ_PROX_TRACE_THREAD")) : 0;
   A.dbg = getenv("BQ_PROX_DBG") ? atoi(getenv("BQ_PROX_DBG")) : 0;
   A.grow_min = getenv("BQ_PROX_GROW") ? atof(getenv("BQ_PROX_GROW")) : 8.0;
+  A.ndist_min = getenv("BQ_PROX_NDIST") ? atof(getenv("BQ_PROX_NDIST")) : 1024.0;
   BQ_CUDA(cudaMemsetAsync(ctx->ws.barrier, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&A};
   BQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)G), dim3(NT), args, dyn, st));
