@@ -212,19 +212,6 @@ int bq_ls_conv(bq_ctx* ctx, int32_t dtype, int32_t n, int32_t B, int32_t op, con
 /* out_b = f . in_b (f real, N; in/out complex B x N). */
 int bq_cscale_real(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* f, const void* in,
                    void* out, void* stream);
-/* per-view <a_b, c_b> = sum conj(a) c -> out (2B doubles, device), deterministic. */
-int bq_cdot(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* a, const void* c, double* out,
-            void* stream);
-/* out_b = a_b + sgn * coef_b * c_b (coef_b complex at coef[coef_stride * b]); active may be NULL. */
-int bq_caxpy(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* a, const double* coef,
-             int32_t coef_stride, double sgn, const void* c, void* out, const int32_t* active, void* stream);
-/* BiCGSTAB scalar recurrences (stage 0: beta/omega from <rh,r>; 1: alpha; 2: omega). */
-int bq_bicg_scalars(bq_ctx* ctx, int32_t B, int32_t stage, const double* d0, const double* d1,
-                    double* state, double* coef, void* stream);
-int bq_bicg_p(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* r, const void* v,
-              const double* coef, void* p, const int32_t* active, void* stream);
-int bq_bicg_x(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const double* state, const void* p,
-              const void* s, const void* t, void* x, void* r, const int32_t* mode, void* stream);
 /* Device-resident batched BiCGSTAB, x_b = A^-1 rhs_b from x0 = 0 to the relative residual tol
  * (oracle/physics.py bicgstab per view): adjoint 0 solves A = I - G_dom diag f, 1 solves A^H.
  * vec_work: 6 B N complex; conv_scratch: the bq_ls_conv pad_buf; small_work:

@@ -50,11 +50,6 @@ EXPORTS = (
     "bq_ls_conv",
     "bq_ls_bicgstab",
     "bq_ls_bicgstab_small_bytes",
-    "bq_cdot",
-    "bq_caxpy",
-    "bq_bicg_scalars",
-    "bq_bicg_p",
-    "bq_bicg_x",
     "bq_ls_grad_accum",
     "bq_ls_potential",
     "bq_cscale_real",
@@ -148,11 +143,6 @@ _SIGS = {
     "bq_ls_bicgstab": (C.c_int, [_P, _I32, _I32, _I32, _I32, _P, _P, _P, _P, _D, _I32, _P, _P, _P, _P, _P]),
     "bq_ls_bicgstab_small_bytes": (C.c_int64, [_P, _I32, _I32]),
     "bq_cscale_real": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
-    "bq_cdot": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
-    "bq_caxpy": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _I32, _D, _P, _P, _P, _P]),
-    "bq_bicg_scalars": (C.c_int, [_P, _I32, _I32, _P, _P, _P, _P, _P]),
-    "bq_bicg_p": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P, _P, _P]),
-    "bq_bicg_x": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P, _P, _P, _P, _P]),
     "bq_ls_grad_accum": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _D, _P, _I32, _P]),
     "bq_ls_potential": (C.c_int, [_P, _I32, _I64, _P, _D, _D, _I32, _P, _P, _P]),
 }

@@ -6,13 +6,14 @@
 //   bq_green_init        green_kernel_hat       K on the 2n-padded grid, FFT'd once
 //   bq_ls_incident       incident               plane waves generated in-kernel
 //   bq_ls_conv           Green.dom / dom_adj / det / det_adj (+ the LS operator A, A^H)
-//   bq_cdot / bq_bicg_*  bicgstab               batched BiCGSTAB vector algebra
+//   bq_ls_bicgstab       bicgstab               device-resident batched BiCGSTAB
 //
-// B200 design: views are batched (B views per call); the 3-D transforms of the
-// (2n)^3 padded grid are batched cuFFT C2C/Z2Z plans (plan cache in the
-// context); padding + contrast multiply, the spectral Green multiply and the
-// crop + axpy are each ONE fused pointwise kernel over the batch; per-view
-// dot products are deterministic two-stage reductions (no float atomics).
+// B200 design: views are batched (B views per call).  For padded sizes 16..512
+// the convolution is ls_fft.cu's five pruned line passes (the padded grid is
+// never formed); other sizes use batched cuFFT C2C/Z2Z plans (plan cache in the
+// context) between fused pad / spectral-multiply / crop kernels.  The
+// BiCGSTAB below keeps every scalar and decision on the device; its per-view
+// dot products are fixed-order block partials (no float atomics).
 #include <cufft.h>
 
 #include <map>
@@ -257,68 +258,7 @@ __global__ void det_kernel(int n, int B, const typename Cx<T>::V* __restrict__ P
   }
 }
 
-// per-view dots <a_b, c_b> = sum conj(a) c   (stage 1: per-block partials)
-template <typename T>
-__global__ void cdot_kernel(long long N, int B, const typename Cx<T>::V* __restrict__ a,
-                            const typename Cx<T>::V* __restrict__ c, double* __restrict__ partials) {
-  const int b = blockIdx.y;
-  double re = 0.0, im = 0.0;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
-    const auto av = a[(long long)b * N + j];
-    const auto cv = c[(long long)b * N + j];
-    re += (double)av.x * cv.x + (double)av.y * cv.y;
-    im += (double)av.x * cv.y - (double)av.y * cv.x;
-  }
-  __shared__ double sr[32], si[32];
-  for (int o = 16; o > 0; o >>= 1) {
-    re += __shfl_down_sync(0xffffffffu, re, o);
-    im += __shfl_down_sync(0xffffffffu, im, o);
-  }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) sr[warp] = re, si[warp] = im;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double R = 0, I = 0;
-    for (int w = 0; w < (int)(blockDim.x / 32); ++w) R += sr[w], I += si[w];
-    partials[((long long)b * gridDim.x + blockIdx.x) * 2] = R;
-    partials[((long long)b * gridDim.x + blockIdx.x) * 2 + 1] = I;
-  }
-}
-__global__ void cdot_finish(int nblk, int B, const double* partials, double* out /* 2B */) {
-  const int b = threadIdx.x;
-  if (b < B) {
-    double R = 0, I = 0;
-    for (int k = 0; k < nblk; ++k) R += partials[((long long)b * nblk + k) * 2], I += partials[((long long)b * nblk + k) * 2 + 1];
-    out[2 * b] = R;
-    out[2 * b + 1] = I;
-  }
-}
-
-// out[b] = a[b] + coef[b] * c[b]   (coef complex per view, optionally conjugated/negated)
-template <typename T>
-__global__ void caxpy_kernel(long long N, int B, const typename Cx<T>::V* __restrict__ a, const double* __restrict__ coef,
-                             int cstride, double sgn, const typename Cx<T>::V* __restrict__ c,
-                             typename Cx<T>::V* __restrict__ out, const int* __restrict__ active) {
-  using V = typename Cx<T>::V;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N * B; t += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(t / N);
-    if (active && !active[b]) continue;
-    V k;
-    k.x = (T)(sgn * coef[cstride * b]);
-    k.y = (T)(sgn * coef[cstride * b + 1]);
-    const V r = cmul(k, c[t]);
-    V o;
-    o.x = a[t].x + r.x;
-    o.y = a[t].y + r.y;
-    out[t] = o;
-  }
-}
-
-// BiCGSTAB scalar recurrences per view (oracle/physics.py bicgstab)
-//  stage 0: rho_new = d0; beta = (rho_new/rho)(alpha/omega); -> coef[beta, -omega]
-//  stage 1: alpha = rho_new / d0 (d0 = <rh, v>)
-//  stage 2: omega = d0 / d1 (d0 = <t, s>, d1 = <t, t>); rho = rho_new
-// state per view (doubles): [rho(2), alpha(2), omega(2), rho_new(2)]
+// complex double helpers of the BiCGSTAB recurrences
 __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
   const double den = b.x * b.x + b.y * b.y;
   return make_double2((a.x * b.x + a.y * b.y) / den, (a.y * b.x - a.x * b.y) / den);
@@ -326,84 +266,6 @@ __device__ __forceinline__ double2 cdiv(double2 a, double2 b) {
 __device__ __forceinline__ double2 cmuld(double2 a, double2 b) {
   return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
 }
-__global__ void bicg_scalar_kernel(int B, int stage, const double* d0, const double* d1, double* state, double* coef) {
-  const int b = threadIdx.x;
-  if (b >= B) return;
-  double* s = state + 8 * b;
-  double2 rho = make_double2(s[0], s[1]), alpha = make_double2(s[2], s[3]), omega = make_double2(s[4], s[5]);
-  if (stage == 0) {
-    const double2 rn = make_double2(d0[2 * b], d0[2 * b + 1]);
-    const double2 beta = cmuld(cdiv(rn, rho), cdiv(alpha, omega));
-    s[6] = rn.x, s[7] = rn.y;
-    coef[4 * b] = beta.x, coef[4 * b + 1] = beta.y;
-    coef[4 * b + 2] = omega.x, coef[4 * b + 3] = omega.y;
-  } else if (stage == 1) {
-    const double2 rn = make_double2(s[6], s[7]);
-    alpha = cdiv(rn, make_double2(d0[2 * b], d0[2 * b + 1]));
-    s[2] = alpha.x, s[3] = alpha.y;
-  } else {
-    omega = cdiv(make_double2(d0[2 * b], d0[2 * b + 1]), make_double2(d1[2 * b], d1[2 * b + 1]));
-    s[4] = omega.x, s[5] = omega.y;
-    s[0] = s[6], s[1] = s[7];
-  }
-}
-
-// p = r + beta (p - omega v)      (per view, active only)
-template <typename T>
-__global__ void bicg_p_kernel(long long N, int B, const typename Cx<T>::V* __restrict__ r,
-                              const typename Cx<T>::V* __restrict__ v, const double* __restrict__ coef,
-                              typename Cx<T>::V* __restrict__ p, const int* __restrict__ active) {
-  using V = typename Cx<T>::V;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N * B; t += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(t / N);
-    if (!active[b]) continue;
-    V beta, omega;
-    beta.x = (T)coef[4 * b], beta.y = (T)coef[4 * b + 1];
-    omega.x = (T)coef[4 * b + 2], omega.y = (T)coef[4 * b + 3];
-    const V ov = cmul(omega, v[t]);
-    V q;
-    q.x = p[t].x - ov.x;
-    q.y = p[t].y - ov.y;
-    const V bq = cmul(beta, q);
-    V o;
-    o.x = r[t].x + bq.x;
-    o.y = r[t].y + bq.y;
-    p[t] = o;
-  }
-}
-
-// x += alpha p + omega s ; r = s - omega t   (stage "full"); or x += alpha p (early exit)
-template <typename T>
-__global__ void bicg_x_kernel(long long N, int B, const double* __restrict__ state, const typename Cx<T>::V* __restrict__ p,
-                              const typename Cx<T>::V* __restrict__ s, const typename Cx<T>::V* __restrict__ tt,
-                              typename Cx<T>::V* __restrict__ x, typename Cx<T>::V* __restrict__ r,
-                              const int* __restrict__ mode /* per view: 0 skip, 1 early, 2 full */) {
-  using V = typename Cx<T>::V;
-  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < N * B; t += (long long)gridDim.x * blockDim.x) {
-    const int b = (int)(t / N);
-    const int md = mode[b];
-    if (md == 0) continue;
-    V alpha, omega;
-    alpha.x = (T)state[8 * b + 2], alpha.y = (T)state[8 * b + 3];
-    omega.x = (T)state[8 * b + 4], omega.y = (T)state[8 * b + 5];
-    const V ap = cmul(alpha, p[t]);
-    V xo = x[t];
-    xo.x += ap.x;
-    xo.y += ap.y;
-    if (md == 2) {
-      const V os = cmul(omega, s[t]);
-      xo.x += os.x;
-      xo.y += os.y;
-      const V ot = cmul(omega, tt[t]);
-      V rr;
-      rr.x = s[t].x - ot.x;
-      rr.y = s[t].y - ot.y;
-      r[t] = rr;
-    }
-    x[t] = xo;
-  }
-}
-
 // grad[j] += Re(conj(fp_j u_b[j]) * w_b[j]) summed over the batch in view order
 template <typename T>
 __global__ void grad_accum_kernel(long long N, int B, const T* __restrict__ fp, const typename Cx<T>::V* __restrict__ u,
@@ -529,63 +391,6 @@ extern "C" int bq_cscale_real(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, 
   DT_SWITCH(dtype, (cscale_kernel<T><<<grid_for(ctx, N * B), 256, 0, st>>>(N, B, (const T*)f,
                                                                             (const typename Cx<T>::V*)in,
                                                                             (typename Cx<T>::V*)out)));
-  BQ_CUDA(cudaGetLastError());
-  return BQ_OK;
-}
-
-extern "C" int bq_cdot(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* a, const void* c, double* out,
-                       void* stream) {
-  BQ_CHECK(ctx && a && c && out && B >= 1 && B <= 256, BQ_EINVAL, "bq_cdot: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream;
-  const int nblk = (int)std::min<long long>(64, std::max<long long>(1, (N + 255) / 256));
-  double* partials = ctx->ws.partials;
-  BQ_CHECK((long long)nblk * B * 2 <= (long long)kMaxBlocks * kMaxVals, BQ_EINVAL, "bq_cdot: batch too large");
-  DT_SWITCH(dtype, (cdot_kernel<T><<<dim3(nblk, B), 256, 0, st>>>(N, B, (const typename Cx<T>::V*)a,
-                                                                   (const typename Cx<T>::V*)c, partials)));
-  cdot_finish<<<1, 256, 0, st>>>(nblk, B, partials, out);
-  BQ_CUDA(cudaGetLastError());
-  return BQ_OK;
-}
-
-extern "C" int bq_caxpy(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* a, const double* coef,
-                        int32_t coef_stride, double sgn, const void* c, void* out, const int32_t* active,
-                        void* stream) {
-  BQ_CHECK(ctx && a && coef && c && out, BQ_EINVAL, "bq_caxpy: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream;
-  DT_SWITCH(dtype, (caxpy_kernel<T><<<grid_for(ctx, N * B), 256, 0, st>>>(N, B, (const typename Cx<T>::V*)a, coef,
-                                                                           coef_stride, sgn,
-                                                                           (const typename Cx<T>::V*)c,
-                                                                           (typename Cx<T>::V*)out, active)));
-  BQ_CUDA(cudaGetLastError());
-  return BQ_OK;
-}
-
-extern "C" int bq_bicg_scalars(bq_ctx* ctx, int32_t B, int32_t stage, const double* d0, const double* d1,
-                               double* state, double* coef, void* stream) {
-  BQ_CHECK(ctx && state && B >= 1 && B <= 256 && stage >= 0 && stage <= 2, BQ_EINVAL, "bq_bicg_scalars: bad arguments");
-  bicg_scalar_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(B, stage, d0, d1, state, coef);
-  BQ_CUDA(cudaGetLastError());
-  return BQ_OK;
-}
-
-extern "C" int bq_bicg_p(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const void* r, const void* v,
-                         const double* coef, void* p, const int32_t* active, void* stream) {
-  BQ_CHECK(ctx && r && v && coef && p && active, BQ_EINVAL, "bq_bicg_p: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream;
-  DT_SWITCH(dtype, (bicg_p_kernel<T><<<grid_for(ctx, N * B), 256, 0, st>>>(N, B, (const typename Cx<T>::V*)r,
-                                                                            (const typename Cx<T>::V*)v, coef,
-                                                                            (typename Cx<T>::V*)p, active)));
-  BQ_CUDA(cudaGetLastError());
-  return BQ_OK;
-}
-
-extern "C" int bq_bicg_x(bq_ctx* ctx, int32_t dtype, int64_t N, int32_t B, const double* state, const void* p,
-                         const void* s, const void* t, void* x, void* r, const int32_t* mode, void* stream) {
-  BQ_CHECK(ctx && state && p && x && mode, BQ_EINVAL, "bq_bicg_x: bad arguments");
-  cudaStream_t st = (cudaStream_t)stream;
-  DT_SWITCH(dtype, (bicg_x_kernel<T><<<grid_for(ctx, N * B), 256, 0, st>>>(
-                        N, B, state, (const typename Cx<T>::V*)p, (const typename Cx<T>::V*)s,
-                        (const typename Cx<T>::V*)t, (typename Cx<T>::V*)x, (typename Cx<T>::V*)r, mode)));
   BQ_CUDA(cudaGetLastError());
   return BQ_OK;
 }

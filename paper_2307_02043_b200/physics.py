@@ -7,10 +7,11 @@ detector one voxel past the +z face, BiCGSTAB from x0 = 0 with a relative
 residual tolerance) and implemented here on libbq:
 
 * ``bq_green_init``  : FFT of the Green kernel, once per setup
-* ``bq_ls_conv``     : pad (+ contrast multiply) -> batched cuFFT -> spectral
-                       Green multiply -> inverse cuFFT -> crop / axpy or detector
-* ``bq_cdot``, ``bq_bicg_*`` : batched BiCGSTAB (per-view scalars on the device,
-                       deterministic dots, converged views masked out)
+* ``bq_ls_conv``     : padded Green convolution as five pruned line passes
+                       (ls_fft.cu; cuFFT on the padded grid for other sizes)
+* ``bq_ls_bicgstab`` : batched BiCGSTAB run on the device (per-view scalars and
+                       stopping tests on the GPU, dots fused into the producing
+                       kernels, converged views skipped)
 * ``bq_ls_grad_accum`` : Re(conj(f' u) . w) summed over the views of the batch
 
 The views plug into the reference's ``ViewProblem`` contract
@@ -107,20 +108,6 @@ class ScatterViewSet:
         self._check(self.lib.bq_ls_conv(self.ctx, self.code, self.n, B, op, self.khat.data_ptr(), _abi.ptr(f),
                                         v.data_ptr(), float(alpha), float(beta), _abi.ptr(addend),
                                         self._padbuf(B).data_ptr(), out.data_ptr(), self._st()), "ls_conv")
-        return out
-
-    def cdot(self, a, c):
-        B = a.shape[0]
-        out = torch.empty(2 * B, dtype=torch.float64, device=self.device)
-        self._check(self.lib.bq_cdot(self.ctx, self.code, a.shape[1], B, a.data_ptr(), c.data_ptr(), out.data_ptr(),
-                                     self._st()), "cdot")
-        return out
-
-    def caxpy(self, a, coef, stride, sgn, c, out=None, active=None):
-        out = torch.empty_like(a) if out is None else out
-        self._check(self.lib.bq_caxpy(self.ctx, self.code, a.shape[1], a.shape[0], a.data_ptr(), coef.data_ptr(),
-                                      stride, float(sgn), c.data_ptr(), out.data_ptr(), _abi.ptr(active), self._st()),
-                    "caxpy")
         return out
 
     # -- batched BiCGSTAB (oracle/physics.py bicgstab) ------------------------
