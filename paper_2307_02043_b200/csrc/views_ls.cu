@@ -556,23 +556,22 @@ __global__ void bg_x_kernel(long long N, const double* __restrict__ state, const
   block_part3(dre, dim, dnn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
 }
 
-// scalar recurrences and decisions, one warp per view (fixed-order sums)
+// scalar recurrences and decisions, one 256-thread block per view (fixed-order sums)
 __global__ void bg_ctl_kernel(int stage, int nblk, const double* __restrict__ part, double* state, int* mode,
                               int* active, int* act2, int* iters, int it, double tol, int* count) {
-  const int b = blockIdx.x, lane = threadIdx.x;
+  const int b = blockIdx.x;
   const bool need = stage == BG_INIT || (stage == BG_OMEGA ? mode[b] == 2 : active[b] != 0);
+  if (!need) return;  // block-uniform
   double s0 = 0.0, s1 = 0.0, s2 = 0.0;
-  if (need)
-    for (int k = lane; k < nblk; k += 32) {
-      const double* q = part + ((long long)b * nblk + k) * 3;
-      s0 += q[0], s1 += q[1], s2 += q[2];
-    }
-  for (int o = 16; o > 0; o >>= 1) {
-    s0 += __shfl_down_sync(0xffffffffu, s0, o);
-    s1 += __shfl_down_sync(0xffffffffu, s1, o);
-    s2 += __shfl_down_sync(0xffffffffu, s2, o);
+  for (int k = threadIdx.x; k < nblk; k += blockDim.x) {
+    const double* q = part + ((long long)b * nblk + k) * 3;
+    s0 += q[0], s1 += q[1], s2 += q[2];
   }
-  if (lane != 0) return;
+  __shared__ double tot[3];
+  block_part3(s0, s1, s2, tot);
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  s0 = tot[0], s1 = tot[1], s2 = tot[2];
   double* s = state + kBS * b;
   if (stage == BG_INIT) {
     const double nb = sqrt(s2);
@@ -697,21 +696,21 @@ int bicgstab_impl(bq_ctx* ctx, int dtype, int n, int B, int adjoint, const void*
   const int op = adjoint ? 1 : 0;
   const dim3 vg(nbv, B);
   bg_init_kernel<T><<<vg, 256, 0, st>>>(N, (const V*)rhs, x, r, rh, p, v, part);
-  bg_ctl_kernel<<<B, 32, 0, st>>>(BG_INIT, nbv, part, state, mode, active, act2, iters, 0, tol, count);
+  bg_ctl_kernel<<<B, 256, 0, st>>>(BG_INIT, nbv, part, state, mode, active, act2, iters, 0, tol, count);
   BQ_CUDA(cudaGetLastError());
   int rc;
   for (int it = 1; it <= max_iter; ++it) {
     int nb = 0;
     bg_p_kernel<T><<<vg, 256, 0, st>>>(N, r, v, state, p, active);
     if ((rc = bg_conv<T>(ctx, dtype, n, B, op, khat, f, p, conv_scratch, v, active, rh, part, nbv, &nb, st))) return rc;
-    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_ALPHA, nb, part, state, mode, active, act2, iters, it, tol, count);
+    bg_ctl_kernel<<<B, 256, 0, st>>>(BG_ALPHA, nb, part, state, mode, active, act2, iters, it, tol, count);
     bg_s_kernel<T><<<vg, 256, 0, st>>>(N, r, v, state, s, active, part);
-    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_S, nbv, part, state, mode, active, act2, iters, it, tol, count);
+    bg_ctl_kernel<<<B, 256, 0, st>>>(BG_S, nbv, part, state, mode, active, act2, iters, it, tol, count);
     if ((rc = bg_conv<T>(ctx, dtype, n, B, op, khat, f, s, conv_scratch, t, act2, s, part, nbv, &nb, st))) return rc;
-    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_OMEGA, nb, part, state, mode, active, act2, iters, it, tol, count);
+    bg_ctl_kernel<<<B, 256, 0, st>>>(BG_OMEGA, nb, part, state, mode, active, act2, iters, it, tol, count);
     BQ_CUDA(cudaMemsetAsync(count, 0, sizeof(int), st));
     bg_x_kernel<T><<<vg, 256, 0, st>>>(N, state, p, s, t, rh, x, r, mode, part);
-    bg_ctl_kernel<<<B, 32, 0, st>>>(BG_END, nbv, part, state, mode, active, act2, iters, it, tol, count);
+    bg_ctl_kernel<<<B, 256, 0, st>>>(BG_END, nbv, part, state, mode, active, act2, iters, it, tol, count);
     BQ_CUDA(cudaGetLastError());
     BQ_CUDA(cudaMemcpyAsync(&ctx->host_flags[it & 1], count, sizeof(int), cudaMemcpyDeviceToHost, st));
     BQ_CUDA(cudaEventRecord(ctx->flag_ev[it & 1], st));
