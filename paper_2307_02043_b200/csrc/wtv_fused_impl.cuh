@@ -51,6 +51,7 @@
 #endif
 
 #include <algorithm>
+#include <type_traits>
 
 #include "prox_common.cuh"
 
@@ -90,6 +91,7 @@ struct FCtl {
   double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK], dmax[BQ_MAX_RANK];
   double chol[BQ_MAX_RANK * BQ_MAX_RANK];
   double K0[BQ_MAX_RANK], Cin[36], Cout[36];
+  double gram[36];  // setup U^T D^-1 U (raw partials): sum over all voxels of u s^T = sign * gsc(gram)
   unsigned long long t_last;
   unsigned long long phase_ns[8], phase_work_ns[8];
   int phase_cnt[8];
@@ -250,7 +252,10 @@ struct Fields {
 
 // Classify voxel (a, s, u) for the Newton aggregates of box (gc, gwid) and
 // accumulate; returns true for a "near" voxel (must go to the list).
-template <typename T, int R, int NACC, typename AccT>
+// Only Cin is accumulated: Cout = sum_all u s^T - Cin = sign * gram - Cin is
+// formed by the controller from the setup gram (one accumulator class fewer).
+// HINF: the upper bound is +inf (no "high" class).
+template <typename T, int R, int NACC, typename AccT, bool HINF = false>
 __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], const T (&u)[R > 0 ? R : 1], T l, T h,
                                           const T* gc, const T* gwid, AccT (&acc)[NACC]) {
   using V = FV<R>;
@@ -263,12 +268,12 @@ __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], con
   // safety margin for rounding of a + s.gamma anywhere in the box
   const T eps = (sizeof(T) == 4) ? (T)1e-5 : (T)1e-13;
   rho = rho * ((T)1 + eps) + (fabs(zc) + fabs(av)) * eps;
-  const bool inside = (zc - rho > l) && (zc + rho < h);
+  const bool inside = (zc - rho > l) && (HINF || zc + rho < h);
   const bool low = !inside && (zc + rho <= l);
-  const bool high = !inside && !low && (zc - rho >= h);
+  const bool high = HINF ? false : (!inside && !low && (zc - rho >= h));
   const bool near = !inside && !low && !high;
   // branch-free accumulation (selects, never arithmetic on an unused +-inf bound)
-  const T k0 = low ? av - l : (high ? av - h : (near ? av : (T)0));
+  const T k0 = low ? av - l : (HINF ? (near ? av : (T)0) : (high ? av - h : (near ? av : (T)0)));
   int k = 0;
 #pragma unroll
   for (int c = 0; c < R; ++c) {
@@ -276,7 +281,6 @@ __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], con
     for (int c2 = 0; c2 <= c; ++c2, ++k) {
       const AccT us = (AccT)u[c] * (AccT)s[c2];
       acc[V::CIN + k] += inside ? us : (AccT)0;
-      acc[V::COUT + k] += inside ? (AccT)0 : us;
     }
     acc[V::K0 + c] += (AccT)u[c] * (AccT)k0;
   }
@@ -427,7 +431,7 @@ struct Ctl {
     if (R > 0) chol_solve<R>(c.chol, coef);
     for (int i = 0; i < R; ++i) c.gw[i] = c.single ? 0.0 : A.reg * coef[i];
     for (int i = 0; i < R; ++i) c.K0[i] = red[V::K0 + i];
-    for (int k = 0; k < V::S; ++k) c.Cin[k] = red[V::CIN + k], c.Cout[k] = red[V::COUT + k];
+    for (int k = 0; k < V::S; ++k) c.Cin[k] = red[V::CIN + k], c.Cout[k] = A.sign * gsc(c.gram[k]) - c.Cin[k];
     c.nl_ok = red[V::OVF] == 0.0;
     c.ndist = red[V::NCNT] > A.ndist_min ? 1 : 0;
     c.fallbacks = 0;
@@ -469,6 +473,7 @@ struct Ctl {
             cap[i * R + j] = val;
             cap[j * R + i] = val;
           }
+        for (int q = 0; q < V::S; ++q) c.gram[q] = red[q];
         c.status = 0;
         if (R > 0 && !chol<R>(cap)) {
           c.status = BQ_ENOTPD;
@@ -722,6 +727,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   const int xr = KX > 0 ? lane % (KX / 4) : lane & (A.lpr - 1);
   const int yr = KX > 0 ? lane / (KX / 4) : lane >> A.lpr_log2;
   const int xb = 4 * xr;
+  const bool first_in_row = xr == 0, last_in_row = xb + 4 >= K1;
   const int W = g.W;
   const int TYe = (W - 1) * rpw;
   const bool used = warp < W;
@@ -746,6 +752,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   T* const qbuf = dyn + NS * g.stage_elems;   // [2][SRW][K1]
   T* const srcbuf = qbuf + 2 * g.slot_elems;  // [2][SRW][K1]
   const T lo_s = (T)A.lo, hi_s = (T)A.hi;
+  const bool hinf = !(MODE == 0 && A.hi_arr != nullptr) && isinf(A.hi) && A.hi > 0;  // box [lo, +inf)
 
   // ---- producer warp (warp W): issues the bulk copies, 2 stages ahead ----
   if (warp == W) {
@@ -855,7 +862,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
 
     // ---- dual update at plane k (dual_tv_solver.py:225-235) -------------
-    const T qright = __shfl_down_sync(FULLM, qc[0], 1);  // x+1 of element 3
+    // x+1 of element 3; the row's last lane uses its own element 3 (zero gradient)
+    const T qsh = __shfl_down_sync(FULLM, qc[0], 1);
+    const T qright = last_in_row ? qc[3] : qsh;
     T src[3][4];
     T vv[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -863,8 +872,10 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     if (pin && act) {
       const bool has_y = nd >= 2 && y < K2 - 1;
       const bool has_up = nd >= 3 && k < K3 - 1;
-      T qy[4] = {0, 0, 0, 0};
+      T qy[4];  // q of row y+1; at the last row q itself (zero gradient, no select)
       if (has_y) Vec4<T>::rw(qbuf + (long long)(k & 1) * g.slot_elems + rowoff + K1, qy);
+      else qy[0] = qc[0], qy[1] = qc[1], qy[2] = qc[2], qy[3] = qc[3];
+      if (!has_up) qn4[0] = qc[0], qn4[1] = qc[1], qn4[2] = qc[2], qn4[3] = qc[3];  // last plane
       T pc4[3][4], pp4[3][4];
 #pragma unroll
       for (int n = 0; n < 3; ++n) {
@@ -877,9 +888,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
       for (int v = 0; v < 4; ++v) {
         T gr[3];
         const T right = (v < 3) ? qc[v + 1] : qright;
-        gr[0] = (xb + v < K1 - 1) ? right - qc[v] : (T)0;
-        gr[1] = has_y ? qy[v] - qc[v] : (T)0;
-        gr[2] = has_up ? qn4[v] - qc[v] : (T)0;
+        gr[0] = right - qc[v];
+        gr[1] = qy[v] - qc[v];
+        gr[2] = qn4[v] - qc[v];
         T w[3], pc3[3];
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
@@ -908,6 +919,12 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
           src[n][v] = div_p ? w[n] : w[n] + m_cur * (w[n] - pc3[n]);
         }
       }
+      // boundary rows of D^T have no "-p" term: zero the components the
+      // divergence must not see (they feed nothing else), so its sums need no
+      // per-voxel selects
+      if (last_in_row) src[0][3] = 0;
+      if (!has_y) src[1][0] = src[1][1] = src[1][2] = src[1][3] = 0;
+      if (!has_up) src[2][0] = src[2][1] = src[2][2] = src[2][3] = 0;
       if (real && !warm) {
         const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
 #pragma unroll
@@ -930,7 +947,8 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
 
     // ---- a_i = v - reg D^-1 div(src) at plane k + Newton aggregates -----
-    const T left1 = __shfl_up_sync(FULLM, src[0][3], 1);
+    const T lsh = __shfl_up_sync(FULLM, src[0][3], 1);
+    const T left1 = first_in_row ? (T)0 : lsh;
     if (pin && !warm && used && !halo) {
       T av[4] = {0, 0, 0, 0};
       const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
@@ -943,10 +961,12 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
             av[v] = vv[v];
             continue;
           }
+          // boundary terms are zero in the data: src at the far faces was
+          // zeroed, up is 0 at y = 0, f3prev is 0 at the first plane
           const T lk = (v == 0) ? left1 : src[0][v - 1];
-          T dv = (xb + v < K1 - 1 ? -src[0][v] : (T)0) + (xb + v > 0 ? lk : (T)0);
-          if (nd >= 2) dv += (y < K2 - 1 ? -src[1][v] : (T)0) + (y > 0 ? up[v] : (T)0);
-          if (nd >= 3) dv += (k < K3 - 1 ? -src[2][v] : (T)0) + (k > 0 ? f3prev[v] : (T)0);
+          T dv = lk - src[0][v];
+          if (nd >= 2) dv += up[v] - src[1][v];
+          if (nd >= 3) dv += f3prev[v] - src[2][v];
           const T de = dv * iec[v];
           av[v] = vv[v] - reg * de;
 #pragma unroll
@@ -963,19 +983,24 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
       }
       bool nrv[4] = {false, false, false, false};
       bool any = false;
+      auto classify = [&](auto hinf_tag) {
+        constexpr bool HI = decltype(hinf_tag)::value;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        if (real && R > 0) {
-          T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
+        for (int v = 0; v < 4; ++v) {
+          if (real && R > 0) {
+            T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
 #pragma unroll
-          for (int c = 0; c < R; ++c) {
-            uv[c] = uc[c][v];
-            sv[c] = sg * uv[c] * iec[v];
+            for (int c = 0; c < R; ++c) {
+              uv[c] = uc[c][v];
+              sv[c] = sg * uv[c] * iec[v];
+            }
+            nrv[v] = aggregate<T, R, NACC, T, HI>(av[v], sv, uv, l[v], h[v], sh.gc, sh.gwid, fa);
+            any |= nrv[v];
           }
-          nrv[v] = aggregate<T, R, NACC, T>(av[v], sv, uv, l[v], h[v], sh.gc, sh.gwid, fa);
-          any |= nrv[v];
         }
-      }
+      };
+      if (hinf) classify(std::true_type{});
+      else classify(std::false_type{});
       if (__any_sync(FULLM, any)) {  // near voxels are rare: one vote per step
 #pragma unroll
         for (int v = 0; v < 4; ++v) {
