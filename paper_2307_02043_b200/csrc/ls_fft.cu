@@ -279,61 +279,110 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V
 // ZC: z pass over columns (y < m, x < m), in place in Q:
 //   forward z-DFT of planes [z0, z0+nzi), * K_hat (conj if adj),
 //   inverse z-DFT, keep planes [zo0, zo0+nzo) -> Q slots 0..nzo-1.
+// One block owns one (y, x-chunk) column group and walks the B views of the
+// batch: the twiddles and the block's K_hat columns (folded z index, n+1
+// values per line) are staged into shared memory once (cp.async, overlapping
+// the first view's loads and forward DFT) and reused by every view, and the
+// next active view's column is prefetched into L2 while this one computes.
 // ---------------------------------------------------------------------------
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
+template <int R1, int R2, int L>
+constexpr int zc_smem_elems(int n) {
+  return R1 * R2 + R1 * R2 * L + (n + 1) * L;
+}
+
 template <typename T, int R1, int R2, int C, int L>
-__global__ void __launch_bounds__(C* L) zc_kernel(int n, int z0, int nzi, int zo0, int nzo, int adj,
+__global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi, int zo0, int nzo, int adj,
                                                   const typename CV<T>::V* __restrict__ khat,
                                                   typename CV<T>::V* __restrict__ q, const int* __restrict__ active) {
-  if (active && !active[blockIdx.x]) return;
   using V = typename CV<T>::V;
-  constexpr int M = R1 * R2, XT = M / L;
+  constexpr int M = R1 * R2, XT = M / L, NT = C * L;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* tw = (V*)smraw;
   V* sm = tw + M;
+  V* ks = sm + M * L;  // [fz <= n][l]: K_hat of this block's columns, folded z
   const int tid = threadIdx.x, l = tid % L, t = tid / L;
-  const int b = blockIdx.x, y = blockIdx.y / XT, x = (blockIdx.y % XT) * L + l;
-  load_twiddles<V, M>(tw, tid, C * L);
-  V* col = q + (long long)b * n * M * M + (long long)y * M + x;
+  const int y = blockIdx.x / XT, xc = blockIdx.x % XT, x = xc * L + l;
   const long long zs = (long long)M * M;
-  V a[R1 / C][R2];
-#pragma unroll
-  for (int s = 0; s < R1 / C; ++s)
-#pragma unroll
-    for (int n2 = 0; n2 < R2; ++n2) {
-      const int e = t + C * s + R1 * n2;
-      a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
+  const long long vstride = (long long)n * zs;  // one view's Q
+  const int fy = y <= n ? y : M - y;
+  {
+    const V* kb = khat + (long long)fy * M;
+    const int nk = (n + 1) * L;
+    for (int i = tid; i < nk; i += NT) {
+      const int fz = i / L, xx = xc * L + i % L;
+      const int fx = xx <= n ? xx : M - xx;
+      if (sizeof(V) == 8) cp_async8(&ks[i], kb + fz * zs + fx);
+      else cp_async16(&ks[i], kb + fz * zs + fx);
     }
-  __syncthreads();
-  step1<R1, R2, C, L, true, -1>(a, sm, tw, l, t);
-  __syncthreads();
-  V c[R2 / C][R1];
-  step3<R1, R2, C, L, true, -1>(c, sm, l, t);
-  // spectral multiply: c[s][k1] = X[kz], kz = k2 + R2 k1, k2 = t + C s
-  const int fy = y <= n ? y : M - y, fx = x <= n ? x : M - x;
-  const V* kcol = khat + (long long)fy * M + fx;
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  }
+  load_twiddles<V, M>(tw, tid, NT);
+  auto next_active = [&](int b) {
+    while (b < B && active && !active[b]) ++b;
+    return b;
+  };
+  bool first = true;
+  for (int b = next_active(0); b < B; b = next_active(b + 1)) {
+    V* col = q + (long long)b * vstride + (long long)y * M + x;
+    V a[R1 / C][R2];
 #pragma unroll
-  for (int s = 0; s < R2 / C; ++s)
+    for (int s = 0; s < R1 / C; ++s)
 #pragma unroll
-    for (int k1 = 0; k1 < R1; ++k1) {
-      const int kz = t + C * s + R2 * k1;
-      const int fz = kz <= n ? kz : M - kz;
-      V k = kcol[(long long)fz * zs];
-      if (adj) k.y = -k.y;
-      c[s][k1] = cmul(c[s][k1], k);
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const int e = t + C * s + R1 * n2;
+        a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
+      }
+    {  // the next active view's column into L2 while this one computes
+      const int bn = next_active(b + 1);
+      if (bn < B) {
+        const V* nc = q + (long long)bn * vstride + (long long)y * M + x;
+        for (int e = t; e < nzi; e += C) prefetch_l2(nc + e * zs);
+      }
     }
-  __syncthreads();  // step-3 reads of sm are done before it is rewritten
-  // inverse with (R1', R2') = (R2, R1): c[s][n2'] = x'[n1' + R2 n2'], n1' = t + C s
-  step1<R2, R1, C, L, true, 1>(c, sm, tw, l, t);
-  __syncthreads();
-  V o[R1 / C][R2];
-  step3<R2, R1, C, L, true, 1>(o, sm, l, t);
+    if (first) cp_async_wait_all();
+    __syncthreads();  // twiddles + K_hat staged (first view); previous view's reads of sm done
+    step1<R1, R2, C, L, true, -1>(a, sm, tw, l, t);
+    __syncthreads();
+    V c[R2 / C][R1];
+    step3<R1, R2, C, L, true, -1>(c, sm, l, t);
+    // spectral multiply: c[s][k1] = X[kz], kz = k2 + R2 k1, k2 = t + C s
 #pragma unroll
-  for (int s = 0; s < R1 / C; ++s)
+    for (int s = 0; s < R2 / C; ++s)
 #pragma unroll
-    for (int k1 = 0; k1 < R2; ++k1) {
-      const int z = t + C * s + R1 * k1;
-      if (z >= zo0 && z < zo0 + nzo) col[(z - zo0) * zs] = o[s][k1];
-    }
+      for (int k1 = 0; k1 < R1; ++k1) {
+        const int kz = t + C * s + R2 * k1;
+        const int fz = kz <= n ? kz : M - kz;
+        V k = ks[fz * L + l];
+        if (adj) k.y = -k.y;
+        c[s][k1] = cmul(c[s][k1], k);
+      }
+    __syncthreads();  // step-3 reads of sm are done before it is rewritten
+    // inverse with (R1', R2') = (R2, R1): c[s][n2'] = x'[n1' + R2 n2'], n1' = t + C s
+    step1<R2, R1, C, L, true, 1>(c, sm, tw, l, t);
+    __syncthreads();
+    V o[R1 / C][R2];
+    step3<R2, R1, C, L, true, 1>(o, sm, l, t);
+#pragma unroll
+    for (int s = 0; s < R1 / C; ++s)
+#pragma unroll
+      for (int k1 = 0; k1 < R2; ++k1) {
+        const int z = t + C * s + R1 * k1;
+        if (z >= zo0 && z < zo0 + nzo) col[(z - zo0) * zs] = o[s][k1];
+      }
+    first = false;
+  }
+  if (first) cp_async_wait_all();  // no active view: retire the staging copies
 }
 
 // ---------------------------------------------------------------------------
@@ -492,6 +541,7 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   constexpr int NT = C * L;
   const size_t sm_row = sizeof(V) * (M + smem_elems<R1, R2, L, false>());
   const size_t sm_col = sizeof(V) * (M + smem_elems<R1, R2, L, true>());
+  const size_t sm_zc = sizeof(V) * zc_smem_elems<R1, R2, L>(n);
   const long long N = (long long)n * n * n;
   V* q = (V*)scratch;                 // B x n x m x m
   V* hx = q + (long long)B * 4 * N;   // B x n x n x m
@@ -500,15 +550,15 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   const bool adj = op == 1 || op == 3;
   int rc;
   if ((rc = prep(xf_kernel<T, R1, R2, C, L>, sm_row)) || (rc = prep(yf_kernel<T, R1, R2, C, L>, sm_col)) ||
-      (rc = prep(zc_kernel<T, R1, R2, C, L>, sm_col)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
+      (rc = prep(zc_kernel<T, R1, R2, C, L>, sm_zc)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
       (rc = prep(xi_kernel<T, R1, R2, C, L>, sm_row)))
     return rc;
   const int rows_in = nzi * n, rows_out = nzo * n;
   xf_kernel<T, R1, R2, C, L><<<dim3(B, (rows_in + L - 1) / L), NT, sm_row, st>>>(
       n, rows_in, (op == 0 || op == 2) ? (const T*)f : nullptr, (const V*)v, hx, active);
   yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q, active);
-  zc_kernel<T, R1, R2, C, L><<<dim3(B, M * (M / L)), NT, sm_col, st>>>(n, z0, nzi, zo0, nzo, adj ? 1 : 0,
-                                                                       (const V*)khat, q, active);
+  zc_kernel<T, R1, R2, C, L><<<dim3(M * (M / L)), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
+                                                                  (const V*)khat, q, active);
   yi_kernel<T, R1, R2, C, L><<<dim3(B, nzo * (M / L)), NT, sm_col, st>>>(n, q, hx, active);
   if (nblk) *nblk = (rows_out + L - 1) / L;
   const bool crop = op != 2;
