@@ -188,6 +188,17 @@ __device__ __forceinline__ V czero() {
   return v;
 }
 
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+
 // ---------------------------------------------------------------------------
 // XF: forward x pass over rows (row = z*n + y, rows = nz_in*n) of the compact
 // input (f .* v, or the detector residual plane), zero-padded to m.
@@ -285,16 +296,9 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V
 // the first view's loads and forward DFT) and reused by every view, and the
 // next active view's column is prefetched into L2 while this one computes.
 // ---------------------------------------------------------------------------
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
-}
-__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];" ::"l"(p)); }
+#ifndef LS_ZC_PF
+#define LS_ZC_PF 512  // ZC: prefetch the next view's column into L2 for m >= LS_ZC_PF (helps at 512, not 256)
+#endif
 
 template <int R1, int R2, int L>
 constexpr int zc_smem_elems(int n) {
@@ -345,7 +349,7 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
       }
     {  // the next active view's column into L2 while this one computes
       const int bn = next_active(b + 1);
-      if (bn < B) {
+      if (M >= LS_ZC_PF && bn < B) {
         const V* nc = q + (long long)bn * vstride + (long long)y * M + x;
         for (int e = t; e < nzi; e += C) prefetch_l2(nc + e * zs);
       }
@@ -449,6 +453,15 @@ __global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typenam
   for (int s = 0; s < R1 / C; ++s)
 #pragma unroll
     for (int n2 = 0; n2 < R2; ++n2) a[s][n2] = ok ? src[t + C * s + R1 * n2] : czero<V>();
+  if (ok) {  // the epilogue's inputs into L2 while the transform runs
+    constexpr int LINE = 128 / sizeof(V);
+    const long long ob = ((long long)b * rows + row) * n;
+    for (int e = t * LINE; e < n; e += C * LINE) {
+      if (v && alpha != 0.0) prefetch_l2(v + ob + e);
+      if (addend) prefetch_l2(addend + ob + e);
+      if (dotp) prefetch_l2(da + ob + e);
+    }
+  }
   __syncthreads();
   step1<R1, R2, C, L, false, 1>(a, sm, tw, l, t);
   __syncthreads();
