@@ -17,11 +17,11 @@ using fused::al16;
 using fused::fused_launch;
 
 // Fast-path eligibility: 16-byte-aligned fields, K1 in {4, 8, ..., 128}
-// dividing 128, ring/ping-pong scratch supplied.
+// dividing 128 or K1 == 256 (two warps per x-row), ring/ping-pong scratch supplied.
 bool fused_eligible(const bq_wtv_desc& D) {
   const long long K1 = D.dims[0];
   if (D.ndim != 3) return false;
-  if (!(K1 >= 4 && K1 <= 128 && K1 % 4 == 0 && 128 % K1 == 0)) return false;
+  if (!((K1 >= 4 && K1 <= 128 && K1 % 4 == 0 && 128 % K1 == 0) || K1 == 256)) return false;
   if (!D.p2 || !D.a2 || !D.pb || !D.p) return false;
   const void* ptrs[] = {D.p, D.pb, D.p2, D.a, D.a2, D.v, D.x, D.d, D.U, D.lo_arr, D.hi_arr};
   for (const void* q : ptrs)

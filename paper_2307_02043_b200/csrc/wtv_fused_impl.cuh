@@ -109,6 +109,7 @@ template <typename T>
 struct FArgs {
   int ndim, mode, sign, accelerated, max_iter, newton_max_iter, wpm_only, vec;
   int K1, K2, K3, lpr, rpw, nty, lpr_log2;
+  int wpr;  // warps per x-row: 1 (K1 <= 128, rpw rows per warp) or 2 (K1 == 256, a half row each)
   long long N, plane, tile_planes;
   double tau, reg, step, eps, newton_eps, lo, hi;
   const T* lo_arr;
@@ -658,7 +659,8 @@ __device__ __forceinline__ void issue_step(const FArgs<T>& A, const StepIter& it
                                            const T* Pp, const T* Ain, int lane) {
   const int K1 = A.K1, K2 = A.K2, rpw = A.rpw;
   const long long N = A.N, plane = A.plane;
-  const int TYe = (g.W - 1) * rpw;
+  const int GW = g.W / A.wpr;  // row groups (the first is the halo group)
+  const int TYe = (GW - 1) * rpw;
   const int y0 = (int)it.tile * TYe;
   const int y_base = y0 - rpw;
   // enumerate copies: index -> (slot, base, plane, row range)
@@ -683,8 +685,8 @@ __device__ __forceinline__ void issue_step(const FArgs<T>& A, const StepIter& it
     const long long zk = it.k;
     pick(M.V, A.v, zk, y0, y0 + TYe);
     for (int n = 0; n < A.ndim; ++n) {
-      pick(M.PC0 + n, Pc + n * N, zk, y_base, y_base + g.W * rpw);
-      if (M.PP0 >= 0) pick(M.PP0 + n, Pp + n * N, zk, y_base, y_base + g.W * rpw);
+      pick(M.PC0 + n, Pc + n * N, zk, y_base, y_base + GW * rpw);
+      if (M.PP0 >= 0) pick(M.PP0 + n, Pp + n * N, zk, y_base, y_base + GW * rpw);
     }
   }
   unsigned bytes = 0;
@@ -723,16 +725,24 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   const long long N = A.N;
   constexpr int nd = 3;  // the fused path serves 3-D grids (others use wtv_prox.cu)
   const int K1 = KX > 0 ? KX : A.K1, K2 = A.K2, K3 = A.K3;
-  const int rpw = KX > 0 ? 128 / KX : A.rpw;
-  const int xr = KX > 0 ? lane % (KX / 4) : lane & (A.lpr - 1);
-  const int yr = KX > 0 ? lane / (KX / 4) : lane >> A.lpr_log2;
-  const int xb = 4 * xr;
-  const bool first_in_row = xr == 0, last_in_row = xb + 4 >= K1;
+  // x-split (K1 == 256): warps 2g and 2g+1 hold the left / right half of row group g
+  const int wpr = KX > 0 ? (KX > 128 ? 2 : 1) : A.wpr;
+  const int rpw = KX > 0 ? (KX >= 128 ? 1 : 128 / KX) : A.rpw;
+  const int xr = KX > 0 ? (KX >= 128 ? lane : lane % (KX / 4)) : lane & (A.lpr - 1);
+  const int yr = KX > 0 ? (KX >= 128 ? 0 : lane / (KX / 4)) : lane >> A.lpr_log2;
+  const int xh = wpr == 2 ? (warp & 1) : 0;
+  const int wg = wpr == 2 ? (warp >> 1) : warp;
+  const int xb = 4 * xr + 128 * xh;
+  const bool first_in_row = xr == 0 && xh == 0, last_in_row = xb + 4 >= K1;
+  const bool edge_src = wpr == 2 && xh == 0 && lane == 31;  // publishes its x+1 / x-1 halves' values
+  const bool edge_dst = wpr == 2 && xh == 1 && lane == 0;
   const int W = g.W;
-  const int TYe = (W - 1) * rpw;
+  const int GW = W / wpr;
+  const int TYe = (GW - 1) * rpw;
   const bool used = warp < W;
-  const bool halo = warp == 0;
-  const int sr = warp * rpw + yr;  // staged row of this thread
+  const bool halo = wg == 0;
+  const int sr = wg * rpw + yr;  // staged row of this thread
+  __shared__ T s_edge[2][32];    // x-split: div source x = 127 of each staged row, by step parity
   const T* __restrict__ Pc = A.ring[sh.slot_cur];
   const T* __restrict__ Pp = A.ring[sh.slot_prev];
   T* __restrict__ Pn = A.ring[sh.slot_new];
@@ -854,7 +864,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         Vec4<T>::st(qdst + rowoff, qn4);
       }
       if (halo && yr == 0 && y0 + TYe < K2) {
-        const long long off = (long long)(W * rpw) * K1 + xb;
+        const long long off = (long long)(GW * rpw) * K1 + xb;
         T qb[4], ib[4], ub[R > 0 ? R : 1][4];
         qrow(off, qb, ib, ub);
         Vec4<T>::st(qdst + off, qb);
@@ -864,7 +874,8 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     // ---- dual update at plane k (dual_tv_solver.py:225-235) -------------
     // x+1 of element 3; the row's last lane uses its own element 3 (zero gradient)
     const T qsh = __shfl_down_sync(FULLM, qc[0], 1);
-    const T qright = last_in_row ? qc[3] : qsh;
+    // x-split: q(x = 128) of this row comes from the q row published in the last step
+    const T qright = last_in_row ? qc[3] : (edge_src ? qbuf[(long long)(k & 1) * g.slot_elems + rowoff + 4] : qsh);
     T src[3][4];
     T vv[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -923,6 +934,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
       // divergence must not see (they feed nothing else), so its sums need no
       // per-voxel selects
       if (last_in_row) src[0][3] = 0;
+      if (edge_src) s_edge[k & 1][sr] = src[0][3];
       if (!has_y) src[1][0] = src[1][1] = src[1][2] = src[1][3] = 0;
       if (!has_up) src[2][0] = src[2][1] = src[2][2] = src[2][3] = 0;
       if (real && !warm) {
@@ -948,7 +960,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
 
     // ---- a_i = v - reg D^-1 div(src) at plane k + Newton aggregates -----
     const T lsh = __shfl_up_sync(FULLM, src[0][3], 1);
-    const T left1 = first_in_row ? (T)0 : lsh;
+    const T left1 = first_in_row ? (T)0 : (edge_dst ? s_edge[k & 1][sr] : lsh);
     if (pin && !warm && used && !halo) {
       T av[4] = {0, 0, 0, 0};
       const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
@@ -1109,16 +1121,21 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   const long long gtid = (long long)blockIdx.x * NT + threadIdx.x;
   const long long seg_begin = (long long)blockIdx.x * A.tile_planes / gridDim.x;
   const long long seg_end = (long long)(blockIdx.x + 1) * A.tile_planes / gridDim.x;
-  const long long tp_s = (long long)((A.K2 + (A.geo.W - 1) * A.rpw - 1) / ((A.geo.W - 1) * A.rpw)) * A.K3;
+  const int GWs = A.geo.W / A.wpr;
+  const long long tp_s = (long long)((A.K2 + (GWs - 1) * A.rpw - 1) / ((GWs - 1) * A.rpw)) * A.K3;
   const long long seg_begin_s = (long long)blockIdx.x * tp_s / gridDim.x;
   const long long seg_end_s = (long long)(blockIdx.x + 1) * tp_s / gridDim.x;
   const Fields<T, R> F{A.d, A.U, A.lo_arr, A.hi_arr, N, (T)A.tau, (T)A.lo, (T)A.hi, (T)A.sign};
-  const int lpr = A.lpr, rpw = A.rpw;
-  const int xr = lane % lpr, yr = lane / lpr, xb = 4 * xr;
-  const bool halo = warp == RW;
-  const int slot = halo ? yr : rpw + warp * rpw + yr;
-  const int TYe = RW * rpw;
-  const int rows_used = (RW + 1) * rpw;
+  const int lpr = A.lpr, rpw = A.rpw, wpr = A.wpr;
+  // standalone DIV pass: NG row groups of wpr warps, the last group is the halo
+  const int NG = (RW + 1) / wpr;
+  const int xh = wpr == 2 ? (warp & 1) : 0, wg = warp / wpr;
+  const int xr = lane % lpr, yr = lane / lpr, xb = 4 * xr + 128 * xh;
+  const bool halo = wg >= NG - 1;
+  const int slot = halo ? yr : rpw + wg * rpw + yr;
+  const int TYe = (NG - 1) * rpw;
+  const int rows_used = NG * rpw;
+  __shared__ T s_dedge[2][64];
   (void)ROWS;
   constexpr int NW = NT / 32;
   constexpr int EWN = 3 + 2 * (R > 0 ? R : 1);
@@ -1214,7 +1231,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         const int z1 = (int)min((long long)K3, z0 + (seg_end - pos));
         pos += z1 - z0;
         const int y0 = (int)tile * TYe;
-        const int y = halo ? (y0 - rpw + yr) : (y0 + warp * rpw + yr);
+        const int y = halo ? (y0 - rpw + yr) : (y0 + wg * rpw + yr);
         const bool act = y >= 0 && y < K2;
         const bool has_y = nd >= 2 && y < K2 - 1;
         const int zs = (z0 > 0 && nd >= 3) ? z0 - 1 : z0;
@@ -1313,8 +1330,10 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
 #pragma unroll
             for (int k = 0; k < 4; ++k) rows[((long long)buf * rows_used + slot) * K1 + xb + k] = src[1][k];
           }
+          if (wpr == 2 && xh == 0 && lane == 31) s_dedge[buf][slot] = src[0][3];
           __syncthreads();
-          const T left1 = __shfl_up_sync(FULLM, src[0][3], 1);
+          const T lsh = __shfl_up_sync(FULLM, src[0][3], 1);
+          const T left1 = (wpr == 2 && xh == 1 && lane == 0) ? s_dedge[buf][slot] : lsh;
           if (!halo && !warm && act) {
             // ---- a_i = v - reg D^-1 div(src)  (tv_ops.py:122-159) -------
             T av[4], vv[4];
@@ -1824,8 +1843,9 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.partials = ctx->ws.partials;
   A.red = (double*)ctx->ws.ctl;
   A.bar = ctx->ws.barrier;
-  A.lpr = A.K1 / 4;
+  A.lpr = std::min(A.K1 / 4, 32);
   A.rpw = 32 / A.lpr;
+  A.wpr = A.K1 > 128 ? A.K1 / 128 : 1;
   A.lpr_log2 = 0;
   while ((1 << A.lpr_log2) < A.lpr) ++A.lpr_log2;
   if (D.d) {
@@ -1839,7 +1859,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
     }
     A.ie = (T*)ctx->aux_buf;
   }
-  const int TYe = RW * A.rpw;
+  const int TYe = ((RW + 1) / A.wpr - 1) * A.rpw;  // standalone DIV pass tile
   A.nty = (A.K2 + TYe - 1) / TYe;
   A.tile_planes = (long long)A.nty * A.K3;
 
@@ -1849,22 +1869,24 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   M.make(D.d != nullptr, D.lo_arr != nullptr, D.hi_arr != nullptr, D.ndim, true);
   const size_t smem_cap = 200 * 1024;
   int W = NT / 32 - 1;  // + 1 producer warp
+  W -= W % A.wpr;       // whole row groups
   const char* ns_env = getenv("BQ_PROX_STAGES");
   const int nst = ns_env ? std::max(2, std::min(NSTAGE, atoi(ns_env))) : 2;
   auto staged_bytes = [&](int w) {
-    const long long srw = (long long)w * A.rpw + 1;
+    const long long srw = (long long)(w / A.wpr) * A.rpw + 1;
     return (size_t)(nst * M.nfield + 4) * srw * A.K1 * sizeof(T);
   };
   const char* w_env = getenv("BQ_PROX_WARPS");
   if (w_env) W = std::max(2, std::min(W, atoi(w_env)));
-  while (W > 2 && staged_bytes(W) > smem_cap) --W;
+  W -= W % A.wpr;
+  while (W > 2 * A.wpr && staged_bytes(W) > smem_cap) W -= A.wpr;
   BQ_CHECK(staged_bytes(W) <= smem_cap, BQ_EINVAL, "wtv_fused: stage does not fit in shared memory");
   A.geo.W = W;
   A.geo.nstage = nst;
-  A.geo.SRW = W * A.rpw + 1;
+  A.geo.SRW = (W / A.wpr) * A.rpw + 1;
   A.geo.slot_elems = (long long)A.geo.SRW * A.K1;
   A.geo.stage_elems = (long long)M.nfield * A.geo.slot_elems;
-  const size_t base_dyn = std::max<size_t>(2ull * (RW + 1) * A.rpw * A.K1 * sizeof(T), staged_bytes(W));
+  const size_t base_dyn = std::max<size_t>(2ull * ((RW + 1) / A.wpr) * A.rpw * A.K1 * sizeof(T), staged_bytes(W));
   // near-list region after the stages (so the next pass's prefetched stages survive the on-chip Newton)
   int optin = 0, static_b = 0;
   BQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
@@ -1884,7 +1906,8 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   long long G = std::min<long long>(ctx->num_sms, A.tile_planes);
   G = std::max<long long>(1, std::min<long long>(G, (A.N + 2047) / 2048));
   {
-    const long long tp_s = (long long)((A.K2 + (W - 1) * A.rpw - 1) / ((W - 1) * A.rpw)) * A.K3;
+    const int GW = W / A.wpr;
+    const long long tp_s = (long long)((A.K2 + (GW - 1) * A.rpw - 1) / ((GW - 1) * A.rpw)) * A.K3;
     G = std::min<long long>(G, tp_s);
   }
   G = std::min<long long>(G, kMaxBlocks / 2);  // partials are double-buffered

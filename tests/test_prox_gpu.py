@@ -91,7 +91,9 @@ def _diag_problem(seed, dims, r=1, reg=0.05, iso=True, lo=0.0, hi=np.inf):
 
 
 @pytest.mark.parametrize("dims,r,iso", [((16, 16, 16), 1, True), ((32, 24, 20), 2, True), ((40, 33), 3, False),
-                                        ((20, 18, 16), 4, True)])
+                                        ((20, 18, 16), 4, True),
+                                        # K1 = 256: the fused kernel's x-split rows (two warps per row)
+                                        ((256, 12, 10), 1, True), ((256, 7, 9), 2, False), ((256, 21, 5), 4, True)])
 def test_diag_prox_f64_vs_oracle(dims, r, iso):
     d, u, v = _diag_problem(7, dims, r)
     prob = D.DualTvProblem(grid=bq.Grid(dims), v=v, w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05,
@@ -101,6 +103,19 @@ def test_diag_prox_f64_vs_oracle(dims, r, iso):
     assert rel_l2(rep.x, ref["x"]) <= F64_TOL
     assert rel_l2(rep.p_star, ref["p_star"]) <= F64_TOL
     assert rep.newton_iterations == ref["newton_iterations"]
+
+
+def test_xsplit_rows_f32_vs_oracle():
+    """K1 = 256 (x-split rows) in fp32 at a size with several row tiles and z segments."""
+    d, u, v = _diag_problem(11, (256, 40, 24), 1)
+    ref = O.fgp_prox((256, 40, 24), v, O.Metric(U=u, d=d), reg=0.05, eps=1e-300, max_iter=40)
+    w = W.DiagPlusLowRank(1.0, torch.tensor(u, dtype=torch.float32, device="cuda"),
+                          d=torch.tensor(d, dtype=torch.float32, device="cuda"))
+    prob = D.DualTvProblem(grid=bq.Grid((256, 40, 24)), v=torch.tensor(v, dtype=torch.float32, device="cuda"), w=w,
+                           reg=0.05)
+    rep = D.solve(prob, eps=1e-300, max_iter=40)
+    assert rel_l2(rep.x.double().cpu().numpy(), ref["x"]) <= F32_TOL
+    assert rel_l2(rep.p_star.double().cpu().numpy(), ref["p_star"]) <= F32_TOL
 
 
 def test_config2_shape_f32_vs_f64_and_oracle_64():
