@@ -61,7 +61,7 @@ using namespace prox;
 
 enum : int { F_SETUP = 0, F_DIV = 1, F_NEWTON = 2, F_FUSED = 3, F_FINAL = 4, F_DONE = 5, F_NLOCAL = 6, F_NDIST = 7 };
 
-constexpr int CAPW = 64;   // near-list capacity per warp per pass
+constexpr int CAPW = 64;   // minimum near-list capacity per warp per pass (FArgs::capw scales it with the grid)
 constexpr unsigned FULLM = 0xffffffffu;
 
 template <int R>
@@ -125,7 +125,8 @@ struct FArgs {
   double* partials;
   double* red;
   unsigned* bar;
-  void* near_data;  // [2][G * NW * CAPW * EW] entries (T), NW = warps per block; by pass parity
+  void* near_data;  // [2][G * NW * capw * EW] entries (T), NW = warps per block; by pass parity
+  int capw;         // near-list capacity per warp per pass (>= CAPW, ~1/20 of a warp's voxels per pass)
   T* ie;            // 1/d per voxel (written by the setup pass; staged instead of d)
   int* near_cnt;  // [2][G * NW]  (pass parity: a fast block's next pass never
                   //  overwrites lists a slow block is still gathering)
@@ -293,14 +294,15 @@ __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], con
 // never has to chase indices.
 template <typename T, int R>
 __device__ __forceinline__ void near_push(bool flag, T av, T l, T h, const T (&u)[R > 0 ? R : 1],
-                                          const T (&s)[R > 0 ? R : 1], int lane, T* seg, int& cnt, bool& ovf) {
+                                          const T (&s)[R > 0 ? R : 1], int lane, T* seg, int& cnt, bool& ovf,
+                                          int cap) {
   constexpr int EW = 3 + 2 * (R > 0 ? R : 1);
   const unsigned m = __ballot_sync(FULLM, flag);
   if (m == 0) return;
   const int n = __popc(m);
-  if (cnt + n > CAPW) {
+  if (cnt + n > cap) {
     ovf = true;
-    cnt = CAPW;
+    cnt = cap;
     return;
   }
   if (flag) {
@@ -1022,7 +1024,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
             uv[c] = (R > 0) ? uc[c][v] : (T)0;
             sv[c] = sg * uv[c] * iec[v];
           }
-          near_push<T, R>(nrv[v], av[v], l[v], h[v], uv, sv, lane, near_seg, ncnt, ovf);
+          near_push<T, R>(nrv[v], av[v], l[v], h[v], uv, sv, lane, near_seg, ncnt, ovf, A.capw);
         }
       }
     }
@@ -1139,8 +1141,9 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   (void)ROWS;
   constexpr int NW = NT / 32;
   constexpr int EWN = 3 + 2 * (R > 0 ? R : 1);
-  const long long seg_elems = (long long)gridDim.x * NW * CAPW * EWN;  // one parity's list area
-  T* my_seg0 = reinterpret_cast<T*>(A.near_data) + ((long long)blockIdx.x * NW + warp) * CAPW * EWN;
+  const int capw = A.capw;
+  const long long seg_elems = (long long)gridDim.x * NW * capw * EWN;  // one parity's list area
+  T* my_seg0 = reinterpret_cast<T*>(A.near_data) + ((long long)blockIdx.x * NW + warp) * capw * EWN;
   int npass = 0;  // DIV/FUSED passes so far (same in every block)
   int my_cnt = 0;  // this warp's near entries in the last pass
 
@@ -1369,7 +1372,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
                 s[c] = F.sg * u[c] * iec[k];
               }
               const bool nr = (R > 0) ? aggregate<T, R, NACC, double>(av[k], s, u, l[k], h[k], sh.gc, sh.gwid, acc) : false;
-              near_push<T, R>(nr, av[k], l[k], h[k], u, s, lane, my_seg, ncnt, ovf);
+              near_push<T, R>(nr, av[k], l[k], h[k], u, s, lane, my_seg, ncnt, ovf, A.capw);
             }
           } else if (!halo) {
             // keep the warp's ballots aligned with the active lanes' calls
@@ -1377,7 +1380,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
 #pragma unroll
             for (int c = 0; c < (R > 0 ? R : 1); ++c) z1[c] = 0;
 #pragma unroll
-            for (int k = 0; k < 4; ++k) near_push<T, R>(false, (T)0, (T)0, (T)0, z1, z1, lane, my_seg, ncnt, ovf);
+            for (int k = 0; k < 4; ++k) near_push<T, R>(false, (T)0, (T)0, (T)0, z1, z1, lane, my_seg, ncnt, ovf, A.capw);
           }
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
@@ -1619,7 +1622,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
           if (s_pref[mid] <= e) lo = mid;
           else hi = mid;
         }
-        return nd + ((long long)lo * CAPW + (e - s_pref[lo])) * EW;
+        return nd + ((long long)lo * capw + (e - s_pref[lo])) * EW;
       };
       if (total > 0 && indexed) {
         constexpr int SPT = 8;
@@ -1710,7 +1713,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
               for (int sidx = t0; sidx < nseg; sidx += tstride) {
                 const int cnt = __ldcg(&ncnt_l[sidx]);
                 for (int e = 0; e < cnt; ++e) {
-                  const T* d = nd + ((long long)sidx * CAPW + e) * EW;
+                  const T* d = nd + ((long long)sidx * capw + e) * EW;
                   T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
 #pragma unroll
                   for (int c = 0; c < R; ++c) uv[c] = __ldcg(&d[3 + c]), sv[c] = __ldcg(&d[3 + R + c]);
@@ -1913,7 +1916,14 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   G = std::min<long long>(G, kMaxBlocks / 2);  // partials are double-buffered
   // near-list workspace
   constexpr int EWN = 3 + 2 * (R > 0 ? R : 1);
-  const size_t data_bytes = 2 * (size_t)G * (NT / 32) * CAPW * EWN * sizeof(T);
+  {
+    // near-list capacity: ~1/20 of the voxels a warp sees per pass (64 at 128^3, 512 at 256^3)
+    const long long per_warp = A.N / (G * (NT / 32));
+    int cap = CAPW;
+    while (cap < 1024 && cap < per_warp / 20) cap *= 2;
+    A.capw = cap;
+  }
+  const size_t data_bytes = 2 * (size_t)G * (NT / 32) * A.capw * EWN * sizeof(T);
   const size_t need = data_bytes + 2 * (size_t)G * (NT / 32) * sizeof(int);
   if (ctx->near_bytes < need) {
     cudaFree(ctx->near_buf);
