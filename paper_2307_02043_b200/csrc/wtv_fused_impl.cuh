@@ -728,7 +728,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   constexpr int nd = 3;  // the fused path serves 3-D grids (others use wtv_prox.cu)
   const int K1 = KX > 0 ? KX : A.K1, K2 = A.K2, K3 = A.K3;
   // x-split (K1 == 256): warps 2g and 2g+1 hold the left / right half of row group g
-  const int wpr = KX > 0 ? (KX > 128 ? 2 : 1) : A.wpr;
+  constexpr int wpr = KX > 128 ? 2 : 1;  // the x-split has its own instantiation (KX == 256)
   const int rpw = KX > 0 ? (KX >= 128 ? 1 : 128 / KX) : A.rpw;
   const int xr = KX > 0 ? (KX >= 128 ? lane : lane % (KX / 4)) : lane & (A.lpr - 1);
   const int yr = KX > 0 ? (KX >= 128 ? 0 : lane / (KX / 4)) : lane >> A.lpr_log2;
@@ -1028,8 +1028,12 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         }
       }
     }
+    // only the classes the step accumulates (Cout, OVF and NCNT stay constant
+    // here, so the compiler keeps no registers or adds for them)
 #pragma unroll
-    for (int q = 0; q < NACC; ++q) acc[q] += (double)fa[q];
+    for (int q = 0; q < V::COUT; ++q) acc[q] += (double)fa[q];
+    acc[V::NRM] += (double)fa[V::NRM];
+    acc[V::NRM + 1] += (double)fa[V::NRM + 1];
     // ---- carries -------------------------------------------------------
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -1058,7 +1062,10 @@ struct FCfg {
   static constexpr int NT = (RW + 1) * 32;    // + 1 halo warp
 };
 
-template <typename T, int R>
+// KX: row length of the staged FUSED pass as a compile-time constant (128,
+// 256 = x-split rows) or 0 (runtime K1 <= 128).  One kernel per KX so each
+// gets its own register allocation.
+template <typename T, int R, int KX>
 __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A) {
   using V = FV<R>;
   constexpr int RW = FCfg<T, R>::RW;
@@ -1123,12 +1130,13 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   const long long gtid = (long long)blockIdx.x * NT + threadIdx.x;
   const long long seg_begin = (long long)blockIdx.x * A.tile_planes / gridDim.x;
   const long long seg_end = (long long)(blockIdx.x + 1) * A.tile_planes / gridDim.x;
-  const int GWs = A.geo.W / A.wpr;
+  constexpr int wpr = KX > 128 ? 2 : 1;  // warps per x-row
+  const int GWs = A.geo.W / wpr;
   const long long tp_s = (long long)((A.K2 + (GWs - 1) * A.rpw - 1) / ((GWs - 1) * A.rpw)) * A.K3;
   const long long seg_begin_s = (long long)blockIdx.x * tp_s / gridDim.x;
   const long long seg_end_s = (long long)(blockIdx.x + 1) * tp_s / gridDim.x;
   const Fields<T, R> F{A.d, A.U, A.lo_arr, A.hi_arr, N, (T)A.tau, (T)A.lo, (T)A.hi, (T)A.sign};
-  const int lpr = A.lpr, rpw = A.rpw, wpr = A.wpr;
+  const int lpr = A.lpr, rpw = A.rpw;
   // standalone DIV pass: NG row groups of wpr warps, the last group is the halo
   const int NG = (RW + 1) / wpr;
   const int xh = wpr == 2 ? (warp & 1) : 0, wg = warp / wpr;
@@ -1194,12 +1202,8 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         A.trace[320 + 10] = (unsigned long long)(pre + 100 * s_pre[0]);
       }
 #endif
-      if (A.K1 == 128)
-        fused_staged<T, R, NACC, 0, 128>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
-                                         s_empty, uses, acc, my_seg, ncnt, ovf, pre);
-      else
-        fused_staged<T, R, NACC, 0, 0>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
-                                       s_empty, uses, acc, my_seg, ncnt, ovf, pre);
+      fused_staged<T, R, NACC, 0, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
+                                      s_empty, uses, acc, my_seg, ncnt, ovf, pre);
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
       my_cnt = ncnt;
@@ -1866,7 +1870,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.nty = (A.K2 + TYe - 1) / TYe;
   A.tile_planes = (long long)A.nty * A.K3;
 
-  auto kern = wtv_fused_kernel<T, R>;
+  auto kern = A.K1 == 128 ? wtv_fused_kernel<T, R, 128> : (A.K1 == 256 ? wtv_fused_kernel<T, R, 256> : wtv_fused_kernel<T, R, 0>);
   // staged FUSED pass: widest tile whose double-buffered stage fits in smem
   StageMap<R> M;
   M.make(D.d != nullptr, D.lo_arr != nullptr, D.hi_arr != nullptr, D.ndim, true);
