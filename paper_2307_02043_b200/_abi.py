@@ -164,7 +164,7 @@ def load_library(path: Path | str | None = None):
             return _lib
         import os
 
-        p = Path(path) if path is not None else Path(os.environ.get("BQ_LIB", LIB_PATH))
+        p = Path(path) if path is not None else Path(os.environ.get("BQ_LIB") or LIB_PATH)
         if not p.exists():
             raise BqError(
                 f"{p} is missing: build it with `python -m paper_2307_02043_b200.build` "

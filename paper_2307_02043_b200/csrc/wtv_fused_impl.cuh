@@ -800,6 +800,19 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   }
   StepIter cons;
   cons.init(seg_begin, seg_end, K3, nd);
+  // Partial sums of the pass: the accumulated classes (RHS, K0, Cin, norms) are
+  // summed per thread in the field type across steps; in fp32 they are flushed
+  // every FLUSH steps through a fixed-order warp reduction into per-warp f64
+  // accumulators in shared memory (so the f64 partials hold no registers during
+  // the march), and into acc at the end of the pass.
+  constexpr int NSUM = V::COUT + 2;  // [0, COUT) and the two norms
+  constexpr int FLUSH = sizeof(T) == 4 ? 32 : (1 << 30);
+  __shared__ double s_wacc[16][sizeof(T) == 4 ? NSUM : 1];
+  T fa[NACC];
+#pragma unroll
+  for (int q = 0; q < NACC; ++q) fa[q] = 0;
+  if (sizeof(T) == 4)
+    for (int q = lane; q < NSUM; q += 32) s_wacc[warp][q] = 0.0;
   T qc[4] = {0, 0, 0, 0}, iec[4] = {1, 1, 1, 1}, uc[R > 0 ? R : 1][4];
   T f3prev[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -831,10 +844,6 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     const bool pin = cons.has_pin();
     if (k == cons.zs - 1) f3prev[0] = f3prev[1] = f3prev[2] = f3prev[3] = 0;
     const int rowoff = sr * K1 + xb;
-    // per-step partial sums in the field type (one f64 conversion per step)
-    T fa[NACC];
-#pragma unroll
-    for (int q = 0; q < NACC; ++q) fa[q] = 0;
 
     // ---- q(k+1) of this row (+ the row below the tile, by warp 0) -------
     T qn4[4] = {0, 0, 0, 0}, ien[4] = {1, 1, 1, 1}, un[R > 0 ? R : 1][4];
@@ -1028,12 +1037,17 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         }
       }
     }
-    // only the classes the step accumulates (Cout, OVF and NCNT stay constant
-    // here, so the compiler keeps no registers or adds for them)
+    if (sizeof(T) == 4 && (s % FLUSH) == FLUSH - 1) {
 #pragma unroll
-    for (int q = 0; q < V::COUT; ++q) acc[q] += (double)fa[q];
-    acc[V::NRM] += (double)fa[V::NRM];
-    acc[V::NRM + 1] += (double)fa[V::NRM + 1];
+      for (int q = 0; q < NSUM; ++q) {
+        const int src_q = q < V::COUT ? q : V::NRM + (q - V::COUT);
+        double t = (double)fa[src_q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULLM, t, o);
+        if (lane == 0) s_wacc[warp][q] += t;
+        fa[src_q] = 0;
+      }
+    }
     // ---- carries -------------------------------------------------------
 #pragma unroll
     for (int v = 0; v < 4; ++v) {
@@ -1046,14 +1060,26 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     cons.advance();
     ++s;
   }
+  // only the classes the steps accumulate (Cout, OVF and NCNT are untouched)
+#pragma unroll
+  for (int q = 0; q < V::COUT; ++q) acc[q] += (double)fa[q];
+  acc[V::NRM] += (double)fa[V::NRM];
+  acc[V::NRM + 1] += (double)fa[V::NRM + 1];
+  if (sizeof(T) == 4 && lane == 0) {  // s_wacc[warp] is written by this lane only
+#pragma unroll
+    for (int q = 0; q < NSUM; ++q) acc[q < V::COUT ? q : V::NRM + (q - V::COUT)] += s_wacc[warp][q];
+  }
 }
 
 // ---------------------------------------------------------------------------
 // The kernel
 // ---------------------------------------------------------------------------
+#ifndef BQ_LIGHT_R
+#define BQ_LIGHT_R 4  // fp32 ranks <= this run 11 row warps (168 registers), higher ranks 7
+#endif
 template <typename T, int R>
 struct FCfg {
-  static constexpr bool kLight = sizeof(T) == 4 && R <= 2;
+  static constexpr bool kLight = sizeof(T) == 4 && R <= BQ_LIGHT_R;
   // 11 row warps + 1 halo/producer warp = 384 threads -> ~168 registers
 #ifndef BQ_FUSED_RW
 #define BQ_FUSED_RW 11
