@@ -284,6 +284,9 @@ def run_ours(args):
     ls = None
     if not args.no_ls:
         ls = ls_measure(args, dev, ws)  # collective at N > 1
+    more = None
+    if rank == 0 and not args.no_more:
+        more = prox_variants(dev, flush)
 
     if rank == 0:
         peak, peak_kind = hbm_peak()
@@ -318,6 +321,7 @@ def run_ours(args):
                     "h2d_bytes_per_step": 3 * N * 4, "d2h_bytes_per_step": N * 4},
             "gpu_launches": args.steps,
             "ls": ls,
+            "prox_more": more,
             "clocks": sampler.summary(),
             "wall_s_timed_region": wall,
             "prox_phases_last_step": phases,
@@ -327,6 +331,59 @@ def run_ours(args):
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.destroy_process_group()
+
+
+def prox_variants(dev, flush):
+    """Secondary prox shapes (reported beside the headline, not the headline):
+    the config-2 law at 256^3 (config 5's grid, x-split rows) and the BQNPM
+    metric W = tau I + U U^T with rank 4 (K_s = 4) at 128^3 and 256^3.  Each:
+    3 warm-up solves, 5 timed solves of 100 FGP iterations, L2 flushed between."""
+    import torch
+
+    import paper_2307_02043_b200 as bq
+    from paper_2307_02043_b200 import dual_tv_solver as D
+    from paper_2307_02043_b200.configs import config2_inputs
+    from paper_2307_02043_b200.wpm import BoxSet, DiagPlusLowRank
+
+    peak, _ = hbm_peak()
+    out = []
+    cache = {}
+    for n, r, diag in [(256, 1, True), (128, 4, False), (256, 4, False)]:
+        if n not in cache:
+            cache[n] = config2_inputs(n)
+        inp = cache[n]
+        N = n ** 3
+        v = torch.from_numpy(inp["v"].astype(np.float32)).to(dev)
+        if diag:
+            w = DiagPlusLowRank(1.0, torch.from_numpy(inp["u"].astype(np.float32)).to(dev)[:, None],
+                                d=torch.from_numpy(inp["d"].astype(np.float32)).to(dev))
+        else:
+            g = torch.Generator(device="cpu").manual_seed(2000 + r)
+            U = (torch.randn(N, r, generator=g) / np.sqrt(N)).to(dev)
+            w = DiagPlusLowRank(inp["tau_twin"], U)
+        prob = D.DualTvProblem(grid=bq.Grid((n, n, n)), v=v, w=w, reg=inp["reg"], box=BoxSet(0.0, np.inf))
+        wsp = D.ProxWorkspace(prob.grid, torch.float32, dev)
+        for _ in range(3):
+            D.solve_async(prob, wsp, eps=1e-300, max_iter=100)
+        ts = []
+        for _ in range(5):
+            flush.fill_(1.0)
+            s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            s.record()
+            D.solve_async(prob, wsp, eps=1e-300, max_iter=100)
+            e.record()
+            torch.cuda.synchronize(dev)
+            ts.append(s.elapsed_time(e))
+        ms = float(np.median(ts))
+        bpv = bytes_per_voxel_iter(4, r, diag)
+        achieved = bpv * N * 100 / (ms * 1e-3) / 1e9
+        out.append({"workload": f"{n}^3 fp32 rank {r} " + ("diag(d)+uu^T (config-2 law)" if diag else
+                                                           "tau I + U U^T (BQNPM metric)") + ", 100 FGP iterations",
+                    "ms_per_solve": ms, "value": N * 100 / (ms * 1e-3), "unit": UNIT,
+                    "roofline": {"achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                                 "algorithmic_bytes_per_voxel_iter": bpv}})
+        del prob, wsp, w, v
+    return out
 
 
 def ls_measure(args, dev, ws=1):
@@ -408,6 +465,7 @@ def main():
     ap.add_argument("--cpu-iters", type=int, default=8)
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ls", action="store_true")
+    ap.add_argument("--no-more", action="store_true", help="skip the secondary prox shapes (256^3, rank 4)")
     ap.add_argument("--ls-n", type=int, default=128)
     ap.add_argument("--ls-steps", type=int, default=2)
     args = ap.parse_args()
