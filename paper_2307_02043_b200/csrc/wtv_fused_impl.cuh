@@ -1937,7 +1937,13 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   BQ_CHECK(per_sm > 0, BQ_ECUDA, "wtv_fused: kernel does not fit on an SM");
   // one block per SM; small problems use fewer (cheaper barriers, enough work)
   long long G = std::min<long long>(ctx->num_sms, A.tile_planes);
-  G = std::max<long long>(1, std::min<long long>(G, (A.N + 2047) / 2048));
+  {
+    // small grids: at least ~min_vox voxels per block (the z-march depth per block
+    // sets the pass latency there, the barrier cost grows only slowly with G)
+    const char* mv = getenv("BQ_PROX_MINVOX");
+    const long long min_vox = mv ? std::max(64, atoi(mv)) : 512;
+    G = std::max<long long>(1, std::min<long long>(G, (A.N + min_vox - 1) / min_vox));
+  }
   {
     const int GW = W / A.wpr;
     const long long tp_s = (long long)((A.K2 + (GW - 1) * A.rpw - 1) / ((GW - 1) * A.rpw)) * A.K3;
