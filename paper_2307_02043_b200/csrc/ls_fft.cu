@@ -127,6 +127,36 @@ __device__ __forceinline__ void dft(V (&a)[R]) {
   for (int k = 0; k < R; ++k) a[k] = t[k];
 }
 
+// dft with pruning: HIN -- inputs a[R/2 .. R) are zero (the first DIF stage
+// is a twiddle only); HOUT -- only the outputs k < R/2 are needed (the last
+// stage keeps its even positions, which are the bit-reversed k < R/2).
+template <int R, int DIR, bool HIN, bool HOUT, typename V>
+__device__ __forceinline__ void dft_p(V (&a)[R]) {
+#pragma unroll
+  for (int half = R / 2; half >= 1; half >>= 1) {
+#pragma unroll
+    for (int base = 0; base < R; base += 2 * half) {
+#pragma unroll
+      for (int j = 0; j < half; ++j) {
+        const V u = a[base + j], v = a[base + j + half];
+        if (HIN && half == R / 2) {
+          a[base + j + half] = tw32<DIR>(u, j * (32 / (2 * half)));
+        } else if (HOUT && half == 1) {
+          a[base + j] = cadd(u, v);
+        } else {
+          a[base + j] = cadd(u, v);
+          a[base + j + half] = tw32<DIR>(csub(u, v), j * (32 / (2 * half)));
+        }
+      }
+    }
+  }
+  V t[R];
+#pragma unroll
+  for (int k = 0; k < (HOUT ? R / 2 : R); ++k) t[k] = a[brev<R>(k)];
+#pragma unroll
+  for (int k = 0; k < (HOUT ? R / 2 : R); ++k) a[k] = t[k];
+}
+
 // shared-memory position of Y[n1][k2] for line l.  COL: lines are adjacent
 // columns and l is the fastest index; rows: each line's slab is padded so the
 // step-3 reads (stride R1+1) are bank-conflict free.
@@ -141,12 +171,12 @@ constexpr int smem_elems() {
 }
 
 // step 1: a[s][n2] = x[n1 + R1 n2] (n1 = t + C s) -> smem Y[n1][k2] w_m^(DIR n1 k2)
-template <int R1, int R2, int C, int L, bool COL, int DIR, typename V>
+template <int R1, int R2, int C, int L, bool COL, int DIR, bool HIN = false, typename V>
 __device__ __forceinline__ void step1(V (&a)[R1 / C][R2], V* sm, const V* tw, int l, int t) {
   constexpr int M = R1 * R2;
 #pragma unroll
   for (int s = 0; s < R1 / C; ++s) {
-    dft<R2, DIR>(a[s]);
+    dft_p<R2, DIR, HIN, false>(a[s]);
     const int n1 = t + C * s;
 #pragma unroll
     for (int k2 = 0; k2 < R2; ++k2) {
@@ -158,14 +188,14 @@ __device__ __forceinline__ void step1(V (&a)[R1 / C][R2], V* sm, const V* tw, in
 }
 
 // step 3: b[s][k1] = X[k2 + R2 k1], k2 = t + C s
-template <int R1, int R2, int C, int L, bool COL, int DIR, typename V>
+template <int R1, int R2, int C, int L, bool COL, int DIR, bool HOUT = false, typename V>
 __device__ __forceinline__ void step3(V (&b)[R2 / C][R1], const V* sm, int l, int t) {
 #pragma unroll
   for (int s = 0; s < R2 / C; ++s) {
     const int k2 = t + C * s;
 #pragma unroll
     for (int n1 = 0; n1 < R1; ++n1) b[s][n1] = sm[spos<R1, R2, L, COL>(l, n1, k2)];
-    dft<R1, DIR>(b[s]);
+    dft_p<R1, DIR, false, HOUT>(b[s]);
   }
 }
 
@@ -305,7 +335,10 @@ constexpr int zc_smem_elems(int n) {
   return R1 * R2 + R1 * R2 * L + (n + 1) * L;
 }
 
-template <typename T, int R1, int R2, int C, int L>
+// STD: the volume-to-volume case (z0 = zo0 = 0, nzi = nzo = n = m/2): the
+// zero half of the input and the dropped half of the output are compile-time
+// (no bounds tests, pruned first forward / last inverse DFT stages).
+template <typename T, int R1, int R2, int C, int L, bool STD>
 __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi, int zo0, int nzo, int adj,
                                                   const typename CV<T>::V* __restrict__ khat,
                                                   typename CV<T>::V* __restrict__ q, const int* __restrict__ active) {
@@ -337,6 +370,7 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
     return b;
   };
   bool first = true;
+  constexpr int ZS = M * M;  // plane stride (32-bit offsets within one view's Q)
   for (int b = next_active(0); b < B; b = next_active(b + 1)) {
     V* col = q + (long long)b * vstride + (long long)y * M + x;
     V a[R1 / C][R2];
@@ -345,7 +379,8 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
 #pragma unroll
       for (int n2 = 0; n2 < R2; ++n2) {
         const int e = t + C * s + R1 * n2;
-        a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
+        if (STD) a[s][n2] = n2 < R2 / 2 ? col[e * ZS] : czero<V>();
+        else a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
       }
     {  // the next active view's column into L2 while this one computes
       const int bn = next_active(b + 1);
@@ -356,7 +391,7 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
     }
     if (first) cp_async_wait_all();
     __syncthreads();  // twiddles + K_hat staged (first view); previous view's reads of sm done
-    step1<R1, R2, C, L, true, -1>(a, sm, tw, l, t);
+    step1<R1, R2, C, L, true, -1, STD>(a, sm, tw, l, t);
     __syncthreads();
     V c[R2 / C][R1];
     step3<R1, R2, C, L, true, -1>(c, sm, l, t);
@@ -376,13 +411,17 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
     step1<R2, R1, C, L, true, 1>(c, sm, tw, l, t);
     __syncthreads();
     V o[R1 / C][R2];
-    step3<R2, R1, C, L, true, 1>(o, sm, l, t);
+    step3<R2, R1, C, L, true, 1, STD>(o, sm, l, t);
 #pragma unroll
     for (int s = 0; s < R1 / C; ++s)
 #pragma unroll
       for (int k1 = 0; k1 < R2; ++k1) {
         const int z = t + C * s + R1 * k1;
-        if (z >= zo0 && z < zo0 + nzo) col[(z - zo0) * zs] = o[s][k1];
+        if (STD) {
+          if (k1 < R2 / 2) col[z * ZS] = o[s][k1];
+        } else if (z >= zo0 && z < zo0 + nzo) {
+          col[(z - zo0) * zs] = o[s][k1];
+        }
       }
     first = false;
   }
@@ -563,15 +602,19 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   const bool adj = op == 1 || op == 3;
   int rc;
   if ((rc = prep(xf_kernel<T, R1, R2, C, L>, sm_row)) || (rc = prep(yf_kernel<T, R1, R2, C, L>, sm_col)) ||
-      (rc = prep(zc_kernel<T, R1, R2, C, L>, sm_zc)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
+      (rc = prep(zc_kernel<T, R1, R2, C, L, true>, sm_zc)) || (rc = prep(zc_kernel<T, R1, R2, C, L, false>, sm_zc)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
       (rc = prep(xi_kernel<T, R1, R2, C, L>, sm_row)))
     return rc;
   const int rows_in = nzi * n, rows_out = nzo * n;
   xf_kernel<T, R1, R2, C, L><<<dim3(B, (rows_in + L - 1) / L), NT, sm_row, st>>>(
       n, rows_in, (op == 0 || op == 2) ? (const T*)f : nullptr, (const V*)v, hx, active);
   yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q, active);
-  zc_kernel<T, R1, R2, C, L><<<dim3(M * (M / L)), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
-                                                                  (const V*)khat, q, active);
+  if (nzi == n && nzo == n && z0 == 0 && zo0 == 0)
+    zc_kernel<T, R1, R2, C, L, true><<<dim3(M * (M / L)), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
+                                                                        (const V*)khat, q, active);
+  else
+    zc_kernel<T, R1, R2, C, L, false><<<dim3(M * (M / L)), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
+                                                                         (const V*)khat, q, active);
   yi_kernel<T, R1, R2, C, L><<<dim3(B, nzo * (M / L)), NT, sm_col, st>>>(n, q, hx, active);
   if (nblk) *nblk = (rows_out + L - 1) / L;
   const bool crop = op != 2;
