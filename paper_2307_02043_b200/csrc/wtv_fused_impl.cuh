@@ -276,15 +276,14 @@ __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], con
   const bool near = !inside && !low && !high;
   // branch-free accumulation (selects, never arithmetic on an unused +-inf bound)
   const T k0 = low ? av - l : (HINF ? (near ? av : (T)0) : (high ? av - h : (near ? av : (T)0)));
+  // Cin += [inside] u s^T as one select per column and fused multiply-adds
   int k = 0;
 #pragma unroll
   for (int c = 0; c < R; ++c) {
+    const AccT ui = inside ? (AccT)u[c] : (AccT)0;
 #pragma unroll
-    for (int c2 = 0; c2 <= c; ++c2, ++k) {
-      const AccT us = (AccT)u[c] * (AccT)s[c2];
-      acc[V::CIN + k] += inside ? us : (AccT)0;
-    }
-    acc[V::K0 + c] += (AccT)u[c] * (AccT)k0;
+    for (int c2 = 0; c2 <= c; ++c2, ++k) acc[V::CIN + k] = fma(ui, (AccT)s[c2], acc[V::CIN + k]);
+    acc[V::K0 + c] = fma((AccT)u[c], (AccT)k0, acc[V::K0 + c]);
   }
   return near;
 }
