@@ -287,6 +287,12 @@ def run_ours(args):
     more = None
     if rank == 0 and not args.no_more:
         more = prox_variants(dev, flush)
+    loop = None
+    if rank == 0 and not args.no_loop:
+        sys.path.insert(0, str(ROOT / "bench"))
+        import loop_bench
+
+        loop = loop_bench.measure(reps=2)
 
     if rank == 0:
         peak, peak_kind = hbm_peak()
@@ -322,6 +328,7 @@ def run_ours(args):
             "gpu_launches": args.steps,
             "ls": ls,
             "prox_more": more,
+            "bqnpm_loop": loop,
             "clocks": sampler.summary(),
             "wall_s_timed_region": wall,
             "prox_phases_last_step": phases,
@@ -466,6 +473,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ls", action="store_true")
     ap.add_argument("--no-more", action="store_true", help="skip the secondary prox shapes (256^3, rank 4)")
+    ap.add_argument("--no-loop", action="store_true", help="skip the end-to-end BQNPM loop runs (bench/loop_bench.py)")
     ap.add_argument("--ls-n", type=int, default=128)
     ap.add_argument("--ls-steps", type=int, default=2)
     args = ap.parse_args()

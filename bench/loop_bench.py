@@ -43,23 +43,27 @@ def timed_run(views, grid, cfg, xgt, reps):
             "final_snr_db": float(tr.rows[-1].snr_db)}
 
 
-def main():
-    ap = argparse.ArgumentParser()
-    ap.add_argument("--reps", type=int, default=3)
-    args = ap.parse_args()
-    out = {}
+def measure(reps=3):
+    out = {"note": "wall clock of bqnpm_run incl. Lipschitz startup + initializer, view construction excluded"}
     n = 32
     grid = Grid((n, n, n))
     xgt = make_phantom(grid, seed=0).values - 1.333  # the reference's nested spheres, as dn in [0, 0.03]
     views = make_linear_views(grid, 16, seed=1001, x_gt=xgt, noise_snr_db=30.0)
     cfg = S.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=20, box=BoxSet(0.0, 0.1), seed=0)
-    out["dct_32_L16_bqnpm20"] = timed_run(views, grid, cfg, xgt, args.reps)
+    out["dct_32_L16_bqnpm20"] = timed_run(views, grid, cfg, xgt, reps)
     out["dct_32_L16_bqnpm20"]["reference_cpu_s"] = 4.93  # SURVEY 6, measured on the reference in the survey container
     xgt1 = born_spheres_phantom(n, seed=1000)
     views1, _ = PH.make_scatter_views(n, 16, model="born", x_gt=xgt1, noise_snr_db=30.0, seed=1001,
                                       dtype=torch.complex128, theta_deg=35.0, batch=8)
-    out["config1_born_32_L16_bqnpm20"] = timed_run(views1, grid, cfg, xgt1, args.reps)
-    print(json.dumps(out))
+    out["config1_born_32_L16_bqnpm20"] = timed_run(views1, grid, cfg, xgt1, reps)
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--reps", type=int, default=3)
+    args = ap.parse_args()
+    print(json.dumps(measure(args.reps)))
 
 
 if __name__ == "__main__":
