@@ -234,11 +234,13 @@ __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefe
 // input (f .* v, or the detector residual plane), zero-padded to m.
 // ---------------------------------------------------------------------------
 template <typename T, int R1, int R2, int C, int L>
-__global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __restrict__ f,
+__global__ void __launch_bounds__(C* L) xf_kernel(int n_rt, int rows, const T* __restrict__ f,
                                                   const typename CV<T>::V* __restrict__ v,
                                                   typename CV<T>::V* __restrict__ hx, const int* __restrict__ active) {
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2;
+  constexpr int n = M / 2;  // the pruned passes serve n = m/2 only (dispatch on 2n)
+  (void)n_rt;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* tw = (V*)smraw;
   V* sm = tw + M;
@@ -267,7 +269,7 @@ __global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __re
       a[s][n2] = x;
     }
   __syncthreads();
-  step1<R1, R2, C, L, false, -1>(a, sm, tw, l, t);
+  step1<R1, R2, C, L, false, -1, true>(a, sm, tw, l, t);
   __syncthreads();
   V c[R2 / C][R1];
   step3<R1, R2, C, L, false, -1>(c, sm, l, t);
@@ -284,11 +286,13 @@ __global__ void __launch_bounds__(C* L) xf_kernel(int n, int rows, const T* __re
 // YF: forward y pass over columns (z < nz_in, x < m): Hx[z][y<n][x] -> Q[z][y<m][x]
 // ---------------------------------------------------------------------------
 template <typename T, int R1, int R2, int C, int L>
-__global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V* __restrict__ hx,
+__global__ void __launch_bounds__(C* L) yf_kernel(int n_rt, const typename CV<T>::V* __restrict__ hx,
                                                   typename CV<T>::V* __restrict__ q, const int* __restrict__ active) {
   if (active && !active[blockIdx.x]) return;
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2, XT = M / L;
+  constexpr int n = M / 2;  // the pruned passes serve n = m/2 only (dispatch on 2n)
+  (void)n_rt;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* tw = (V*)smraw;
   V* sm = tw + M;
@@ -305,7 +309,7 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n, const typename CV<T>::V
       a[s][n2] = e < n ? src[(long long)e * M] : czero<V>();
     }
   __syncthreads();
-  step1<R1, R2, C, L, true, -1>(a, sm, tw, l, t);
+  step1<R1, R2, C, L, true, -1, true>(a, sm, tw, l, t);
   __syncthreads();
   V c[R2 / C][R1];
   step3<R1, R2, C, L, true, -1>(c, sm, l, t);
@@ -432,11 +436,13 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
 // YI: inverse y pass over columns (z < nz_out, x < m): Q[z][y<m][x] -> Hx[z][y<n][x]
 // ---------------------------------------------------------------------------
 template <typename T, int R1, int R2, int C, int L>
-__global__ void __launch_bounds__(C* L) yi_kernel(int n, const typename CV<T>::V* __restrict__ q,
+__global__ void __launch_bounds__(C* L) yi_kernel(int n_rt, const typename CV<T>::V* __restrict__ q,
                                                   typename CV<T>::V* __restrict__ hx, const int* __restrict__ active) {
   if (active && !active[blockIdx.x]) return;
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2, XT = M / L;
+  constexpr int n = M / 2;  // the pruned passes serve n = m/2 only (dispatch on 2n)
+  (void)n_rt;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* tw = (V*)smraw;
   V* sm = tw + M;
@@ -453,7 +459,7 @@ __global__ void __launch_bounds__(C* L) yi_kernel(int n, const typename CV<T>::V
   step1<R1, R2, C, L, true, 1>(a, sm, tw, l, t);
   __syncthreads();
   V c[R2 / C][R1];
-  step3<R1, R2, C, L, true, 1>(c, sm, l, t);
+  step3<R1, R2, C, L, true, 1, true>(c, sm, l, t);
   V* dst = hx + ((long long)b * n + z) * n * M + x;
 #pragma unroll
   for (int s = 0; s < R2 / C; ++s)
@@ -470,7 +476,7 @@ __global__ void __launch_bounds__(C* L) yi_kernel(int n, const typename CV<T>::V
 //   out = beta * scale * (fconj .* G) + alpha * v + addend
 // ---------------------------------------------------------------------------
 template <typename T, int R1, int R2, int C, int L>
-__global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typename CV<T>::V* __restrict__ hx,
+__global__ void __launch_bounds__(C* L) xi_kernel(int n_rt, int rows, const typename CV<T>::V* __restrict__ hx,
                                                   double scale, const T* __restrict__ fconj,
                                                   const typename CV<T>::V* __restrict__ v, double alpha, double beta,
                                                   const typename CV<T>::V* __restrict__ addend,
@@ -478,6 +484,8 @@ __global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typenam
                                                   const typename CV<T>::V* __restrict__ da, double* __restrict__ dotp) {
   using V = typename CV<T>::V;
   constexpr int M = R1 * R2;
+  constexpr int n = M / 2;  // the pruned passes serve n = m/2 only (dispatch on 2n)
+  (void)n_rt;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* tw = (V*)smraw;
   V* sm = tw + M;
@@ -505,7 +513,7 @@ __global__ void __launch_bounds__(C* L) xi_kernel(int n, int rows, const typenam
   step1<R1, R2, C, L, false, 1>(a, sm, tw, l, t);
   __syncthreads();
   V c[R2 / C][R1];
-  step3<R1, R2, C, L, false, 1>(c, sm, l, t);
+  step3<R1, R2, C, L, false, 1, true>(c, sm, l, t);
   // fused per-view dot partials of the result: (sum conj(da) out, sum |out|^2)
   double dre = 0.0, dim = 0.0, dnn = 0.0;
   if (ok) {
