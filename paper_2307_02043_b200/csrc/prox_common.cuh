@@ -17,11 +17,17 @@ __device__ __forceinline__ float rcp(float x) { return __frcp_rn(x); }
 __device__ __forceinline__ double rcp(double x) { return 1.0 / x; }
 
 // Isotropic dual-ball projection p / max(||p||, 1) (tv_ops.py:177-179).
+// f32: branch-free, s = min(1/sqrt(ss), 1) is 1 exactly when ss <= 1 (also
+// for ss == 0 or a denormal ss, whose ftz reciprocal root is +inf).
+__device__ __forceinline__ float rsqrt_ftz(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float ball_scale(float ss) { return fminf(rsqrt_ftz(ss), 1.0f); }
 __device__ __forceinline__ void ball(float (&w)[3], float ss) {
-  if (ss > 1.0f) {
-    const float s = rsqrtf(ss);
-    w[0] *= s, w[1] *= s, w[2] *= s;
-  }
+  const float s = ball_scale(ss);
+  w[0] *= s, w[1] *= s, w[2] *= s;
 }
 __device__ __forceinline__ void ball(double (&w)[3], double ss) {
   const double den = fmax(sqrt(ss), 1.0);
@@ -63,6 +69,75 @@ struct Vec4<double> {
     reinterpret_cast<double2*>(p)[1] = make_double2(o[2], o[3]);
   }
 };
+
+// ---- voxel pairs: sm_100 packed fp32x2 arithmetic (FADD2/FMUL2/FFMA2) ----
+// One instruction serves two adjacent voxels in f32 (the x-vector of a lane
+// is held as two pairs); f64 pairs are two scalar operations.  Negation and
+// |x| of an operand fold into the packed instruction's operand modifiers.
+template <typename T>
+struct Pair;
+template <>
+struct Pair<float> {
+  using t = float2;
+};
+template <>
+struct Pair<double> {
+  using t = double2;
+};
+template <typename T>
+using pair_t = typename Pair<T>::t;
+
+__device__ __forceinline__ float2 mk2(float a, float b) { return make_float2(a, b); }
+__device__ __forceinline__ double2 mk2(double a, double b) { return make_double2(a, b); }
+__device__ __forceinline__ float2 bc2(float a) { return make_float2(a, a); }
+__device__ __forceinline__ double2 bc2(double a) { return make_double2(a, a); }
+__device__ __forceinline__ float2 add2(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 sub2(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a, b); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
+__device__ __forceinline__ float2 abs2(float2 a) { return make_float2(fabsf(a.x), fabsf(a.y)); }
+__device__ __forceinline__ double2 add2(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 sub2(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double2 mul2(double2 a, double2 b) { return make_double2(a.x * b.x, a.y * b.y); }
+__device__ __forceinline__ double2 fma2(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, c.x), fma(a.y, b.y, c.y));
+}
+__device__ __forceinline__ double2 abs2(double2 a) { return make_double2(fabs(a.x), fabs(a.y)); }
+// element e (compile-time under unrolling) of a 2-pair x-vector
+template <typename P>
+__device__ __forceinline__ auto& el(P (&a)[2], int e) {
+  return (e & 1) ? a[e >> 1].y : a[e >> 1].x;
+}
+template <typename P>
+__device__ __forceinline__ const auto& el(const P (&a)[2], int e) {
+  return (e & 1) ? a[e >> 1].y : a[e >> 1].x;
+}
+// 4 consecutive elements as two pairs (16-byte f32 / 2 x 16-byte f64 accesses)
+__device__ __forceinline__ void ld2(const float* p, float2 (&o)[2]) {
+  const float4 v = *reinterpret_cast<const float4*>(p);
+  o[0] = make_float2(v.x, v.y), o[1] = make_float2(v.z, v.w);
+}
+__device__ __forceinline__ void ld2(const double* p, double2 (&o)[2]) {
+  o[0] = reinterpret_cast<const double2*>(p)[0];
+  o[1] = reinterpret_cast<const double2*>(p)[1];
+}
+__device__ __forceinline__ void st2(float* p, const float2 (&o)[2]) {
+  *reinterpret_cast<float4*>(p) = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
+}
+__device__ __forceinline__ void st2(double* p, const double2 (&o)[2]) {
+  reinterpret_cast<double2*>(p)[0] = o[0];
+  reinterpret_cast<double2*>(p)[1] = o[1];
+}
+// dual-ball projection of two voxels' (w0, w1, w2) given ss = ||w||^2 per voxel
+__device__ __forceinline__ void ball2(float2 (&w)[3], float2 ss) {
+  const float2 s = make_float2(ball_scale(ss.x), ball_scale(ss.y));
+  w[0] = mul2(w[0], s), w[1] = mul2(w[1], s), w[2] = mul2(w[2], s);
+}
+__device__ __forceinline__ void ball2(double2 (&w)[3], double2 ss) {
+  const double dx = fmax(sqrt(ss.x), 1.0), dy = fmax(sqrt(ss.y), 1.0);
+#pragma unroll
+  for (int n = 0; n < 3; ++n) w[n].x /= dx, w[n].y /= dy;
+}
 
 // ---- small dense linear algebra for the controller (r <= 8), unrolled ----
 // cap/H are symmetric; packed lower index k(i, j) = i (i + 1) / 2 + j, j <= i.

@@ -288,6 +288,54 @@ __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], con
   return near;
 }
 
+// aggregate() for a voxel pair (packed f32x2 where the arithmetic allows):
+// the same classification and sums, element by element; u is the lane's
+// [RR][2] pair array, p selects the pair.
+template <typename T, int R, int NACC, bool HINF>
+__device__ __forceinline__ void aggregate2(pair_t<T> av, const pair_t<T> (&s)[R > 0 ? R : 1],
+                                           const pair_t<T> (&u)[R > 0 ? R : 1][2], int p, pair_t<T> l,
+                                           pair_t<T> h, const T* gc, const T* gwid,
+                                           pair_t<T> (&acc)[NACC], bool& n0, bool& n1) {
+  using V = FV<R>;
+  using P = pair_t<T>;
+  P zc = av, rho = bc2((T)0);
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    zc = fma2(s[c], bc2(gc[c]), zc);
+    rho = fma2(abs2(s[c]), bc2(gwid[c]), rho);
+  }
+  const T eps = (sizeof(T) == 4) ? (T)1e-5 : (T)1e-13;
+  rho = fma2(rho, bc2((T)1 + eps), mul2(add2(abs2(zc), abs2(av)), bc2(eps)));
+  const P lo_side = sub2(zc, rho), hi_side = add2(zc, rho);
+  const P avl = sub2(av, l);
+  bool in[2], nr[2];
+  P k0;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const T ls = e ? lo_side.y : lo_side.x, hs = e ? hi_side.y : hi_side.x;
+    const T le = e ? l.y : l.x, he = e ? h.y : h.x, a = e ? av.y : av.x;
+    const bool inside = (ls > le) && (HINF || hs < he);
+    const bool low = !inside && (hs <= le);
+    const bool high = HINF ? false : (!inside && !low && (ls >= he));
+    const bool near = !inside && !low && !high;
+    const T kl = e ? avl.y : avl.x;
+    const T kv = low ? kl : (HINF ? (near ? a : (T)0) : (high ? a - he : (near ? a : (T)0)));
+    if (e) k0.y = kv;
+    else k0.x = kv;
+    in[e] = inside, nr[e] = near;
+  }
+  int k = 0;
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    const P uu = u[c][p];
+    const P ui = mk2(in[0] ? uu.x : (T)0, in[1] ? uu.y : (T)0);
+#pragma unroll
+    for (int c2 = 0; c2 <= c; ++c2, ++k) acc[V::CIN + k] = fma2(ui, s[c2], acc[V::CIN + k]);
+    acc[V::K0 + c] = fma2(uu, k0, acc[V::K0 + c]);
+  }
+  n0 = nr[0], n1 = nr[1];
+}
+
 // Warp-deterministic compaction of near voxels into this warp's segment; the
 // entry carries the voxel's data (a, lo, hi, u[R], s[R]) so the on-chip Newton
 // never has to chase indices.
@@ -709,9 +757,9 @@ __device__ __forceinline__ void issue_step(const FArgs<T>& A, const StepIter& it
              bytes, bar);
 }
 
-// MODE 0: generic (runtime per-voxel d, optional bound arrays); 1: per-voxel
-// d, scalar bounds; 2: scalar tau, scalar bounds.  Modes 1/2 make the stage
-// layout a compile-time constant.
+// MODE 0: generic (optional bound arrays); 1: scalar bounds (the bounds are
+// pass constants, no bound fields in the stage).  Per-voxel d or scalar tau is
+// a runtime choice in both.
 // KX > 0: the row length K1 == KX is a compile-time constant (lane -> voxel
 // mapping, row offsets and every per-row branch fold; K1 == 128 is the
 // common 128^3 case), KX == 0: runtime K1.
@@ -752,7 +800,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   const T m_prev = sh.m_prev, m_cur = sh.m_cur;
   const bool div_p = sh.div_p;
   const T step = (T)A.step, reg = (T)A.reg, sg = (T)A.sign;
-  const bool diag = MODE == 0 ? (A.d != nullptr) : (MODE == 1);
+  const bool diag = A.d != nullptr;
   const T itauT = diag ? (T)1 : rcp((T)A.tau);
   const bool iso = A.mode == BQ_TV_ISO;
   StageMap<R> M;
@@ -800,22 +848,33 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   StepIter cons;
   cons.init(seg_begin, seg_end, K3, nd);
   // Partial sums of the pass: the accumulated classes (RHS, K0, Cin, norms) are
-  // summed per thread in the field type across steps; in fp32 they are flushed
-  // every FLUSH steps through a fixed-order warp reduction into per-warp f64
-  // accumulators in shared memory (so the f64 partials hold no registers during
-  // the march), and into acc at the end of the pass.
+  // summed per thread in the field type across steps, as voxel pairs (packed
+  // f32x2 in f32); in fp32 they are flushed every FLUSH steps through a
+  // fixed-order warp reduction into per-warp f64 accumulators in shared memory
+  // (so the f64 partials hold no registers during the march), and into acc at
+  // the end of the pass.
+  using P = pair_t<T>;
+  constexpr int RR = R > 0 ? R : 1;
   constexpr int NSUM = V::COUT + 2;  // [0, COUT) and the two norms
   constexpr int FLUSH = sizeof(T) == 4 ? 32 : (1 << 30);
   __shared__ double s_wacc[16][sizeof(T) == 4 ? NSUM : 1];
-  T fa[NACC];
+  P fa[NACC];
 #pragma unroll
-  for (int q = 0; q < NACC; ++q) fa[q] = 0;
+  for (int q = 0; q < NACC; ++q) fa[q] = bc2((T)0);
   if (sizeof(T) == 4)
     for (int q = lane; q < NSUM; q += 32) s_wacc[warp][q] = 0.0;
-  T qc[4] = {0, 0, 0, 0}, iec[4] = {1, 1, 1, 1}, uc[R > 0 ? R : 1][4];
-  T f3prev[4] = {0, 0, 0, 0};
+  P qc[2] = {bc2((T)0), bc2((T)0)}, iec[2] = {bc2((T)1), bc2((T)1)}, uc[RR][2];
+  P f3p[2] = {bc2((T)0), bc2((T)0)};
 #pragma unroll
-  for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][0] = uc[c][1] = uc[c][2] = uc[c][3] = 0;
+  for (int c = 0; c < RR; ++c) uc[c][0] = uc[c][1] = bc2((T)0);
+  // branch-free forms of the pass constants: src = w + m_src (w - p_{i-1})
+  // (m_src = 0 on the last iteration, the div source is p_i itself); sgz =
+  // sign * gamma so that q = clamp(a + (u / d) sgz) (the sign is exact)
+  const P m_src2 = bc2(div_p ? (T)0 : m_cur), m_prev2 = bc2(m_prev), step2 = bc2(step);
+  const P nreg2 = bc2(sh.single ? (T)0 : -reg);
+  T sgz[RR], gcv[RR], gwv[RR];
+#pragma unroll
+  for (int c = 0; c < RR; ++c) sgz[c] = R > 0 ? sg * sh.gz[c] : (T)0, gcv[c] = sh.gc[c], gwv[c] = sh.gwid[c];
   int s = 0;
   while (cons.valid) {
     const int b = s & 1;
@@ -841,122 +900,114 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     const bool real = act && !halo;
     const bool warm = k < cons.z0;
     const bool pin = cons.has_pin();
-    if (k == cons.zs - 1) f3prev[0] = f3prev[1] = f3prev[2] = f3prev[3] = 0;
+    if (k == cons.zs - 1) f3p[0] = f3p[1] = bc2((T)0);
     const int rowoff = sr * K1 + xb;
 
     // ---- q(k+1) of this row (+ the row below the tile, by warp 0) -------
-    T qn4[4] = {0, 0, 0, 0}, ien[4] = {1, 1, 1, 1}, un[R > 0 ? R : 1][4];
+    P qn[2] = {bc2((T)0), bc2((T)0)}, ien[2] = {bc2((T)1), bc2((T)1)}, un[RR][2];
 #pragma unroll
-    for (int c = 0; c < (R > 0 ? R : 1); ++c) un[c][0] = un[c][1] = un[c][2] = un[c][3] = 0;
+    for (int c = 0; c < RR; ++c) un[c][0] = un[c][1] = bc2((T)0);
     if (cons.has_qin()) {
-      auto qrow = [&](long long off, T (&q)[4], T (&ie)[4], T (&u)[R > 0 ? R : 1][4]) {
-        T l[4], h[4];
-        Vec4<T>::rw(stg + M.A * g.slot_elems + off, q);
-        if (diag) Vec4<T>::rw(stg + M.D * g.slot_elems + off, ie);  // 1/d, precomputed
-        else ie[0] = ie[1] = ie[2] = ie[3] = itauT;
+      auto qrow = [&](long long off, P (&q)[2], P (&ie)[2], P (&u)[RR][2]) {
+        P l[2], h[2];
+        ld2(stg + M.A * g.slot_elems + off, q);
+        if (diag) ld2(stg + M.D * g.slot_elems + off, ie);  // 1/d, precomputed
+        else ie[0] = ie[1] = bc2(itauT);
 #pragma unroll
-        for (int c = 0; c < R; ++c) Vec4<T>::rw(stg + (M.U0 + c) * g.slot_elems + off, u[c]);
-        if (M.LO >= 0) Vec4<T>::rw(stg + M.LO * g.slot_elems + off, l);
-        else l[0] = l[1] = l[2] = l[3] = lo_s;
-        if (M.HI >= 0) Vec4<T>::rw(stg + M.HI * g.slot_elems + off, h);
-        else h[0] = h[1] = h[2] = h[3] = hi_s;
+        for (int c = 0; c < R; ++c) ld2(stg + (M.U0 + c) * g.slot_elems + off, u[c]);
+        if (MODE == 0 && M.LO >= 0) ld2(stg + M.LO * g.slot_elems + off, l);
+        else l[0] = l[1] = bc2(lo_s);
+        if (MODE == 0 && M.HI >= 0) ld2(stg + M.HI * g.slot_elems + off, h);
+        else h[0] = h[1] = bc2(hi_s);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          T z = q[v];
+        for (int p = 0; p < 2; ++p) {
+          P z = q[p];
 #pragma unroll
-          for (int c = 0; c < R; ++c) z += (sg * u[c][v] * ie[v]) * sh.gz[c];
-          q[v] = clampv(z, l[v], h[v]);
+          for (int c = 0; c < R; ++c) z = fma2(mul2(u[c][p], ie[p]), bc2(sgz[c]), z);
+          q[p] = mk2(clampv(z.x, l[p].x, h[p].x), clampv(z.y, l[p].y, h[p].y));
         }
       };
       T* qdst = qbuf + (long long)((k + 1) & 1) * g.slot_elems;
       if (act) {
-        qrow(rowoff, qn4, ien, un);
-        Vec4<T>::st(qdst + rowoff, qn4);
+        qrow(rowoff, qn, ien, un);
+        st2(qdst + rowoff, qn);
       }
       if (halo && yr == 0 && y0 + TYe < K2) {
         const long long off = (long long)(GW * rpw) * K1 + xb;
-        T qb[4], ib[4], ub[R > 0 ? R : 1][4];
+        P qb[2], ib[2], ub[RR][2];
         qrow(off, qb, ib, ub);
-        Vec4<T>::st(qdst + off, qb);
+        st2(qdst + off, qb);
       }
     }
 
     // ---- dual update at plane k (dual_tv_solver.py:225-235) -------------
     // x+1 of element 3; the row's last lane uses its own element 3 (zero gradient)
-    const T qsh = __shfl_down_sync(FULLM, qc[0], 1);
+    const T qsh = __shfl_down_sync(FULLM, qc[0].x, 1);
     // x-split: q(x = 128) of this row comes from the q row published in the last step
-    const T qright = last_in_row ? qc[3] : (edge_src ? qbuf[(long long)(k & 1) * g.slot_elems + rowoff + 4] : qsh);
-    T src[3][4];
-    T vv[4] = {0, 0, 0, 0};
+    const T qright = last_in_row ? qc[1].y : (edge_src ? qbuf[(long long)(k & 1) * g.slot_elems + rowoff + 4] : qsh);
+    P src[3][2];
+    P vv[2] = {bc2((T)0), bc2((T)0)};
 #pragma unroll
-    for (int n = 0; n < 3; ++n) src[n][0] = src[n][1] = src[n][2] = src[n][3] = 0;
+    for (int n = 0; n < 3; ++n) src[n][0] = src[n][1] = bc2((T)0);
     if (pin && act) {
-      const bool has_y = nd >= 2 && y < K2 - 1;
-      const bool has_up = nd >= 3 && k < K3 - 1;
-      T qy[4];  // q of row y+1; at the last row q itself (zero gradient, no select)
-      if (has_y) Vec4<T>::rw(qbuf + (long long)(k & 1) * g.slot_elems + rowoff + K1, qy);
-      else qy[0] = qc[0], qy[1] = qc[1], qy[2] = qc[2], qy[3] = qc[3];
-      if (!has_up) qn4[0] = qc[0], qn4[1] = qc[1], qn4[2] = qc[2], qn4[3] = qc[3];  // last plane
-      T pc4[3][4], pp4[3][4];
+      const bool has_y = y < K2 - 1;
+      const bool has_up = k < K3 - 1;
+      P qy[2];  // q of row y+1; at the last row q itself (zero gradient, no select)
+      if (has_y) ld2(qbuf + (long long)(k & 1) * g.slot_elems + rowoff + K1, qy);
+      else qy[0] = qc[0], qy[1] = qc[1];
+      if (!has_up) qn[0] = qc[0], qn[1] = qc[1];  // last plane
+      P pc[3][2], pp[3][2];
 #pragma unroll
       for (int n = 0; n < 3; ++n) {
-        pc4[n][0] = pc4[n][1] = pc4[n][2] = pc4[n][3] = 0;
-        if (n < nd) Vec4<T>::rw(stg + (M.PC0 + n) * g.slot_elems + rowoff, pc4[n]);
-        if (n < nd && M.PP0 >= 0) Vec4<T>::rw(stg + (M.PP0 + n) * g.slot_elems + rowoff, pp4[n]);
+        ld2(stg + (M.PC0 + n) * g.slot_elems + rowoff, pc[n]);
+        ld2(stg + (M.PP0 + n) * g.slot_elems + rowoff, pp[n]);
       }
-      T pn[3][4];
+      const bool acc_n = real && !warm;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        T gr[3];
-        const T right = (v < 3) ? qc[v + 1] : qright;
-        gr[0] = right - qc[v];
-        gr[1] = qy[v] - qc[v];
-        gr[2] = qn4[v] - qc[v];
-        T w[3], pc3[3];
+      for (int p = 0; p < 2; ++p) {
+        // x neighbours straddle the pairs: element 2p+1's right is 2p+2
+        const T r0 = qc[p].y, r1 = p == 0 ? qc[1].x : qright;
+        P w[3];
+        w[0] = mk2(r0 - qc[p].x, r1 - qc[p].y);
+        w[1] = sub2(qy[p], qc[p]);
+        w[2] = sub2(qn[p], qc[p]);
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
-          pc3[n] = pc4[n][v];
-          T pb = pc3[n];
-          if (M.PP0 >= 0 && n < nd) pb = pc3[n] + m_prev * (pc3[n] - pp4[n][v]);  // P_bar_{i-1} (:235)
-          w[n] = (n < nd) ? pb + step * gr[n] : (T)0;
+          // P_bar_{i-1} = p_{i-1} + m (p_{i-1} - p_{i-2})  (:235), then + step D q
+          const P pb = fma2(m_prev2, sub2(pc[n][p], pp[n][p]), pc[n][p]);
+          w[n] = fma2(step2, w[n], pb);
         }
         if (iso) {
-          T ss = w[0] * w[0];
-          if (nd >= 2) ss += w[1] * w[1];
-          if (nd >= 3) ss += w[2] * w[2];
-          ball(w, ss);
+          ball2(w, fma2(w[2], w[2], fma2(w[1], w[1], mul2(w[0], w[0]))));
         } else {
 #pragma unroll
-          for (int n = 0; n < 3; ++n) w[n] = clampv(w[n], (T)-1, (T)1);
+          for (int n = 0; n < 3; ++n) w[n] = mk2(clampv(w[n].x, (T)-1, (T)1), clampv(w[n].y, (T)-1, (T)1));
         }
 #pragma unroll
         for (int n = 0; n < 3; ++n) {
-          pn[n][v] = w[n];
-          if (real && !warm && n < nd) {
-            const T df = w[n] - pc3[n];
-            fa[V::NRM] += df * df;
-            fa[V::NRM + 1] += pc3[n] * pc3[n];
+          const P df = sub2(w[n], pc[n][p]);
+          if (acc_n) {
+            fa[V::NRM] = fma2(df, df, fa[V::NRM]);
+            fa[V::NRM + 1] = fma2(pc[n][p], pc[n][p], fa[V::NRM + 1]);
           }
-          src[n][v] = div_p ? w[n] : w[n] + m_cur * (w[n] - pc3[n]);
+          src[n][p] = fma2(m_src2, df, w[n]);
+          pc[n][p] = w[n];  // p_i (stored below)
         }
       }
       // boundary rows of D^T have no "-p" term: zero the components the
       // divergence must not see (they feed nothing else), so its sums need no
       // per-voxel selects
-      if (last_in_row) src[0][3] = 0;
-      if (edge_src) s_edge[k & 1][sr] = src[0][3];
-      if (!has_y) src[1][0] = src[1][1] = src[1][2] = src[1][3] = 0;
-      if (!has_up) src[2][0] = src[2][1] = src[2][2] = src[2][3] = 0;
-      if (real && !warm) {
+      if (last_in_row) src[0][1].y = 0;
+      if (edge_src) s_edge[k & 1][sr] = src[0][1].y;
+      if (!has_y) src[1][0] = src[1][1] = bc2((T)0);
+      if (!has_up) src[2][0] = src[2][1] = bc2((T)0);
+      if (acc_n) {
         const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
 #pragma unroll
-        for (int n = 0; n < 3; ++n)
-          if (n < nd) Vec4<T>::st(Pn + n * N + j, pn[n]);
-        Vec4<T>::rw(stg + M.V * g.slot_elems + rowoff, vv);
+        for (int n = 0; n < 3; ++n) st2(Pn + n * N + j, pc[n]);
+        ld2(stg + M.V * g.slot_elems + rowoff, vv);
       }
-      if (nd >= 2) {
-        Vec4<T>::st(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff, src[1]);
-      }
+      st2(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff, src[1]);
     }
     const unsigned long long t_c = tr ? global_ns() : 0;
     named_sync(1, W * 32);  // q(k+1), div-source rows published; stage b fully read
@@ -969,70 +1020,64 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
 
     // ---- a_i = v - reg D^-1 div(src) at plane k + Newton aggregates -----
-    const T lsh = __shfl_up_sync(FULLM, src[0][3], 1);
+    const T lsh = __shfl_up_sync(FULLM, src[0][1].y, 1);
     const T left1 = first_in_row ? (T)0 : (edge_dst ? s_edge[k & 1][sr] : lsh);
     if (pin && !warm && used && !halo) {
-      T av[4] = {0, 0, 0, 0};
+      P av[2] = {bc2((T)0), bc2((T)0)};
       const long long j = (long long)k * A.plane + (long long)y * K1 + xb;
       if (real) {
-        T up[4] = {0, 0, 0, 0};
-        if (y > 0) Vec4<T>::rw(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff - K1, up);
+        P up[2] = {bc2((T)0), bc2((T)0)};
+        if (y > 0) ld2(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff - K1, up);
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          if (sh.single) {
-            av[v] = vv[v];
-            continue;
-          }
+        for (int p = 0; p < 2; ++p) {
           // boundary terms are zero in the data: src at the far faces was
-          // zeroed, up is 0 at y = 0, f3prev is 0 at the first plane
-          const T lk = (v == 0) ? left1 : src[0][v - 1];
-          T dv = lk - src[0][v];
-          if (nd >= 2) dv += up[v] - src[1][v];
-          if (nd >= 3) dv += f3prev[v] - src[2][v];
-          const T de = dv * iec[v];
-          av[v] = vv[v] - reg * de;
+          // zeroed, up is 0 at y = 0, f3p is 0 at the first plane
+          const T l0 = p == 0 ? left1 : src[0][0].y, l1 = src[0][p].x;
+          P dv = mk2(l0 - src[0][p].x, l1 - src[0][p].y);
+          dv = add2(dv, sub2(up[p], src[1][p]));
+          dv = add2(dv, sub2(f3p[p], src[2][p]));
+          const P de = mul2(dv, iec[p]);
+          av[p] = fma2(nreg2, de, vv[p]);
 #pragma unroll
-          for (int c = 0; c < R; ++c) fa[V::RHS + c] += uc[c][v] * (diag ? de : dv);
+          for (int c = 0; c < R; ++c) fa[V::RHS + c] = fma2(uc[c][p], diag ? de : dv, fa[V::RHS + c]);
         }
-        Vec4<T>::st(Aout + j, av);
+        st2(Aout + j, av);
       }
-      T l[4], h[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) l[v] = lo_s, h[v] = hi_s;
+      P l[2] = {bc2(lo_s), bc2(lo_s)}, h[2] = {bc2(hi_s), bc2(hi_s)};
       if (real) {
-        if (MODE == 0 && A.lo_arr) Vec4<T>::ro(A.lo_arr + j, l);
-        if (MODE == 0 && A.hi_arr) Vec4<T>::ro(A.hi_arr + j, h);
+        if (MODE == 0 && A.lo_arr) ld2(A.lo_arr + j, l);
+        if (MODE == 0 && A.hi_arr) ld2(A.hi_arr + j, h);
       }
       bool nrv[4] = {false, false, false, false};
       bool any = false;
-      auto classify = [&](auto hinf_tag) {
-        constexpr bool HI = decltype(hinf_tag)::value;
+      if (R > 0) {
+        auto classify = [&](auto hinf_tag) {
+          constexpr bool HI = decltype(hinf_tag)::value;
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          if (real && R > 0) {
-            T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
+          for (int p = 0; p < 2; ++p) {
+            P sv[RR];
 #pragma unroll
-            for (int c = 0; c < R; ++c) {
-              uv[c] = uc[c][v];
-              sv[c] = sg * uv[c] * iec[v];
-            }
-            nrv[v] = aggregate<T, R, NACC, T, HI>(av[v], sv, uv, l[v], h[v], sh.gc, sh.gwid, fa);
-            any |= nrv[v];
+            for (int c = 0; c < R; ++c) sv[c] = mul2(mul2(uc[c][p], iec[p]), bc2(sg));
+            bool n0, n1;
+            aggregate2<T, R, NACC, HI>(av[p], sv, uc, p, l[p], h[p], gcv, gwv, fa, n0, n1);
+            // lanes off the grid hold zeros (no contribution) but must not list
+            nrv[2 * p] = n0 && real, nrv[2 * p + 1] = n1 && real;
+            any |= nrv[2 * p] | nrv[2 * p + 1];
           }
-        }
-      };
-      if (hinf) classify(std::true_type{});
-      else classify(std::false_type{});
+        };
+        if (hinf) classify(std::true_type{});
+        else classify(std::false_type{});
+      }
       if (__any_sync(FULLM, any)) {  // near voxels are rare: one vote per step
 #pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          T sv[R > 0 ? R : 1], uv[R > 0 ? R : 1];
+        for (int e = 0; e < 4; ++e) {
+          T sv[RR], uv[RR];
 #pragma unroll
-          for (int c = 0; c < (R > 0 ? R : 1); ++c) {
-            uv[c] = (R > 0) ? uc[c][v] : (T)0;
-            sv[c] = sg * uv[c] * iec[v];
+          for (int c = 0; c < RR; ++c) {
+            uv[c] = (R > 0) ? el(uc[c], e) : (T)0;
+            sv[c] = sg * uv[c] * el(iec, e);
           }
-          near_push<T, R>(nrv[v], av[v], l[v], h[v], uv, sv, lane, near_seg, ncnt, ovf, A.capw);
+          near_push<T, R>(nrv[e], el(av, e), el(l, e), el(h, e), uv, sv, lane, near_seg, ncnt, ovf, A.capw);
         }
       }
     }
@@ -1040,30 +1085,30 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
 #pragma unroll
       for (int q = 0; q < NSUM; ++q) {
         const int src_q = q < V::COUT ? q : V::NRM + (q - V::COUT);
-        double t = (double)fa[src_q];
+        double t = (double)fa[src_q].x + (double)fa[src_q].y;
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULLM, t, o);
         if (lane == 0) s_wacc[warp][q] += t;
-        fa[src_q] = 0;
+        fa[src_q] = bc2((T)0);
       }
     }
     // ---- carries -------------------------------------------------------
 #pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      f3prev[v] = src[2][v];
-      qc[v] = qn4[v];
-      iec[v] = ien[v];
+    for (int p = 0; p < 2; ++p) {
+      f3p[p] = src[2][p];
+      qc[p] = qn[p];
+      iec[p] = ien[p];
 #pragma unroll
-      for (int c = 0; c < (R > 0 ? R : 1); ++c) uc[c][v] = un[c][v];
+      for (int c = 0; c < RR; ++c) uc[c][p] = un[c][p];
     }
     cons.advance();
     ++s;
   }
   // only the classes the steps accumulate (Cout, OVF and NCNT are untouched)
 #pragma unroll
-  for (int q = 0; q < V::COUT; ++q) acc[q] += (double)fa[q];
-  acc[V::NRM] += (double)fa[V::NRM];
-  acc[V::NRM + 1] += (double)fa[V::NRM + 1];
+  for (int q = 0; q < V::COUT; ++q) acc[q] += (double)fa[q].x + (double)fa[q].y;
+  acc[V::NRM] += (double)fa[V::NRM].x + (double)fa[V::NRM].y;
+  acc[V::NRM + 1] += (double)fa[V::NRM + 1].x + (double)fa[V::NRM + 1].y;
   if (sizeof(T) == 4 && lane == 0) {  // s_wacc[warp] is written by this lane only
 #pragma unroll
     for (int q = 0; q < NSUM; ++q) acc[q < V::COUT ? q : V::NRM + (q - V::COUT)] += s_wacc[warp][q];
@@ -1227,8 +1272,14 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         A.trace[320 + 10] = (unsigned long long)(pre + 100 * s_pre[0]);
       }
 #endif
-      fused_staged<T, R, NACC, 0, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
-                                      s_empty, uses, acc, my_seg, ncnt, ovf, pre);
+      // scalar box bounds (the usual case): compile-time stage layout, the
+      // bounds are pass constants; bound arrays take the generic variant
+      if (A.lo_arr == nullptr && A.hi_arr == nullptr)
+        fused_staged<T, R, NACC, 1, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
+                                        s_empty, uses, acc, my_seg, ncnt, ovf, pre);
+      else
+        fused_staged<T, R, NACC, 0, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
+                                        s_empty, uses, acc, my_seg, ncnt, ovf, pre);
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
       my_cnt = ncnt;
