@@ -128,6 +128,21 @@ __device__ __forceinline__ void st2(double* p, const double2 (&o)[2]) {
   reinterpret_cast<double2*>(p)[0] = o[0];
   reinterpret_cast<double2*>(p)[1] = o[1];
 }
+// pass accumulators: a pair (packed multiply-add, folded at flush time) or a
+// scalar that takes both products of the pair at once (x first, then y)
+__device__ __forceinline__ void accf(float2& a, float2 x, float2 y) { a = fma2(x, y, a); }
+__device__ __forceinline__ void accf(double2& a, double2 x, double2 y) { a = fma2(x, y, a); }
+__device__ __forceinline__ void accf(float& a, float2 x, float2 y) { a = fmaf(x.y, y.y, fmaf(x.x, y.x, a)); }
+__device__ __forceinline__ void accf(double& a, double2 x, double2 y) { a = fma(x.y, y.y, fma(x.x, y.x, a)); }
+__device__ __forceinline__ void acc_zero(float2& a) { a = make_float2(0.f, 0.f); }
+__device__ __forceinline__ void acc_zero(double2& a) { a = make_double2(0.0, 0.0); }
+__device__ __forceinline__ void acc_zero(float& a) { a = 0.f; }
+__device__ __forceinline__ void acc_zero(double& a) { a = 0.0; }
+__device__ __forceinline__ double acc_fold(float2 a) { return (double)a.x + (double)a.y; }
+__device__ __forceinline__ double acc_fold(double2 a) { return a.x + a.y; }
+__device__ __forceinline__ double acc_fold(float a) { return (double)a; }
+__device__ __forceinline__ double acc_fold(double a) { return a; }
+
 // dual-ball projection of two voxels' (w0, w1, w2) given ss = ||w||^2 per voxel
 __device__ __forceinline__ void ball2(float2 (&w)[3], float2 ss) {
   const float2 s = make_float2(ball_scale(ss.x), ball_scale(ss.y));

@@ -23,6 +23,9 @@ bool fused_eligible(const bq_wtv_desc& D) {
   if (D.ndim != 3) return false;
   if (!((K1 >= 4 && K1 <= 128 && K1 % 4 == 0 && 128 % K1 == 0) || K1 == 256)) return false;
   if (!D.p2 || !D.a2 || !D.pb || !D.p) return false;
+  // scalar box bounds only (the stage layout and the bounds are pass
+  // constants); per-voxel bound arrays take the general kernel
+  if (D.lo_arr || D.hi_arr) return false;
   const void* ptrs[] = {D.p, D.pb, D.p2, D.a, D.a2, D.v, D.x, D.d, D.U, D.lo_arr, D.hi_arr};
   for (const void* q : ptrs)
     if (!al16(q)) return false;

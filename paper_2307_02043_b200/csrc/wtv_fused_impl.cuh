@@ -291,11 +291,11 @@ __device__ __forceinline__ bool aggregate(T av, const T (&s)[R > 0 ? R : 1], con
 // aggregate() for a voxel pair (packed f32x2 where the arithmetic allows):
 // the same classification and sums, element by element; u is the lane's
 // [RR][2] pair array, p selects the pair.
-template <typename T, int R, int NACC, bool HINF>
+template <typename T, int R, int NACC, bool HINF, typename AccT>
 __device__ __forceinline__ void aggregate2(pair_t<T> av, const pair_t<T> (&s)[R > 0 ? R : 1],
                                            const pair_t<T> (&u)[R > 0 ? R : 1][2], int p, pair_t<T> l,
                                            pair_t<T> h, const T* gc, const T* gwid,
-                                           pair_t<T> (&acc)[NACC], bool& n0, bool& n1) {
+                                           AccT (&acc)[NACC], bool& n0, bool& n1) {
   using V = FV<R>;
   using P = pair_t<T>;
   P zc = av, rho = bc2((T)0);
@@ -330,8 +330,8 @@ __device__ __forceinline__ void aggregate2(pair_t<T> av, const pair_t<T> (&s)[R 
     const P uu = u[c][p];
     const P ui = mk2(in[0] ? uu.x : (T)0, in[1] ? uu.y : (T)0);
 #pragma unroll
-    for (int c2 = 0; c2 <= c; ++c2, ++k) acc[V::CIN + k] = fma2(ui, s[c2], acc[V::CIN + k]);
-    acc[V::K0 + c] = fma2(uu, k0, acc[V::K0 + c]);
+    for (int c2 = 0; c2 <= c; ++c2, ++k) accf(acc[V::CIN + k], ui, s[c2]);
+    accf(acc[V::K0 + c], uu, k0);
   }
   n0 = nr[0], n1 = nr[1];
 }
@@ -858,9 +858,12 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   constexpr int NSUM = V::COUT + 2;  // [0, COUT) and the two norms
   constexpr int FLUSH = sizeof(T) == 4 ? 32 : (1 << 30);
   __shared__ double s_wacc[16][sizeof(T) == 4 ? NSUM : 1];
-  P fa[NACC];
+  // pair accumulators at ranks <= 2; higher ranks fold each pair into a scalar
+  // accumulator at once (their 2R + R(R+1)/2 classes would not fit as pairs)
+  using AccT = typename std::conditional<(sizeof(T) == 4 && R <= 2), P, T>::type;
+  AccT fa[NACC];
 #pragma unroll
-  for (int q = 0; q < NACC; ++q) fa[q] = bc2((T)0);
+  for (int q = 0; q < NACC; ++q) acc_zero(fa[q]);
   if (sizeof(T) == 4)
     for (int q = lane; q < NSUM; q += 32) s_wacc[warp][q] = 0.0;
   P qc[2] = {bc2((T)0), bc2((T)0)}, iec[2] = {bc2((T)1), bc2((T)1)}, uc[RR][2];
@@ -872,9 +875,14 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   // sign * gamma so that q = clamp(a + (u / d) sgz) (the sign is exact)
   const P m_src2 = bc2(div_p ? (T)0 : m_cur), m_prev2 = bc2(m_prev), step2 = bc2(step);
   const P nreg2 = bc2(sh.single ? (T)0 : -reg);
-  T sgz[RR], gcv[RR], gwv[RR];
+  // ranks <= 2 keep the shift and box in registers, higher ranks read them
+  // from shared memory at use (register budget)
+  constexpr int RH = R <= 2 ? RR : 1;
+  T sgz[RH], gcv[RH], gwv[RH];
 #pragma unroll
-  for (int c = 0; c < RR; ++c) sgz[c] = R > 0 ? sg * sh.gz[c] : (T)0, gcv[c] = sh.gc[c], gwv[c] = sh.gwid[c];
+  for (int c = 0; c < RH; ++c) sgz[c] = R > 0 ? sg * sh.gz[c] : (T)0, gcv[c] = sh.gc[c], gwv[c] = sh.gwid[c];
+  const T* const gcp = R <= 2 ? gcv : sh.gc;
+  const T* const gwp = R <= 2 ? gwv : sh.gwid;
   int s = 0;
   while (cons.valid) {
     const int b = s & 1;
@@ -923,7 +931,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         for (int p = 0; p < 2; ++p) {
           P z = q[p];
 #pragma unroll
-          for (int c = 0; c < R; ++c) z = fma2(mul2(u[c][p], ie[p]), bc2(sgz[c]), z);
+          for (int c = 0; c < R; ++c) z = fma2(mul2(u[c][p], ie[p]), bc2(R <= 2 ? sgz[c < RH ? c : 0] : sg * sh.gz[c]), z);
           q[p] = mk2(clampv(z.x, l[p].x, h[p].x), clampv(z.y, l[p].y, h[p].y));
         }
       };
@@ -987,8 +995,8 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         for (int n = 0; n < 3; ++n) {
           const P df = sub2(w[n], pc[n][p]);
           if (acc_n) {
-            fa[V::NRM] = fma2(df, df, fa[V::NRM]);
-            fa[V::NRM + 1] = fma2(pc[n][p], pc[n][p], fa[V::NRM + 1]);
+            accf(fa[V::NRM], df, df);
+            accf(fa[V::NRM + 1], pc[n][p], pc[n][p]);
           }
           src[n][p] = fma2(m_src2, df, w[n]);
           pc[n][p] = w[n];  // p_i (stored below)
@@ -1039,7 +1047,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
           const P de = mul2(dv, iec[p]);
           av[p] = fma2(nreg2, de, vv[p]);
 #pragma unroll
-          for (int c = 0; c < R; ++c) fa[V::RHS + c] = fma2(uc[c][p], diag ? de : dv, fa[V::RHS + c]);
+          for (int c = 0; c < R; ++c) accf(fa[V::RHS + c], uc[c][p], diag ? de : dv);
         }
         st2(Aout + j, av);
       }
@@ -1055,11 +1063,28 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
           constexpr bool HI = decltype(hinf_tag)::value;
 #pragma unroll
           for (int p = 0; p < 2; ++p) {
-            P sv[RR];
-#pragma unroll
-            for (int c = 0; c < R; ++c) sv[c] = mul2(mul2(uc[c][p], iec[p]), bc2(sg));
             bool n0, n1;
-            aggregate2<T, R, NACC, HI>(av[p], sv, uc, p, l[p], h[p], gcv, gwv, fa, n0, n1);
+            if constexpr (std::is_same<AccT, P>::value) {
+              P sv[RR];
+#pragma unroll
+              for (int c = 0; c < R; ++c) sv[c] = mul2(mul2(uc[c][p], iec[p]), bc2(sg));
+              aggregate2<T, R, NACC, HI, AccT>(av[p], sv, uc, p, l[p], h[p], gcp, gwp, fa, n0, n1);
+            } else {
+              // higher ranks: voxel by voxel (fewer live registers)
+#pragma unroll
+              for (int e = 0; e < 2; ++e) {
+                T sv[RR], uv[RR];
+#pragma unroll
+                for (int c = 0; c < RR; ++c) {
+                  uv[c] = e ? uc[c][p].y : uc[c][p].x;
+                  sv[c] = sg * uv[c] * (e ? iec[p].y : iec[p].x);
+                }
+                const bool nr = aggregate<T, R, NACC, AccT, HI>(e ? av[p].y : av[p].x, sv, uv, e ? l[p].y : l[p].x,
+                                                                e ? h[p].y : h[p].x, gcp, gwp, fa);
+                if (e) n1 = nr;
+                else n0 = nr;
+              }
+            }
             // lanes off the grid hold zeros (no contribution) but must not list
             nrv[2 * p] = n0 && real, nrv[2 * p + 1] = n1 && real;
             any |= nrv[2 * p] | nrv[2 * p + 1];
@@ -1085,11 +1110,11 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
 #pragma unroll
       for (int q = 0; q < NSUM; ++q) {
         const int src_q = q < V::COUT ? q : V::NRM + (q - V::COUT);
-        double t = (double)fa[src_q].x + (double)fa[src_q].y;
+        double t = acc_fold(fa[src_q]);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(FULLM, t, o);
         if (lane == 0) s_wacc[warp][q] += t;
-        fa[src_q] = bc2((T)0);
+        acc_zero(fa[src_q]);
       }
     }
     // ---- carries -------------------------------------------------------
@@ -1106,9 +1131,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   }
   // only the classes the steps accumulate (Cout, OVF and NCNT are untouched)
 #pragma unroll
-  for (int q = 0; q < V::COUT; ++q) acc[q] += (double)fa[q].x + (double)fa[q].y;
-  acc[V::NRM] += (double)fa[V::NRM].x + (double)fa[V::NRM].y;
-  acc[V::NRM + 1] += (double)fa[V::NRM + 1].x + (double)fa[V::NRM + 1].y;
+  for (int q = 0; q < V::COUT; ++q) acc[q] += acc_fold(fa[q]);
+  acc[V::NRM] += acc_fold(fa[V::NRM]);
+  acc[V::NRM + 1] += acc_fold(fa[V::NRM + 1]);
   if (sizeof(T) == 4 && lane == 0) {  // s_wacc[warp] is written by this lane only
 #pragma unroll
     for (int q = 0; q < NSUM; ++q) acc[q < V::COUT ? q : V::NRM + (q - V::COUT)] += s_wacc[warp][q];
@@ -1272,14 +1297,10 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         A.trace[320 + 10] = (unsigned long long)(pre + 100 * s_pre[0]);
       }
 #endif
-      // scalar box bounds (the usual case): compile-time stage layout, the
-      // bounds are pass constants; bound arrays take the generic variant
-      if (A.lo_arr == nullptr && A.hi_arr == nullptr)
-        fused_staged<T, R, NACC, 1, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
-                                        s_empty, uses, acc, my_seg, ncnt, ovf, pre);
-      else
-        fused_staged<T, R, NACC, 0, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
-                                        s_empty, uses, acc, my_seg, ncnt, ovf, pre);
+      // scalar box bounds (fused_eligible): compile-time stage layout, the
+      // bounds are pass constants
+      fused_staged<T, R, NACC, 1, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
+                                      s_empty, uses, acc, my_seg, ncnt, ovf, pre);
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
       my_cnt = ncnt;

@@ -105,6 +105,24 @@ def test_diag_prox_f64_vs_oracle(dims, r, iso):
     assert rep.newton_iterations == ref["newton_iterations"]
 
 
+@pytest.mark.parametrize("dims,r", [((32, 16, 12), 1), ((20, 18, 16), 2)])
+def test_array_bounds_prox_f64_vs_oracle(dims, r):
+    """Per-voxel box bounds (BoxSet with arrays, wpm.py:109-142): the general
+    kernel serves them (the fused kernel takes scalar bounds only)."""
+    d, u, v = _diag_problem(5, dims, r)
+    rng = np.random.default_rng(6)
+    n = int(np.prod(dims))
+    lo = rng.uniform(-0.2, 0.1, n)
+    hi = lo + rng.uniform(0.2, 1.0, n)
+    prob = D.DualTvProblem(grid=bq.Grid(dims), v=v, w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05,
+                           box=W.BoxSet(lo, hi))
+    rep = D.solve(prob, eps=1e-300, max_iter=40)
+    ref = O.fgp_prox(dims, v, O.Metric(U=u, d=d), reg=0.05, lo=lo, hi=hi, eps=1e-300, max_iter=40)
+    assert rel_l2(rep.x, ref["x"]) <= F64_TOL
+    assert rel_l2(rep.p_star, ref["p_star"]) <= F64_TOL
+    assert np.all(rep.x >= lo) and np.all(rep.x <= hi)
+
+
 def test_xsplit_rows_f32_vs_oracle():
     """K1 = 256 (x-split rows) in fp32 at a size with several row tiles and z segments."""
     d, u, v = _diag_problem(11, (256, 40, 24), 1)
