@@ -121,6 +121,15 @@ __device__ __forceinline__ void ld2(const double* p, double2 (&o)[2]) {
   o[0] = reinterpret_cast<const double2*>(p)[0];
   o[1] = reinterpret_cast<const double2*>(p)[1];
 }
+// read-only for the kernel's lifetime (non-coherent path)
+__device__ __forceinline__ void ld2ro(const float* p, float2 (&o)[2]) {
+  const float4 v = __ldg(reinterpret_cast<const float4*>(p));
+  o[0] = make_float2(v.x, v.y), o[1] = make_float2(v.z, v.w);
+}
+__device__ __forceinline__ void ld2ro(const double* p, double2 (&o)[2]) {
+  o[0] = __ldg(reinterpret_cast<const double2*>(p));
+  o[1] = __ldg(reinterpret_cast<const double2*>(p) + 1);
+}
 __device__ __forceinline__ void st2(float* p, const float2 (&o)[2]) {
   *reinterpret_cast<float4*>(p) = make_float4(o[0].x, o[0].y, o[1].x, o[1].y);
 }

@@ -97,7 +97,18 @@ struct FCtl {
   int phase_cnt[8];
 };
 
-constexpr int NSTAGE = 2;      // depth of the bulk-copy pipeline (measured best)
+constexpr int NSTAGE = 3;      // max depth of the bulk-copy pipeline (3 where the stages fit, else 2)
+
+// per-slot use counters of the stage ring, kept in registers (runtime slot
+// index -> selects, not a local-memory array)
+struct Uses {
+  unsigned u0, u1, u2;
+  __device__ unsigned get(int b) const { return b == 0 ? u0 : (b == 1 ? u1 : u2); }
+  __device__ void inc(int b) {
+    u0 += b == 0, u1 += b == 1, u2 += b == 2;
+  }
+};
+__device__ __forceinline__ int ring_next(int b, int ns) { return b + 1 == ns ? 0 : b + 1; }
 
 struct StageGeo {
   int W, SRW, nstage;           // warps used, staged rows, pipeline depth (<= NSTAGE)
@@ -767,7 +778,7 @@ template <typename T, int R, int NACC, int MODE, int KX>
 __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>& sh, const StageGeo& g,
                                              long long seg_begin, long long seg_end, T* dyn,
                                              unsigned long long* full, unsigned long long* empty,
-                                             unsigned (&uses)[NSTAGE], double (&acc)[NACC], T* near_seg,
+                                             Uses& uses, double (&acc)[NACC], T* near_seg,
                                              int& ncnt, bool& ovf, int pre) {
   using V = FV<R>;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -818,30 +829,28 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     fence_proxy_async_global();  // this pass reads data written before the grid barrier
     StepIter prod;
     prod.init(seg_begin, seg_end, K3, nd);
-    unsigned pu0 = uses[0], pu1 = uses[1];  // include the fills of the prefetched steps
-    int ps = 0;
-    for (; ps < pre && prod.valid; ++ps) prod.advance();
+    Uses pu = uses;  // includes the fills of the prefetched steps
+    int ps = 0, b = 0;
+    for (; ps < pre && prod.valid; ++ps) prod.advance(), b = ring_next(b, NS);
     while (prod.valid) {
-      const int b = ps & 1;
-      if (ps >= 2) mbar_wait(&empty[b], ((b ? pu1 : pu0) - 1) & 1u);  // consumers released it
+      if (ps >= NS) mbar_wait(&empty[b], (pu.get(b) - 1) & 1u);  // consumers released it
       issue_step<T, R>(A, prod, M, g, dyn + b * g.stage_elems, &full[b], Pc, Pp, Ain, lane);
-      if (b) ++pu1;
-      else ++pu0;
+      pu.inc(b);
       prod.advance();
       ++ps;
+      b = ring_next(b, NS);
     }
-    uses[0] = pu0, uses[1] = pu1;  // in step with the consumers
+    uses = pu;  // in step with the consumers
     return;
   }
   if (warp > W) {
     StepIter cnt;
     cnt.init(seg_begin, seg_end, K3, nd);
-    int ps = 0;
+    int b = 0;
     while (cnt.valid) {
-      if (ps & 1) uses[1] += 1;
-      else uses[0] += 1;
+      uses.inc(b);
       cnt.advance();
-      ++ps;
+      b = ring_next(b, NS);
     }
     return;
   }
@@ -883,9 +892,8 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   for (int c = 0; c < RH; ++c) sgz[c] = R > 0 ? sg * sh.gz[c] : (T)0, gcv[c] = sh.gc[c], gwv[c] = sh.gwid[c];
   const T* const gcp = R <= 2 ? gcv : sh.gc;
   const T* const gwp = R <= 2 ? gwv : sh.gwid;
-  int s = 0;
+  int s = 0, b = 0;
   while (cons.valid) {
-    const int b = s & 1;
     T* const stg = dyn + b * g.stage_elems;
     unsigned long long t_a = 0, t_b = 0;
 #if BQ_PROX_TRACE
@@ -894,13 +902,12 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     constexpr bool tr = false;
 #endif
     if (tr) t_a = global_ns();
-    mbar_wait(&full[b], (b ? uses[1] : uses[0]) & 1u);
+    mbar_wait(&full[b], uses.get(b) & 1u);
 #if BQ_PROX_TRACE
     if (s == 0 && blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 7] = global_ns();
 #endif
     if (tr) t_b = global_ns();
-    if (b) uses[1] += 1;
-    else uses[0] += 1;
+    uses.inc(b);
     const int k = cons.k;
     const int y0 = (int)cons.tile * TYe;
     const int y = y0 - rpw + sr;
@@ -1128,6 +1135,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
     cons.advance();
     ++s;
+    b = ring_next(b, NS);
   }
   // only the classes the steps accumulate (Cout, OVF and NCNT are untouched)
 #pragma unroll
@@ -1190,7 +1198,8 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   __shared__ int s_pre[4];  // prefetched steps of the next FUSED pass: count, slot_cur, slot_prev, a_cur
   if (threadIdx.x == 0) s_pre[0] = 0;
   __syncthreads();
-  unsigned uses[NSTAGE] = {0u, 0u};
+  Uses uses{0u, 0u, 0u};
+  const int NS = A.geo.nstage;
   const int PW = A.geo.W;  // producer warp of the staged pass
   // Consume prefetched stages that will not be used (the next pass is not the
   // predicted FUSED pass, or the smem is needed): keeps the mbarrier phase
@@ -1201,14 +1210,13 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   auto csync = [&]() { named_sync(2, NC); };
   auto drain_impl = [&](bool consumers_only) {
     const int n = s_pre[0];
-    for (int i = 0; i < n; ++i) {
-      const int b = i & 1;
+    for (int b = 0; b < n; ++b) {  // n <= NS: the prefetched steps fill slots 0 .. n-1
       if (warp != PW) {
         if (threadIdx.x == 0) {
-          mbar_wait(&s_full[b], uses[b] & 1u);
+          mbar_wait(&s_full[b], uses.get(b) & 1u);
           mbar_arrive(&s_empty[b]);
         }
-        uses[b] += 1;
+        uses.inc(b);
       }
     }
     if (consumers_only) csync();
@@ -1610,7 +1618,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         StepIter it;
         it.init(seg_begin_s, seg_end_s, K3, 3);
         int n = 0;
-        while (it.valid && n < NSTAGE) {
+        while (it.valid && n < NS) {
           it.advance();
           ++n;
         }
@@ -1648,11 +1656,10 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         fence_proxy_async_global();  // reads data written before the grid barrier
         StepIter it;
         it.init(seg_begin_s, seg_end_s, K3, 3);
-        for (int n = 0; n < s_pre[0]; ++n) {
-          const int b = n & 1;
+        for (int b = 0; b < s_pre[0]; ++b) {
           issue_step<T, R>(A, it, M, A.geo, reinterpret_cast<T*>(s_dyn) + b * A.geo.stage_elems, &s_full[b],
                            A.ring[s_pre[1]], A.ring[s_pre[2]], A.abuf[s_pre[3]], lane);
-          uses[b] += 1;
+          uses.inc(b);
           it.advance();
         }
       }
@@ -1971,11 +1978,18 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   // staged FUSED pass: widest tile whose double-buffered stage fits in smem
   StageMap<R> M;
   M.make(D.d != nullptr, D.lo_arr != nullptr, D.hi_arr != nullptr, D.ndim, true);
-  const size_t smem_cap = 200 * 1024;
+  int optin = 0, static_b = 0;
+  BQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
+  {
+    cudaFuncAttributes fa{};
+    BQ_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));
+    static_b = (int)fa.sharedSizeBytes;
+  }
+  const size_t smem_cap = std::min<size_t>(200 * 1024, (size_t)std::max(0, optin - static_b - 3072));
   int W = NT / 32 - 1;  // + 1 producer warp
   W -= W % A.wpr;       // whole row groups
   const char* ns_env = getenv("BQ_PROX_STAGES");
-  const int nst = ns_env ? std::max(2, std::min(NSTAGE, atoi(ns_env))) : 2;
+  int nst = ns_env ? std::max(2, std::min(NSTAGE, atoi(ns_env))) : NSTAGE;
   auto staged_bytes = [&](int w) {
     const long long srw = (long long)(w / A.wpr) * A.rpw + 1;
     return (size_t)(nst * M.nfield + 4) * srw * A.K1 * sizeof(T);
@@ -1983,6 +1997,14 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   const char* w_env = getenv("BQ_PROX_WARPS");
   if (w_env) W = std::max(2, std::min(W, atoi(w_env)));
   W -= W % A.wpr;
+  // a 3-deep ring where it costs at most one warp of tile width, for rows of
+  // <= 128 voxels and ranks <= 2 (measured at 128^3: 3.29 -> 3.14 ms at rank
+  // 1; x-split rows and rank 4 are faster with the wider 2-deep tile)
+  if (!ns_env) {
+    int w3 = W;
+    while (w3 > 2 * A.wpr && staged_bytes(w3) > smem_cap) w3 -= A.wpr;
+    if (!(A.K1 <= 128 && R <= 2 && w3 >= W - 1)) nst = 2;
+  }
   while (W > 2 * A.wpr && staged_bytes(W) > smem_cap) W -= A.wpr;
   BQ_CHECK(staged_bytes(W) <= smem_cap, BQ_EINVAL, "wtv_fused: stage does not fit in shared memory");
   A.geo.W = W;
@@ -1992,13 +2014,6 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.geo.stage_elems = (long long)M.nfield * A.geo.slot_elems;
   const size_t base_dyn = std::max<size_t>(2ull * ((RW + 1) / A.wpr) * A.rpw * A.K1 * sizeof(T), staged_bytes(W));
   // near-list region after the stages (so the next pass's prefetched stages survive the on-chip Newton)
-  int optin = 0, static_b = 0;
-  BQ_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, ctx->device));
-  {
-    cudaFuncAttributes fa{};
-    BQ_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));
-    static_b = (int)fa.sharedSizeBytes;
-  }
   const long long room = (long long)optin - static_b - (long long)base_dyn - 2048;
   const size_t list_bytes = room > 0 ? (size_t)(room / 16 * 16) : 0;
   const size_t dyn = base_dyn + list_bytes;
