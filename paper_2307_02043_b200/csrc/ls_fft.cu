@@ -66,6 +66,27 @@ __device__ __forceinline__ V cmul(V a, V b) {
   return r;
 }
 
+// complex64 on sm_100's packed fp32x2 pipe: an add is one FADD2, a product
+// two instructions (FMUL2 of the rotated operand (-a.y, a.x) by b.y -- the
+// rotation folds into the operand's swap/negate modifiers -- then FFMA2 by
+// b.x), against 2 and 4 scalar instructions.
+__device__ __forceinline__ float2 rot90(float2 a) { return make_float2(-a.y, a.x); }  // i a
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return __fadd2_rn(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return __fadd2_rn(a, make_float2(-b.x, -b.y)); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {
+  return __ffma2_rn(a, make_float2(b.x, b.x), __fmul2_rn(rot90(a), make_float2(b.y, b.y)));
+}
+// a * (c + i s) for scalar c, s
+__device__ __forceinline__ float2 cmul_cs(float2 a, float c, float s) {
+  return __ffma2_rn(a, make_float2(c, c), __fmul2_rn(rot90(a), make_float2(s, s)));
+}
+__device__ __forceinline__ double2 cmul_cs(double2 a, double c, double s) {
+  double2 r;
+  r.x = a.x * c - a.y * s;
+  r.y = a.x * s + a.y * c;
+  return r;
+}
+
 // a * exp(DIR 2 pi i k / 32); k is a compile-time constant after unrolling
 template <int DIR, typename V>
 __device__ __forceinline__ V tw32(V a, int k) {
@@ -89,9 +110,7 @@ __device__ __forceinline__ V tw32(V a, int k) {
     return r;
   }
   const T c = (T)cos32(k), s = (T)(DIR > 0 ? sin32(k) : -sin32(k));
-  r.x = a.x * c - a.y * s;
-  r.y = a.x * s + a.y * c;
-  return r;
+  return cmul_cs(a, c, s);
 }
 
 template <int R>
