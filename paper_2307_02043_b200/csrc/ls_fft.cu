@@ -80,12 +80,28 @@ __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
 __device__ __forceinline__ float2 cmul_cs(float2 a, float c, float s) {
   return __ffma2_rn(a, make_float2(c, c), __fmul2_rn(rot90(a), make_float2(s, s)));
 }
-__device__ __forceinline__ double2 cmul_cs(double2 a, double c, double s) {
-  double2 r;
+template <typename V, typename T>
+__device__ __forceinline__ V cmul_cs(V a, T c, T s) {
+  V r;
   r.x = a.x * c - a.y * s;
   r.y = a.x * s + a.y * c;
   return r;
 }
+// complex64 held as two scalars (scalar FADD/FMUL/FFMA arithmetic): the ZC pass
+// keeps it -- its in-register z-transform pair needs more live values than the
+// packed code's register pairs allow at its occupancy (measured: packed ZC is
+// 12-16% slower at m = 256 / 512)
+struct __align__(8) F2S {
+  float x, y;
+};
+template <typename T>
+struct CVS {
+  using V = typename CV<T>::V;
+};
+template <>
+struct CVS<float> {
+  using V = F2S;
+};
 
 // a * exp(DIR 2 pi i k / 32); k is a compile-time constant after unrolling
 template <int DIR, typename V>
@@ -364,8 +380,9 @@ constexpr int zc_smem_elems(int n) {
 template <typename T, int R1, int R2, int C, int L, bool STD>
 __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi, int zo0, int nzo, int adj,
                                                   const typename CV<T>::V* __restrict__ khat,
-                                                  typename CV<T>::V* __restrict__ q, const int* __restrict__ active) {
-  using V = typename CV<T>::V;
+                                                  typename CV<T>::V* __restrict__ q_, const int* __restrict__ active) {
+  using V = typename CVS<T>::V;
+  V* __restrict__ q = reinterpret_cast<V*>(q_);
   constexpr int M = R1 * R2, XT = M / L, NT = C * L;
   extern __shared__ __align__(16) unsigned char smraw[];
   V* tw = (V*)smraw;
@@ -377,7 +394,7 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
   const long long vstride = (long long)n * zs;  // one view's Q
   const int fy = y <= n ? y : M - y;
   {
-    const V* kb = khat + (long long)fy * M;
+    const V* kb = reinterpret_cast<const V*>(khat) + (long long)fy * M;
     const int nk = (n + 1) * L;
     for (int i = tid; i < nk; i += NT) {
       const int fz = i / L, xx = xc * L + i % L;
