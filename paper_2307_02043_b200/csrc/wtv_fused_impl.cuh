@@ -1638,7 +1638,12 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       if (blockIdx.x == 0 && warp == NT / 32 - 1) {  // latest arrival (phase timeline of the report)
         const long long* col = reinterpret_cast<const long long*>(PT + (size_t)(kMaxVals - 1) * PB);
         long long t = 0;
-        for (unsigned b = lane; b < gridDim.x; b += 32) t = max(t, __ldcg(&col[b]));
+        for (unsigned b = lane; b < gridDim.x; b += 32) {
+          t = max(t, __ldcg(&col[b]));
+#if BQ_PROX_TRACE
+          if (cur == F_FUSED && tr3_on && b < 2048) A.trace[1024 + b] = (unsigned long long)__ldcg(&col[b]);
+#endif
+        }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) t = max(t, __shfl_down_sync(FULLM, t, o));
         if (lane == 0) s_red[kMaxVals - 1] = __longlong_as_double(t);
