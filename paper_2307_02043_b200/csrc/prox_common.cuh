@@ -185,6 +185,24 @@ __device__ __forceinline__ bool chol(double (&a)[R > 0 ? R * R : 1]) {
   }
   return true;
 }
+// chol_solve with the reciprocal diagonal precomputed (multiplies, no divisions)
+template <int R>
+__device__ __forceinline__ void chol_solve_rd(const double* l, const double* rd, double (&b)[R > 0 ? R : 1]) {
+#pragma unroll
+  for (int i = 0; i < R; ++i) {
+    double s = b[i];
+#pragma unroll
+    for (int k = 0; k < i; ++k) s -= l[i * R + k] * b[k];
+    b[i] = s * rd[i];
+  }
+#pragma unroll
+  for (int i = R - 1; i >= 0; --i) {
+    double s = b[i];
+#pragma unroll
+    for (int k = i + 1; k < R; ++k) s -= l[k * R + i] * b[k];
+    b[i] = s * rd[i];
+  }
+}
 template <int R>
 __device__ __forceinline__ void chol_solve(const double* l, double (&b)[R > 0 ? R : 1]) {
 #pragma unroll

@@ -86,10 +86,11 @@ struct FCtl {
   int final_mode, div_p, have_hist, fallbacks;
   int slot_cur, slot_prev, a_cur, local_steps;
   int single, nl_ok, ndist, pad1;  // ndist: long near list -> distributed Newton steps
-  double t, m_prev, m_cur, rel, best_res, last_res, grow;
+  double t, t_next, m_prev, m_cur, rel, best_res, last_res, grow;
   double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
   double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK], dmax[BQ_MAX_RANK];
   double chol[BQ_MAX_RANK * BQ_MAX_RANK];
+  double chol_rdiag[BQ_MAX_RANK];  // 1 / L_ii (the per-iteration solves multiply)
   double K0[BQ_MAX_RANK], Cin[36], Cout[36];
   double gram[36];  // setup U^T D^-1 U (raw partials): sum over all voxels of u s^T = sign * gsc(gram)
   unsigned long long t_last;
@@ -151,6 +152,7 @@ struct FArgs {
   int dbg;                    // debug switches (timing experiments only)
   double grow_min;            // minimum box growth factor of the near-list Newton
   double ndist_min;           // near lists longer than this take distributed (per-block + barrier) steps
+  int pre_max;                // stages of the next FUSED pass prefetched across the barrier (<= nstage)
 };
 
 // shared, per-block copy of what the passes read
@@ -437,7 +439,7 @@ struct Ctl {
       phi[i] = phi_part[i] + c.beta[i];
       ss += phi[i] * phi[i];
     }
-    const double res = sqrt(ss);
+    const double res = R == 1 ? fabs(phi[0]) : sqrt(ss);
     if (res < c.best_res) {
       c.best_res = res;
       for (int i = 0; i < R; ++i) c.best_beta[i] = c.beta[i];
@@ -489,7 +491,7 @@ struct Ctl {
   __device__ void after_div(const double* red) {
     double coef[R > 0 ? R : 1];
     for (int i = 0; i < R; ++i) coef[i] = gsc(red[V::RHS + i]);
-    if (R > 0) chol_solve<R>(c.chol, coef);
+    if (R > 0) chol_solve_rd<R>(c.chol, c.chol_rdiag, coef);
     for (int i = 0; i < R; ++i) c.gw[i] = c.single ? 0.0 : A.reg * coef[i];
     for (int i = 0; i < R; ++i) c.K0[i] = red[V::K0 + i];
     for (int k = 0; k < V::S; ++k) c.Cin[k] = red[V::CIN + k], c.Cout[k] = A.sign * gsc(c.gram[k]) - c.Cin[k];
@@ -543,6 +545,7 @@ struct Ctl {
           return;
         }
         for (int i = 0; i < R * R; ++i) c.chol[i] = cap[i];
+        for (int i = 0; i < R; ++i) c.chol_rdiag[i] = 1.0 / cap[i * R + i];
         for (int i = 0; i < R; ++i) {
           c.beta[i] = A.beta_io ? A.beta_io[i] : 0.0;
           c.gw[i] = 0.0;
@@ -610,7 +613,7 @@ struct Ctl {
             return;
           }
         } else {
-          c.t = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c.t * c.t));
+          c.t = c.t_next;  // 0.5 (1 + sqrt(1 + 4 t^2)), computed by prepare_fused
           if (c.div_p) c.final_mode = 1;  // that was the last iteration
           else c.it += 1;
         }
@@ -650,6 +653,7 @@ struct Ctl {
   // before a FUSED pass: momentum coefficients and the div source
   __device__ void prepare_fused() {
     const double tn = 0.5 * (1.0 + sqrt(1.0 + 4.0 * c.t * c.t));
+    c.t_next = tn;
     c.m_cur = A.accelerated ? (c.t - 1.0) / tn : 0.0;
     c.div_p = (c.it >= A.max_iter) ? 1 : 0;
   }
@@ -1618,7 +1622,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         StepIter it;
         it.init(seg_begin_s, seg_end_s, K3, 3);
         int n = 0;
-        while (it.valid && n < NS) {
+        while (it.valid && n < A.pre_max) {
           it.advance();
           ++n;
         }
@@ -1670,12 +1674,17 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       }
     } else {
     // ---- controller (+ block-local Newton over the near list) ------------
+    const bool tl_side = cur != F_SETUP && cur != F_FINAL;  // (setup resets, final reports the timeline)
+    if (threadIdx.x == 32 && tl_side) {  // phase timeline: its own fields, off the controller's path
+      Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
+      ctl.timeline(cur, s_red, barrier);
+    }
     if (threadIdx.x == 0) {
       Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
 #if BQ_PROX_TRACE
       const long long c0 = clock64();
 #endif
-      ctl.timeline(cur, s_red, barrier);
+      if (!tl_side) ctl.timeline(cur, s_red, barrier);
 #if BQ_PROX_TRACE
       const long long c1 = clock64();
 #endif
@@ -1863,13 +1872,16 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
             Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
             double phi[R > 0 ? R : 1], hp[V::S > 0 ? V::S : 1];
             ctl.local_eval(nacc, phi, hp);
-            ctl.timeline(F_NLOCAL, s_red, false);
             s_c.local_steps += 1;
             ctl.newton_step(phi, hp);
             if (ntr && ntr_k < 40) A.trace[240 + ntr_k++] = global_ns();
           }
           if (big) csync();
           else __syncwarp();
+        }
+        if (threadIdx.x == 0) {  // one timeline stamp for the whole on-chip solve
+          Ctl<T, R> ctl{A, s_c, blockIdx.x == 0};
+          ctl.timeline(F_NLOCAL, s_red, false);
         }
       }
       csync();
@@ -2014,6 +2026,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   BQ_CHECK(staged_bytes(W) <= smem_cap, BQ_EINVAL, "wtv_fused: stage does not fit in shared memory");
   A.geo.W = W;
   A.geo.nstage = nst;
+  A.pre_max = getenv("BQ_PROX_PRE") ? std::max(0, std::min(nst, atoi(getenv("BQ_PROX_PRE")))) : nst;
   A.geo.SRW = (W / A.wpr) * A.rpw + 1;
   A.geo.slot_elems = (long long)A.geo.SRW * A.K1;
   A.geo.stage_elems = (long long)M.nfield * A.geo.slot_elems;
