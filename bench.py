@@ -168,9 +168,13 @@ def run_reference(args):
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded config-2 phantom)",
-        "config": {"workload": f"config2 wTV prox {args.n}^3 diag(d)+uu^T iso reg 0.05 box [0,inf)",
-                   "sample_iters_per_step": sample_iters},
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic (seeded config-2 box phantom + N(0,1) noise)",
+        # the same workload as the device arm (a voxel*iter of one 100-iteration solve);
+        # each step times a bounded sample of its FGP iterations
+        "config": {"workload": f"config2 wTV prox {args.n}^3 W=diag(d)+uu^T iso TV reg 0.05 box [0,inf), "
+                               f"100 FGP iterations per step",
+                   "sample_iters_per_step": sample_iters, "parallelism": "host cores x1 (numpy port)"},
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
