@@ -2014,13 +2014,14 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   const char* w_env = getenv("BQ_PROX_WARPS");
   if (w_env) W = std::max(2, std::min(W, atoi(w_env)));
   W -= W % A.wpr;
-  // a 3-deep ring where it costs at most one warp of tile width, for rows of
-  // <= 128 voxels and ranks <= 2 (measured at 128^3: 3.29 -> 3.14 ms at rank
-  // 1; x-split rows and rank 4 are faster with the wider 2-deep tile)
+  // a 3-deep ring for ranks <= 2 where it costs at most one warp of tile width
+  // (rows <= 128 voxels) or none (x-split rows); measured: 128^3 rank 1
+  // 3.29 -> 3.14 ms, 256^3 rank 1 scalar tau 19.6 -> 18.2 ms; the config-2
+  // law at 256^3 (one field more, narrower tile) and rank 4 are faster 2-deep
   if (!ns_env) {
     int w3 = W;
     while (w3 > 2 * A.wpr && staged_bytes(w3) > smem_cap) w3 -= A.wpr;
-    if (!(A.K1 <= 128 && R <= 2 && w3 >= W - 1)) nst = 2;
+    if (!(R <= 2 && w3 >= W - (A.K1 <= 128 ? 1 : 0))) nst = 2;
   }
   while (W > 2 * A.wpr && staged_bytes(W) > smem_cap) W -= A.wpr;
   BQ_CHECK(staged_bytes(W) <= smem_cap, BQ_EINVAL, "wtv_fused: stage does not fit in shared memory");
