@@ -136,6 +136,23 @@ def test_xsplit_rows_f32_vs_oracle():
     assert rel_l2(rep.p_star.double().cpu().numpy(), ref["p_star"]) <= F32_TOL
 
 
+@pytest.mark.parametrize("dims,r", [((128, 36, 20), 1), ((128, 30, 18), 2), ((256, 20, 16), 1), ((256, 18, 12), 2)])
+def test_scalar_tau_f32_stage_ring_vs_oracle(dims, r):
+    """fp32 BQNPM metric tau I + U U^T at ranks 1-2: the fused kernel's 3-deep
+    stage ring (K1 = 128, and K1 = 256 x-split rows where it fits)."""
+    rng = np.random.default_rng(21)
+    n = int(np.prod(dims))
+    u = rng.standard_normal((n, r)) / np.sqrt(n)
+    v = rng.standard_normal(n) + 0.5
+    ref = O.fgp_prox(dims, v, O.Metric(U=u, tau=1.25), reg=0.05, eps=1e-300, max_iter=40)
+    w = W.DiagPlusLowRank(1.25, torch.tensor(u, dtype=torch.float32, device="cuda"))
+    prob = D.DualTvProblem(grid=bq.Grid(dims), v=torch.tensor(v, dtype=torch.float32, device="cuda"), w=w,
+                           reg=0.05, box=W.BoxSet(0.0, np.inf))
+    rep = D.solve(prob, eps=1e-300, max_iter=40)
+    assert rel_l2(rep.x.double().cpu().numpy(), ref["x"]) <= F32_TOL
+    assert rel_l2(rep.p_star.double().cpu().numpy(), ref["p_star"]) <= F32_TOL
+
+
 def test_config2_shape_f32_vs_f64_and_oracle_64():
     """Config-2 law (W = diag(d) + uu^T, iso TV 0.05, box [0, inf), 100 FGP iters)
     at 64^3: fp32 and fp64 device results vs the fp64 oracle."""
