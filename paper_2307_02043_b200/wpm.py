@@ -57,13 +57,14 @@ class DiagPlusLowRank:
         self._n = int(u.shape[0])
         self.Ut = u.t().contiguous()  # (r, N) device
         self.d = None
+        self._dmin = None
+        dmin = None  # device min(d): positivity test and omega (D-6), read with the gram
         if d is not None:
             dt = to_dev(d, dtype, device)
             if dt.numel() != self._n and self._n:
                 raise ValueError("d must have one entry per voxel")
-            if not bool((dt > 0).all()):
-                raise ValueError("diagonal d must be positive")
             self.d = dt
+            dmin = dt.min().reshape(1).to(torch.float64) if dt.numel() else None
         self.gram = None
         if self.rank:
             self.gram = torch.empty(self.rank * self.rank, dtype=torch.float64, device=device)
@@ -76,7 +77,16 @@ class DiagPlusLowRank:
                 ),
                 "DiagPlusLowRank",
             )
-            g = self.gram.cpu().numpy().reshape(self.rank, self.rank)
+        # one device->host read for the d test, min(d) and the gram
+        parts = [t for t in (dmin, self.gram) if t is not None]
+        host = torch.cat(parts).cpu().numpy() if parts else np.zeros(0)
+        if dmin is not None:
+            self._dmin = float(host[0])
+            if not self._dmin > 0:  # (NaN fails too, like (d > 0).all())
+                raise ValueError("diagonal d must be positive")
+            host = host[1:]
+        if self.rank:
+            g = host.reshape(self.rank, self.rank)
             cap = np.eye(self.rank) + self.sign * (g / self.tau if self.d is None else g)
             try:
                 np.linalg.cholesky(cap)
@@ -101,7 +111,9 @@ class DiagPlusLowRank:
 
     def min_diag(self) -> float:
         """Smallest diagonal entry: the safe lower eigen-bound for omega (D-6)."""
-        return self.tau if self.d is None else float(self.d.min().item())
+        if self.d is None:
+            return self.tau
+        return self._dmin if self._dmin is not None else float(self.d.min().item())
 
     def dense(self, n=None):
         n = self.dim if n is None else n
