@@ -1,0 +1,9 @@
+# ZC register cap A/B: LS_ZC_MINB = 1 (default) vs 4 (<= 64 registers, 4 blocks per SM at m <= 256)
+BQ_LIB=paper_2307_02043_b200/lib/ab/libbq_mb4.so timeout 600 python -m pytest tests/test_ls_fft_gpu.py tests/test_physics_gpu.py -x -q 2>&1 | tail -1
+for rep in 1 2; do
+for lib in "" paper_2307_02043_b200/lib/ab/libbq_mb4.so; do
+  echo "== lib=$lib"
+  BQ_LIB=$lib timeout 300 python bench/ls_bench.py --n 128 --views 64 --batch 16 --steps 2 2>&1 | tail -1
+  BQ_LIB=$lib timeout 300 python bench/ls_bench.py --n 64 --views 32 --batch 8 --steps 3 2>&1 | tail -1
+done
+done

@@ -28,6 +28,7 @@
 // (R1' = R2, R2' = R1) needs for its own step 1, so the spectral multiply and
 // the inverse's first DFT happen without touching shared memory.
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "ls_twiddle.cuh"
@@ -372,6 +373,9 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n_rt, const typename CV<T>
 // STG: the volume-to-volume case at m <= 256 also stages the next active
 // view's column (n planes x L) into shared memory with cp.async while the
 // current view computes, so no view waits on its own global loads
+#ifndef LS_ZC_MINB
+#define LS_ZC_MINB 3  // ZC at m <= 256: minimum resident blocks per SM requested from ptxas (register cap; 2 at m = 512)
+#endif
 #ifndef LS_ZC_VG
 #define LS_ZC_VG 1  // ZC view groups per column group (grid.y); measured: 2 and 4 are no faster at m = 256 / 512
 #endif
@@ -391,7 +395,7 @@ constexpr int zc_smem_elems(int n, bool std_case = false) {
 // zero half of the input and the dropped half of the output are compile-time
 // (no bounds tests, pruned first forward / last inverse DFT stages).
 template <typename T, int R1, int R2, int C, int L, bool STD>
-__global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi, int zo0, int nzo, int adj,
+__global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_kernel(int n, int B, int z0, int nzi, int zo0, int nzo, int adj,
                                                   const typename CV<T>::V* __restrict__ khat,
                                                   typename CV<T>::V* __restrict__ q_, const int* __restrict__ active) {
   using V = typename CVS<T>::V;
@@ -484,17 +488,27 @@ __global__ void __launch_bounds__(C* L) zc_kernel(int n, int B, int z0, int nzi,
     __syncthreads();
     V c[R2 / C][R1];
     step3<R1, R2, C, L, true, -1>(c, sm, l, t);
-    // spectral multiply: c[s][k1] = X[kz], kz = k2 + R2 k1, k2 = t + C s
+    // spectral multiply: c[s][k1] = X[kz], kz = k2 + R2 k1, k2 = t + C s.
+    // Folded index (n = M/2 here): kz <= n exactly when k1 < R1/2 or kz == n,
+    // and M - kz == n at kz == n, so fz = k1 < R1/2 ? kz : M - kz -- a
+    // compile-time choice per unrolled k1 (immediate offsets from two bases);
+    // adj is block-uniform, so it selects a whole loop
+    auto kmul = [&](auto conj) {
 #pragma unroll
-    for (int s = 0; s < R2 / C; ++s)
+      for (int s = 0; s < R2 / C; ++s) {
+        const int k2 = t + C * s;
+        const V* kp = ks + k2 * L + l;            // k1 <  R1/2: fz = k2 + R2 k1
+        const V* km = ks + (M - k2) * L + l;      // k1 >= R1/2: fz = M - k2 - R2 k1
 #pragma unroll
-      for (int k1 = 0; k1 < R1; ++k1) {
-        const int kz = t + C * s + R2 * k1;
-        const int fz = kz <= n ? kz : M - kz;
-        V k = ks[fz * L + l];
-        if (adj) k.y = -k.y;
-        c[s][k1] = cmul(c[s][k1], k);
+        for (int k1 = 0; k1 < R1; ++k1) {
+          V k = k1 < R1 / 2 ? kp[R2 * k1 * L] : km[-R2 * k1 * L];
+          if (decltype(conj)::value) k.y = -k.y;
+          c[s][k1] = cmul(c[s][k1], k);
+        }
       }
+    };
+    if (adj) kmul(std::true_type{});
+    else kmul(std::false_type{});
     __syncthreads();  // step-3 reads of sm are done before it is rewritten
     // inverse with (R1', R2') = (R2, R1): c[s][n2'] = x'[n1' + R2 n2'], n1' = t + C s
     step1<R2, R1, C, L, true, 1>(c, sm, tw, l, t);
