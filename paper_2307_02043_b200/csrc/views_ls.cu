@@ -18,6 +18,7 @@
 
 #include <map>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -504,13 +505,28 @@ __global__ void bg_s_kernel(long long N, const typename Cx<T>::V* __restrict__ r
   alpha.x = (T)state[kBS * b + 2], alpha.y = (T)state[kBS * b + 3];
   const long long o = (long long)b * N;
   double nn = 0.0;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
-    const V av = cmul(alpha, v[o + j]);
+  auto upd = [&](V rv, V vv) {
+    const V av = cmul(alpha, vv);
     V q;
-    q.x = r[o + j].x - av.x;
-    q.y = r[o + j].y - av.y;
-    s[o + j] = q;
+    q.x = rv.x - av.x;
+    q.y = rv.y - av.y;
     nn += (double)q.x * q.x + (double)q.y * q.y;
+    return q;
+  };
+  const long long gs = (long long)gridDim.x * blockDim.x, j0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (std::is_same<T, float>::value && (N & 1) == 0) {
+    // complex64 pairs: 16-byte loads and stores (o = b N is even)
+    const float4* r4 = reinterpret_cast<const float4*>(r + o);
+    const float4* v4 = reinterpret_cast<const float4*>(v + o);
+    float4* s4 = reinterpret_cast<float4*>(s + o);
+    for (long long j = j0; j < (N >> 1); j += gs) {
+      const float4 rv = __ldg(&r4[j]), vv = __ldg(&v4[j]);
+      const V q0 = upd(V{(T)rv.x, (T)rv.y}, V{(T)vv.x, (T)vv.y});
+      const V q1 = upd(V{(T)rv.z, (T)rv.w}, V{(T)vv.z, (T)vv.w});
+      s4[j] = make_float4((float)q0.x, (float)q0.y, (float)q1.x, (float)q1.y);
+    }
+  } else {
+    for (long long j = j0; j < N; j += gs) s[o + j] = upd(r[o + j], v[o + j]);
   }
   block_part3(nn, 0.0, nn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
 }
@@ -531,27 +547,50 @@ __global__ void bg_x_kernel(long long N, const double* __restrict__ state, const
   omega.x = (T)st[4], omega.y = (T)st[5];
   const long long o = (long long)b * N;
   double dre = 0.0, dim = 0.0, dnn = 0.0;
-  for (long long j = blockIdx.x * (long long)blockDim.x + threadIdx.x; j < N; j += (long long)gridDim.x * blockDim.x) {
-    const V ap = cmul(alpha, p[o + j]);
-    V xo = x[o + j];
+  // x += alpha p (+ omega s); r = s - omega t and <rh, r>, |r|^2 (md == 2)
+  auto upd = [&](V pv, V xo, V sv, V tv, V a, V& rr) {
+    const V ap = cmul(alpha, pv);
     xo.x += ap.x;
     xo.y += ap.y;
     if (md == 2) {
-      const V sv = s[o + j];
       const V os = cmul(omega, sv);
       xo.x += os.x;
       xo.y += os.y;
-      const V ot = cmul(omega, t[o + j]);
-      V rr;
+      const V ot = cmul(omega, tv);
       rr.x = sv.x - ot.x;
       rr.y = sv.y - ot.y;
-      r[o + j] = rr;
-      const V a = rh[o + j];
       dre += (double)a.x * rr.x + (double)a.y * rr.y;
       dim += (double)a.x * rr.y - (double)a.y * rr.x;
       dnn += (double)rr.x * rr.x + (double)rr.y * rr.y;
     }
-    x[o + j] = xo;
+    return xo;
+  };
+  const long long gs = (long long)gridDim.x * blockDim.x, j0 = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (std::is_same<T, float>::value && (N & 1) == 0) {
+    // complex64 pairs: 16-byte loads and stores (o = b N is even)
+    const long long N2 = N >> 1;
+    auto ld = [&](const V* a, long long j) { return __ldg(reinterpret_cast<const float4*>(a + o) + j); };
+    for (long long j = j0; j < N2; j += gs) {
+      const float4 pv = ld(p, j);
+      const float4 xv = reinterpret_cast<const float4*>(x + o)[j];
+      float4 sv = make_float4(0.f, 0.f, 0.f, 0.f), tv = sv, av = sv;
+      if (md == 2) sv = ld(s, j), tv = ld(t, j), av = ld(rh, j);
+      V r0, r1;
+      const V x0 = upd(V{(T)pv.x, (T)pv.y}, V{(T)xv.x, (T)xv.y}, V{(T)sv.x, (T)sv.y}, V{(T)tv.x, (T)tv.y},
+                       V{(T)av.x, (T)av.y}, r0);
+      const V x1 = upd(V{(T)pv.z, (T)pv.w}, V{(T)xv.z, (T)xv.w}, V{(T)sv.z, (T)sv.w}, V{(T)tv.z, (T)tv.w},
+                       V{(T)av.z, (T)av.w}, r1);
+      if (md == 2) reinterpret_cast<float4*>(r + o)[j] = make_float4((float)r0.x, (float)r0.y, (float)r1.x, (float)r1.y);
+      reinterpret_cast<float4*>(x + o)[j] = make_float4((float)x0.x, (float)x0.y, (float)x1.x, (float)x1.y);
+    }
+  } else {
+    for (long long j = j0; j < N; j += gs) {
+      V rr;
+      const V xo = upd(p[o + j], x[o + j], md == 2 ? s[o + j] : V{}, md == 2 ? t[o + j] : V{},
+                       md == 2 ? rh[o + j] : V{}, rr);
+      if (md == 2) r[o + j] = rr;
+      x[o + j] = xo;
+    }
   }
   block_part3(dre, dim, dnn, part + ((long long)b * gridDim.x + blockIdx.x) * 3);
 }
