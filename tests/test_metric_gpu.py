@@ -73,3 +73,29 @@ def test_schedule_matches_reference_golden(golden):
     tab = np.array([[M.kappa(k, t, 4) for t in range(1, 5)] for k in range(1, 13)])
     np.testing.assert_array_equal(tab, golden["kappa_table"])
     np.testing.assert_array_equal(np.concatenate(M.partition_views(30, 4)), golden["partition_equi_30_4"])
+
+
+def test_diag_metric_construction_checks():
+    # DiagPlusLowRank with a per-voxel diagonal reads min(d) and the gram in one
+    # device->host copy: d > 0 (NaN rejected too), W PD and omega = 1/min(d) (D-6)
+    from paper_2307_02043_b200.wpm import DiagPlusLowRank
+
+    rng = np.random.default_rng(11)
+    n = 3000
+    d = rng.uniform(0.5, 2.0, n)
+    u = rng.standard_normal((n, 2)) / np.sqrt(n)
+    w = DiagPlusLowRank(1.0, u, d=d, dtype=torch.float64)
+    assert w.min_diag() == pytest.approx(d.min(), rel=0, abs=0)
+    g = w.gram.cpu().numpy().reshape(2, 2)
+    np.testing.assert_allclose(g, u.T @ (u / d[:, None]), rtol=1e-12)
+    w0 = DiagPlusLowRank(1.0, np.zeros((n, 0)), d=d, dtype=torch.float64)  # rank 0: min(d) alone
+    assert w0.rank == 0 and w0.min_diag() == pytest.approx(d.min(), rel=0, abs=0)
+    for bad in (0.0, -1.0, np.nan):
+        db = d.copy()
+        db[n // 3] = bad
+        with pytest.raises(ValueError, match="positive"):
+            DiagPlusLowRank(1.0, u, d=db, dtype=torch.float64)
+    big = np.zeros((n, 1))
+    big[0, 0] = 10.0  # I - U^T D^-1 U / 1 is not PD
+    with pytest.raises(ValueError, match="positive definite"):
+        DiagPlusLowRank(1.0, big, sign=-1, d=d, dtype=torch.float64)
