@@ -213,33 +213,36 @@ def e2e_serial_ms(args, dev, grid, inp, wsp, v_h, d_h, u_h, iters):
     return float(np.mean(ms))
 
 
-def e2e_pipelined_ms(args, dev, grid, inp, wsp, v_h, d_h, u_h, iters):
-    """Two input slots and two workspaces.  While solve i runs on the compute
-    stream, step i+1's inputs stream in and its problem is built and validated
-    on a side stream, and x_{i-1} streams out on a D2H stream.  Every step still
-    copies its own inputs, builds its DiagPlusLowRank / DualTvProblem through
-    the public API (validation syncs included) and has its x read on the host."""
+def e2e_pipelined_ms(args, dev, grid, inp, wsp, v_h, d_h, u_h, iters, slots=3):
+    """Three input slots and workspaces.  Right after solve i is queued, step
+    i+1's inputs stream in on a high-priority side stream and its problem is
+    built and validated there (DiagPlusLowRank / DualTvProblem through the
+    public API, validation syncs included): the copies overlap solve i-1, the
+    validation kernels take the SMs between solve i-1 and solve i, so solve i+1
+    is queued before solve i ends.  x_i streams out on a D2H stream under solve
+    i+1 and the host reads every step's x."""
     import torch
     from paper_2307_02043_b200 import dual_tv_solver as D
 
     main = torch.cuda.current_stream(dev)
-    s_in, s_out = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+    s_in = torch.cuda.Stream(dev, priority=-1)
+    s_out = torch.cuda.Stream(dev)
     N = v_h.numel()
-    bufs = [[torch.empty_like(t, device=dev) for t in (v_h, d_h, u_h)] for _ in range(2)]
-    wsps = [wsp, D.ProxWorkspace(grid, wsp.dtype, dev)]
-    outs = [torch.empty(N, dtype=wsp.dtype).pin_memory() for _ in range(2)]
-    probs = [None, None]  # held until the slot is reused (their tensors live on s_in)
-    ev_in = [torch.cuda.Event() for _ in range(2)]
-    ev_done = [torch.cuda.Event() for _ in range(2)]
-    ev_out = [torch.cuda.Event() for _ in range(2)]
-    used = [False, False]
+    bufs = [[torch.empty_like(t, device=dev) for t in (v_h, d_h, u_h)] for _ in range(slots)]
+    wsps = [wsp] + [D.ProxWorkspace(grid, wsp.dtype, dev) for _ in range(slots - 1)]
+    outs = [torch.empty(N, dtype=wsp.dtype).pin_memory() for _ in range(slots)]
+    probs = [None] * slots  # held until the slot is reused (their tensors live on s_in)
+    ev_in = [torch.cuda.Event() for _ in range(slots)]
+    ev_done = [torch.cuda.Event() for _ in range(slots)]
+    ev_out = [torch.cuda.Event() for _ in range(slots)]
+    used = [False] * slots
     checks = []
 
     def build(i):
-        s = i % 2
+        s = i % slots
         with torch.cuda.stream(s_in):
             if used[s]:
-                s_in.wait_event(ev_done[s])  # the solve that read this slot (step i-2) is done
+                s_in.wait_event(ev_done[s])  # the solve that read this slot (step i-slots) is done
             for dst, src in zip(bufs[s], (v_h, d_h, u_h)):
                 dst.copy_(src, non_blocking=True)
             probs[s] = _e2e_problem(grid, inp, *bufs[s])  # its syncs wait on s_in only
@@ -248,10 +251,10 @@ def e2e_pipelined_ms(args, dev, grid, inp, wsp, v_h, d_h, u_h, iters):
     def run(total):
         build(0)
         for i in range(total):
-            s = i % 2
+            s = i % slots
             main.wait_event(ev_in[s])
             if used[s]:
-                ev_out[s].synchronize()  # host has x_{i-2}; slot s's workspace and output are free
+                ev_out[s].synchronize()  # host has x_{i-slots}; slot s's workspace and output are free
                 checks.append(float(outs[s][N // 2]))
             D.solve_async(probs[s], wsps[s], eps=1e-300, max_iter=iters)
             ev_done[s].record(main)
@@ -262,14 +265,14 @@ def e2e_pipelined_ms(args, dev, grid, inp, wsp, v_h, d_h, u_h, iters):
                 ev_out[s].record(s_out)
             if i + 1 < total:
                 build(i + 1)
-        for s in range(2):
+        for s in range(slots):
             if used[s]:
                 ev_out[s].synchronize()
                 checks.append(float(outs[s][N // 2]))
 
     run(max(args.warmup, 3))
     torch.cuda.synchronize(dev)
-    used[:] = [False, False]
+    used[:] = [False] * slots
     t0 = time.perf_counter()
     run(args.steps)
     torch.cuda.synchronize(dev)
@@ -413,10 +416,10 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": ws * N * iters / (e2e * 1e-3), "unit": UNIT, "ms_per_step": e2e,
                     "h2d_bytes_per_step": 3 * N * 4, "d2h_bytes_per_step": N * 4,
-                    "schedule": "pipelined 2-deep: under solve i, step i+1's H2D (v, d, u) and its "
-                                "DiagPlusLowRank / DualTvProblem build (validation syncs included) run on a "
-                                "side stream and x_{i-1}'s D2H on a copy stream; the host reads every x; "
-                                "wall clock over all steps",
+                    "schedule": "pipelined, 3 slots: step i+1's H2D (v, d, u) and its DiagPlusLowRank / "
+                                "DualTvProblem build (validation syncs included) run on a high-priority side "
+                                "stream under solve i-1, x_i's D2H on a copy stream under solve i+1; the host "
+                                "reads every x; wall clock over all steps",
                     "serial_ms_per_step": e2e_serial},
             "gpu_launches": args.steps,
             "ls": ls,
