@@ -370,25 +370,15 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n_rt, const typename CV<T>
 #define LS_ZC_PF 512  // ZC: prefetch the next view's column into L2 for m >= LS_ZC_PF (helps at 512, not 256)
 #endif
 
-// STG: the volume-to-volume case at m <= 256 also stages the next active
-// view's column (n planes x L) into shared memory with cp.async while the
-// current view computes, so no view waits on its own global loads
 #ifndef LS_ZC_MINB
 #define LS_ZC_MINB 3  // ZC at m <= 256: minimum resident blocks per SM requested from ptxas (register cap; 2 at m = 512)
 #endif
 #ifndef LS_ZC_VG
 #define LS_ZC_VG 1  // ZC view groups per column group (grid.y); measured: 2 and 4 are no faster at m = 256 / 512
 #endif
-#ifndef LS_ZC_STG
-#define LS_ZC_STG 0  // largest m whose volume-to-volume ZC stages the next view in smem (measured slower at 256 and 512: 0)
-#endif
 template <int R1, int R2, int L>
-__host__ __device__ constexpr bool zc_staged(bool std_case) {
-  return std_case && R1 * R2 <= LS_ZC_STG;
-}
-template <int R1, int R2, int L>
-constexpr int zc_smem_elems(int n, bool std_case = false) {
-  return R1 * R2 + R1 * R2 * L + (n + 1) * L + (zc_staged<R1, R2, L>(std_case) ? n * L : 0);
+constexpr int zc_smem_elems(int n) {
+  return R1 * R2 + R1 * R2 * L + (n + 1) * L;
 }
 
 // STD: the volume-to-volume case (z0 = zo0 = 0, nzi = nzo = n = m/2): the
@@ -405,8 +395,6 @@ __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_ke
   V* tw = (V*)smraw;
   V* sm = tw + M;
   V* ks = sm + M * L;  // [fz <= n][l]: K_hat of this block's columns, folded z
-  V* nb = ks + (n + 1) * L;  // STG: [z < n][l] the next view's column chunk
-  constexpr bool STG = zc_staged<R1, R2, L>(STD);
   const int tid = threadIdx.x, l = tid % L, t = tid / L;
   const int y = blockIdx.x / XT, xc = blockIdx.x % XT, x = xc * L + l;
   const long long zs = (long long)M * M;
@@ -434,56 +422,26 @@ __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_ke
   };
   bool first = true;
   constexpr int ZS = M * M;  // plane stride (32-bit offsets within one view's Q)
-  // STG: copy the block's column chunk (planes z < n, L columns) of view bs into nb
-  auto stage = [&](int bs) {
-    const V* c0 = q + (long long)bs * vstride + (long long)y * M + xc * L;
-    if (sizeof(V) == 8 && L % 2 == 0) {
-      for (int i = tid; i < n * (L / 2); i += NT) {
-        const int z = i / (L / 2), xx = 2 * (i % (L / 2));
-        cp_async16(&nb[z * L + xx], c0 + z * ZS + xx);
-      }
-    } else {
-      for (int i = tid; i < n * L; i += NT) {
-        const int z = i / L, xx = i % L;
-        if (sizeof(V) == 8) cp_async8(&nb[i], c0 + z * ZS + xx);
-        else cp_async16(&nb[i], c0 + z * ZS + xx);
-      }
-    }
-    asm volatile("cp.async.commit_group;\n" ::: "memory");
-  };
-  if (STG && next_active(b_lo) < B) stage(next_active(b_lo));
   for (int b = next_active(b_lo); b < B; b = next_active(b + 1)) {
     V* col = q + (long long)b * vstride + (long long)y * M + x;
     V a[R1 / C][R2];
-    if (STG) {
-      cp_async_wait_all();
-      __syncthreads();  // view b's column (and, first, the twiddles + K_hat) staged
 #pragma unroll
-      for (int s = 0; s < R1 / C; ++s)
+    for (int s = 0; s < R1 / C; ++s)
 #pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) a[s][n2] = n2 < R2 / 2 ? nb[(t + C * s + R1 * n2) * L + l] : czero<V>();
-      __syncthreads();  // every read of nb (and of sm by the previous view) done
-      const int bn = next_active(b + 1);
-      if (bn < B) stage(bn);  // lands while this view computes
-    } else {
-#pragma unroll
-      for (int s = 0; s < R1 / C; ++s)
-#pragma unroll
-        for (int n2 = 0; n2 < R2; ++n2) {
-          const int e = t + C * s + R1 * n2;
-          if (STD) a[s][n2] = n2 < R2 / 2 ? col[e * ZS] : czero<V>();
-          else a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
-        }
-      {  // the next active view's column into L2 while this one computes
-        const int bn = next_active(b + 1);
-        if (M >= LS_ZC_PF && bn < B) {
-          const V* nc = q + (long long)bn * vstride + (long long)y * M + x;
-          for (int e = t; e < nzi; e += C) prefetch_l2(nc + e * zs);
-        }
+      for (int n2 = 0; n2 < R2; ++n2) {
+        const int e = t + C * s + R1 * n2;
+        if (STD) a[s][n2] = n2 < R2 / 2 ? col[e * ZS] : czero<V>();
+        else a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
       }
-      if (first) cp_async_wait_all();
-      __syncthreads();  // twiddles + K_hat staged (first view); previous view's reads of sm done
+    {  // the next active view's column into L2 while this one computes
+      const int bn = next_active(b + 1);
+      if (M >= LS_ZC_PF && bn < B) {
+        const V* nc = q + (long long)bn * vstride + (long long)y * M + x;
+        for (int e = t; e < nzi; e += C) prefetch_l2(nc + e * zs);
+      }
     }
+    if (first) cp_async_wait_all();
+    __syncthreads();  // twiddles + K_hat staged (first view); previous view's reads of sm done
     step1<R1, R2, C, L, true, -1, STD>(a, sm, tw, l, t);
     __syncthreads();
     V c[R2 / C][R1];
@@ -701,7 +659,6 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   const size_t sm_row = sizeof(V) * (M + smem_elems<R1, R2, L, false>());
   const size_t sm_col = sizeof(V) * (M + smem_elems<R1, R2, L, true>());
   const size_t sm_zc = sizeof(V) * zc_smem_elems<R1, R2, L>(n);
-  const size_t sm_zs = sizeof(V) * zc_smem_elems<R1, R2, L>(n, true);  // volume-to-volume (STG staging)
   const long long N = (long long)n * n * n;
   V* q = (V*)scratch;                 // B x n x m x m
   V* hx = q + (long long)B * 4 * N;   // B x n x n x m
@@ -710,7 +667,7 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   const bool adj = op == 1 || op == 3;
   int rc;
   if ((rc = prep(xf_kernel<T, R1, R2, C, L>, sm_row)) || (rc = prep(yf_kernel<T, R1, R2, C, L>, sm_col)) ||
-      (rc = prep(zc_kernel<T, R1, R2, C, L, true>, sm_zs)) || (rc = prep(zc_kernel<T, R1, R2, C, L, false>, sm_zc)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
+      (rc = prep(zc_kernel<T, R1, R2, C, L, true>, sm_zc)) || (rc = prep(zc_kernel<T, R1, R2, C, L, false>, sm_zc)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
       (rc = prep(xi_kernel<T, R1, R2, C, L>, sm_row)))
     return rc;
   const int rows_in = nzi * n, rows_out = nzo * n;
@@ -719,7 +676,7 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q, active);
   const int zvg = B < LS_ZC_VG ? (B > 0 ? B : 1) : LS_ZC_VG;
   if (nzi == n && nzo == n && z0 == 0 && zo0 == 0)
-    zc_kernel<T, R1, R2, C, L, true><<<dim3(M * (M / L), zvg), NT, sm_zs, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
+    zc_kernel<T, R1, R2, C, L, true><<<dim3(M * (M / L), zvg), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
                                                                         (const V*)khat, q, active);
   else
     zc_kernel<T, R1, R2, C, L, false><<<dim3(M * (M / L), zvg), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
