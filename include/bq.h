@@ -54,8 +54,11 @@ extern "C" {
 
 typedef struct bq_ctx bq_ctx;
 
-/* Context: one per (device, host thread).  Holds the grid-barrier/control
- * workspace of the persistent kernels and the cuFFT plan cache. */
+/* Context: one per (device, host thread).  Holds the cuFFT plan cache and,
+ * PER STREAM (created on a stream's first use, up to 16 streams), the
+ * grid-barrier/control/partials workspace of the persistent kernels and of the
+ * helper reductions: calls on different streams of one context may run
+ * concurrently; calls on one stream are ordered and share that stream's set. */
 int bq_ctx_create(int device, bq_ctx** out);
 int bq_ctx_destroy(bq_ctx* ctx);
 const char* bq_last_error(void);

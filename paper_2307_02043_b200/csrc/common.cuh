@@ -57,11 +57,16 @@ int ls_conv_pruned(bq_ctx* ctx, int dtype, int n, int B, int op, const void* kha
                    const int* active = nullptr, const void* da = nullptr, double* dotp = nullptr, int* nblk = nullptr);
 }  // namespace bq
 
-struct bq_ctx {
-  int device = 0;
-  int num_sms = 0;
-  bq::Workspace ws;
-  void* fft_cache = nullptr;      // owned by views code
+namespace bq {
+// Per-stream workspace: every buffer a launch writes outside the caller's
+// tensors (barrier counters, block partials, controller block, near lists,
+// 1/d, pinned BiCGSTAB flags).  One set per stream the context is used on, so
+// calls on different streams of one context never share scratch (two
+// concurrently running reductions would otherwise race on the partials and the
+// arrival counter).  Calls on ONE stream are ordered, so they can share.
+struct StreamWs {
+  cudaStream_t stream = nullptr;
+  Workspace ws;
   void* near_buf = nullptr;       // near-voxel lists of the fused prox kernel
   size_t near_bytes = 0;
   void* aux_buf = nullptr;        // per-voxel 1/d of the fused prox kernel
@@ -69,6 +74,22 @@ struct bq_ctx {
   int* host_flags = nullptr;      // pinned: active-view counts of the device BiCGSTAB
   cudaEvent_t flag_ev[2] = {nullptr, nullptr};
 };
+// The workspace of `st` (created on first use); nullptr (error text set) when
+// the allocation fails.
+StreamWs* stream_ws(bq_ctx* ctx, cudaStream_t st);
+}  // namespace bq
+
+struct bq_ctx {
+  int device = 0;
+  int num_sms = 0;
+  void* fft_cache = nullptr;      // owned by views code
+  bq::StreamWs* streams[16] = {}; // per-stream workspaces (see StreamWs)
+  int n_streams = 0;
+};
+
+#define BQ_STREAM_WS(var, ctx, st)                                   \
+  bq::StreamWs* var = bq::stream_ws((ctx), (st));                    \
+  if (!var) return BQ_ECUDA
 
 namespace bq {
 

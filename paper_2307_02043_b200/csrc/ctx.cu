@@ -23,6 +23,45 @@ int cuda_fail(cudaError_t e, const char* where) {
 
 void fft_cache_destroy(void* cache);  // views code
 
+static void stream_ws_free(StreamWs* w) {
+  if (!w) return;
+  cudaFree(w->near_buf);
+  cudaFree(w->aux_buf);
+  if (w->host_flags) cudaFreeHost(w->host_flags);
+  if (w->flag_ev[0]) cudaEventDestroy(w->flag_ev[0]);
+  if (w->flag_ev[1]) cudaEventDestroy(w->flag_ev[1]);
+  cudaFree(w->ws.partials);
+  cudaFree(w->ws.barrier);
+  cudaFree(w->ws.ctl);
+  cudaFree(w->ws.scratch);
+  delete w;
+}
+
+StreamWs* stream_ws(bq_ctx* ctx, cudaStream_t st) {
+  for (int i = 0; i < ctx->n_streams; ++i)
+    if (ctx->streams[i]->stream == st) return ctx->streams[i];
+  if (ctx->n_streams == (int)(sizeof(ctx->streams) / sizeof(ctx->streams[0]))) {
+    set_error("bq_ctx: more than %d streams used on one context", ctx->n_streams);
+    return nullptr;
+  }
+  StreamWs* w = new StreamWs();
+  w->stream = st;
+  w->ws.ctl_bytes = 4096;
+  cudaError_t e;
+  if ((e = cudaMalloc(&w->ws.partials, sizeof(double) * kMaxBlocks * kMaxVals)) != cudaSuccess ||
+      (e = cudaMalloc(&w->ws.barrier, 64)) != cudaSuccess ||
+      (e = cudaMalloc(&w->ws.ctl, w->ws.ctl_bytes)) != cudaSuccess ||
+      (e = cudaMalloc(&w->ws.scratch, sizeof(double) * 4096)) != cudaSuccess ||
+      (e = cudaMemset(w->ws.barrier, 0, 64)) != cudaSuccess ||
+      (e = cudaMemset(w->ws.ctl, 0, w->ws.ctl_bytes)) != cudaSuccess) {
+    stream_ws_free(w);
+    cuda_fail(e, "bq stream workspace");
+    return nullptr;
+  }
+  ctx->streams[ctx->n_streams++] = w;
+  return w;
+}
+
 }  // namespace bq
 
 extern "C" const char* bq_last_error(void) { return bq::g_err; }
@@ -47,21 +86,6 @@ extern "C" int bq_ctx_create(int device, bq_ctx** out) {
   bq_ctx* c = new bq_ctx();
   c->device = device;
   c->num_sms = prop.multiProcessorCount;
-  c->ws.ctl_bytes = 4096;
-  cudaError_t e;
-  if ((e = cudaMalloc(&c->ws.partials, sizeof(double) * kMaxBlocks * kMaxVals)) != cudaSuccess ||
-      (e = cudaMalloc(&c->ws.barrier, 64)) != cudaSuccess ||
-      (e = cudaMalloc(&c->ws.ctl, c->ws.ctl_bytes)) != cudaSuccess ||
-      (e = cudaMalloc(&c->ws.scratch, sizeof(double) * 4096)) != cudaSuccess ||
-      (e = cudaMemset(c->ws.barrier, 0, 64)) != cudaSuccess ||
-      (e = cudaMemset(c->ws.ctl, 0, c->ws.ctl_bytes)) != cudaSuccess) {
-    cudaFree(c->ws.partials);
-    cudaFree(c->ws.barrier);
-    cudaFree(c->ws.ctl);
-    cudaFree(c->ws.scratch);
-    delete c;
-    return cuda_fail(e, "bq_ctx_create workspace");
-  }
   *out = c;
   return BQ_OK;
 }
@@ -72,15 +96,7 @@ extern "C" int bq_ctx_destroy(bq_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   fft_cache_destroy(c->fft_cache);
-  cudaFree(c->near_buf);
-  cudaFree(c->aux_buf);
-  if (c->host_flags) cudaFreeHost(c->host_flags);
-  if (c->flag_ev[0]) cudaEventDestroy(c->flag_ev[0]);
-  if (c->flag_ev[1]) cudaEventDestroy(c->flag_ev[1]);
-  cudaFree(c->ws.partials);
-  cudaFree(c->ws.barrier);
-  cudaFree(c->ws.ctl);
-  cudaFree(c->ws.scratch);
+  for (int i = 0; i < c->n_streams; ++i) stream_ws_free(c->streams[i]);
   delete c;
   return BQ_OK;
 }

@@ -63,7 +63,7 @@ int grid_for(bq_ctx* ctx, long long n) {
   return (int)std::max<long long>(1, std::min<long long>(want, std::min(MAXB, ctx->num_sms * 4)));
 }
 
-RedWs red_ws(bq_ctx* ctx) { return RedWs{ctx->ws.partials, ctx->ws.barrier + 4}; }
+RedWs red_ws(StreamWs* sw) { return RedWs{sw->ws.partials, sw->ws.barrier + 4}; }
 
 // cap = I + sign gram_scaled ; chol in place (lower).  Single thread.
 __device__ bool cap_chol(const double* gram, int r, int sign, double tau, bool diag, double* L) {
@@ -383,7 +383,8 @@ extern "C" int bq_metric_gram(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t ran
   BQ_CHECK(d || tau > 0, BQ_EINVAL, "tau must be positive");
   cudaStream_t st = (cudaStream_t)stream;
   const int G = grid_for(ctx, n);
-  RedWs ws = red_ws(ctx);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
   if (dtype == BQ_F32) {
     RANK_SWITCH(rank, (gram_kernel<float, R><<<G, NT, 0, st>>>(n, (const float*)d, (const float*)U, gram_out, ws)));
   } else {
@@ -402,9 +403,10 @@ extern "C" int bq_metric_apply(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t ra
   BQ_CHECK(rank == 0 || (U && (gram || !inverse)), BQ_EINVAL, "U (and gram for the inverse) required");
   cudaStream_t st = (cudaStream_t)stream;
   const int G = grid_for(ctx, n);
-  RedWs ws = red_ws(ctx);
-  double* rhs = ctx->ws.scratch;
-  int* status = (int*)(ctx->ws.scratch + 64);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
+  double* rhs = sw->ws.scratch;
+  int* status = (int*)(sw->ws.scratch + 64);
   if (rank == 0) {
     if (dtype == BQ_F32)
       metric_out_kernel<float, 0><<<G, NT, 0, st>>>(n, sign, tau, (const float*)d, nullptr, nullptr, nullptr, inverse,
@@ -437,7 +439,8 @@ extern "C" int bq_dot(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, cons
   for (int k = 0; k < count; ++k) P.a[k] = a_ptrs[k], P.b[k] = b_ptrs[k];
   cudaStream_t st = (cudaStream_t)stream;
   const int G = grid_for(ctx, n);
-  RedWs ws = red_ws(ctx);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
 #define DOTS(T)                                                                   \
   switch (count) {                                                                \
     case 1: dots_kernel<T, 1><<<G, NT, 0, st>>>(n, P, dots_out, ws); break;       \
@@ -466,7 +469,8 @@ extern "C" int bq_sr1(bq_ctx* ctx, int32_t dtype, int64_t n, const void* s, cons
   BQ_CHECK(alpha_fallback > 0.0, BQ_EINVAL, "alpha_fallback must be positive, got %g", alpha_fallback);
   cudaStream_t st = (cudaStream_t)stream;
   const int G = grid_for(ctx, n);
-  RedWs ws = red_ws(ctx);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
   if (dtype == BQ_F32) {
     sr1_pass1<float><<<G, NT, 0, st>>>(n, (const float*)s, (const float*)m, gamma, alpha_fallback, est_out, ws);
     sr1_pass2<float><<<G, NT, 0, st>>>(n, (const float*)s, (const float*)m, est_out, ws);
@@ -487,6 +491,8 @@ extern "C" int bq_vk(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const
   BQ_CHECK(ctx && xs && gs && taus && acc_scratch && v_out && n > 0, BQ_EINVAL, "bq_vk: bad arguments");
   BQ_CHECK(count >= 1 && count <= 8, BQ_EINVAL, "bq_vk: 1..8 slots");
   BQ_CHECK(rank >= 0 && rank <= 8 && (rank == 0 || (U_w && gram_w)), BQ_EINVAL, "bq_vk: bad metric");
+  BQ_CHECK(tau_w > 0, BQ_EINVAL, "bq_vk: the aggregated metric needs a positive scalar tau (no per-voxel d)");
+  BQ_CHECK(sign == 1 || sign == -1, BQ_EINVAL, "bq_vk: sign must be +/-1");
   VkPtrs P{};
   for (int k = 0; k < count; ++k) {
     P.x[k] = xs[k];
@@ -496,10 +502,11 @@ extern "C" int bq_vk(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const
   }
   cudaStream_t st = (cudaStream_t)stream;
   const int G = grid_for(ctx, n);
-  RedWs ws = red_ws(ctx);
-  double* utx = ctx->ws.scratch + 128;
-  double* rhs = ctx->ws.scratch + 160;
-  int* status = (int*)(ctx->ws.scratch + 192);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
+  double* utx = sw->ws.scratch + 128;
+  double* rhs = sw->ws.scratch + 160;
+  int* status = (int*)(sw->ws.scratch + 192);
   if (dtype == BQ_F32) {
     vk_pass1<float><<<G, NT, 0, st>>>(n, count, P, utx, ws);
     if (rank == 0) {
@@ -538,7 +545,8 @@ extern "C" int bq_tv_value(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64
   cudaStream_t st = (cudaStream_t)stream;
   const long long n = dims[0] * dims[1] * dims[2];
   const int G = grid_for(ctx, n);
-  RedWs ws = red_ws(ctx);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
   if (dtype == BQ_F32)
     tv_kernel<float><<<G, NT, 0, st>>>(ndim, (int)dims[0], (int)dims[1], (int)dims[2], mode, (const float*)x, out, ws);
   else

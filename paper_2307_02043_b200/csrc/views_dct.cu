@@ -203,7 +203,8 @@ extern "C" int bq_views_combine(bq_ctx* ctx, int32_t dtype, int64_t n, const voi
   for (int i = 0; i < count; ++i) Y.y[i] = ys[i];
   cudaStream_t st = (cudaStream_t)stream;
   const int G = std::min(grid_for(ctx, n, 256), 1024);
-  double* partials = ctx->ws.partials;  // >= 1024 * 64 doubles (kMaxBlocks * kMaxVals)
+  BQ_STREAM_WS(sw, ctx, st);
+  double* partials = sw->ws.partials;  // >= 1024 * 64 doubles (kMaxBlocks * kMaxVals)
   if (dtype == BQ_F32)
     combine_kernel<float><<<G, 256, 0, st>>>(n, (const float*)F, Y, (const unsigned long long*)masks, views_dev, count, scale, (float*)r_out,
                                               partials, cost_out != nullptr);

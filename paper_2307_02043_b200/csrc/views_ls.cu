@@ -727,10 +727,11 @@ int bicgstab_impl(bq_ctx* ctx, int dtype, int n, int B, int adjoint, const void*
   int* active = mode + B;
   int* act2 = active + B;
   int* count = act2 + B;
-  if (!ctx->host_flags) {
-    BQ_CUDA(cudaHostAlloc((void**)&ctx->host_flags, 4 * sizeof(int), cudaHostAllocDefault));
-    BQ_CUDA(cudaEventCreateWithFlags(&ctx->flag_ev[0], cudaEventDisableTiming));
-    BQ_CUDA(cudaEventCreateWithFlags(&ctx->flag_ev[1], cudaEventDisableTiming));
+  BQ_STREAM_WS(sw, ctx, st);
+  if (!sw->host_flags) {
+    BQ_CUDA(cudaHostAlloc((void**)&sw->host_flags, 4 * sizeof(int), cudaHostAllocDefault));
+    BQ_CUDA(cudaEventCreateWithFlags(&sw->flag_ev[0], cudaEventDisableTiming));
+    BQ_CUDA(cudaEventCreateWithFlags(&sw->flag_ev[1], cudaEventDisableTiming));
   }
   const int op = adjoint ? 1 : 0;
   const dim3 vg(nbv, B);
@@ -751,11 +752,11 @@ int bicgstab_impl(bq_ctx* ctx, int dtype, int n, int B, int adjoint, const void*
     bg_x_kernel<T><<<vg, 256, 0, st>>>(N, state, p, s, t, rh, x, r, mode, part);
     bg_ctl_kernel<<<B, 256, 0, st>>>(BG_END, nbv, part, state, mode, active, act2, iters, it, tol, count);
     BQ_CUDA(cudaGetLastError());
-    BQ_CUDA(cudaMemcpyAsync(&ctx->host_flags[it & 1], count, sizeof(int), cudaMemcpyDeviceToHost, st));
-    BQ_CUDA(cudaEventRecord(ctx->flag_ev[it & 1], st));
+    BQ_CUDA(cudaMemcpyAsync(&sw->host_flags[it & 1], count, sizeof(int), cudaMemcpyDeviceToHost, st));
+    BQ_CUDA(cudaEventRecord(sw->flag_ev[it & 1], st));
     if (it >= 2) {  // one iteration late: the GPU already has iteration `it` queued
-      BQ_CUDA(cudaEventSynchronize(ctx->flag_ev[(it - 1) & 1]));
-      if (ctx->host_flags[(it - 1) & 1] == 0) break;
+      BQ_CUDA(cudaEventSynchronize(sw->flag_ev[(it - 1) & 1]));
+      if (sw->host_flags[(it - 1) & 1] == 0) break;
     }
   }
   return BQ_OK;

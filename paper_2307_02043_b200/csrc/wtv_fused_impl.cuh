@@ -1968,9 +1968,10 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.x = (T*)D.x;
   A.beta_io = D.beta;
   A.report = (bq_wtv_report*)D.report;
-  A.partials = ctx->ws.partials;
-  A.red = (double*)ctx->ws.ctl;
-  A.bar = ctx->ws.barrier;
+  BQ_STREAM_WS(sw, ctx, st);
+  A.partials = sw->ws.partials;
+  A.red = (double*)sw->ws.ctl;
+  A.bar = sw->ws.barrier;
   A.lpr = std::min(A.K1 / 4, 32);
   A.rpw = 32 / A.lpr;
   A.wpr = A.K1 > 128 ? A.K1 / 128 : 1;
@@ -1978,14 +1979,14 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   while ((1 << A.lpr_log2) < A.lpr) ++A.lpr_log2;
   if (D.d) {
     const size_t ib = (size_t)A.N * sizeof(T);
-    if (ctx->aux_bytes < ib) {
-      cudaFree(ctx->aux_buf);
-      ctx->aux_buf = nullptr;
-      ctx->aux_bytes = 0;
-      BQ_CUDA(cudaMalloc(&ctx->aux_buf, ib));
-      ctx->aux_bytes = ib;
+    if (sw->aux_bytes < ib) {
+      cudaFree(sw->aux_buf);
+      sw->aux_buf = nullptr;
+      sw->aux_bytes = 0;
+      BQ_CUDA(cudaMalloc(&sw->aux_buf, ib));
+      sw->aux_bytes = ib;
     }
-    A.ie = (T*)ctx->aux_buf;
+    A.ie = (T*)sw->aux_buf;
   }
   const int TYe = ((RW + 1) / A.wpr - 1) * A.rpw;  // standalone DIV pass tile
   A.nty = (A.K2 + TYe - 1) / TYe;
@@ -2066,26 +2067,26 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   }
   const size_t data_bytes = 2 * (size_t)G * (NT / 32) * A.capw * EWN * sizeof(T);
   const size_t need = data_bytes + 2 * (size_t)G * (NT / 32) * sizeof(int);
-  if (ctx->near_bytes < need) {
-    cudaFree(ctx->near_buf);
-    ctx->near_buf = nullptr;
-    ctx->near_bytes = 0;
-    BQ_CUDA(cudaMalloc(&ctx->near_buf, need));
-    ctx->near_bytes = need;
+  if (sw->near_bytes < need) {
+    cudaFree(sw->near_buf);
+    sw->near_buf = nullptr;
+    sw->near_bytes = 0;
+    BQ_CUDA(cudaMalloc(&sw->near_buf, need));
+    sw->near_bytes = need;
   }
-  A.near_data = ctx->near_buf;
-  A.near_cnt = (int*)((char*)ctx->near_buf + data_bytes);
+  A.near_data = sw->near_buf;
+  A.near_cnt = (int*)((char*)sw->near_buf + data_bytes);
 
   A.dyn_bytes = (long long)dyn;
   A.list_off = (long long)base_dyn;
   A.list_bytes = (long long)list_bytes;
-  A.trace = getenv("BQ_PROX_TRACE") ? (unsigned long long*)ctx->ws.scratch : nullptr;
+  A.trace = getenv("BQ_PROX_TRACE") ? (unsigned long long*)sw->ws.scratch : nullptr;
   A.trace_pass = getenv("BQ_PROX_TRACE") ? atoi(getenv("BQ_PROX_TRACE")) : 0;
   A.trace_thread = getenv("BQ_PROX_TRACE_THREAD") ? atoi(getenv("BQ_PROX_TRACE_THREAD")) : 0;
   A.dbg = getenv("BQ_PROX_DBG") ? atoi(getenv("BQ_PROX_DBG")) : 0;
   A.grow_min = getenv("BQ_PROX_GROW") ? atof(getenv("BQ_PROX_GROW")) : 8.0;
   A.ndist_min = getenv("BQ_PROX_NDIST") ? atof(getenv("BQ_PROX_NDIST")) : 1024.0;
-  BQ_CUDA(cudaMemsetAsync(ctx->ws.barrier, 0, 2 * sizeof(unsigned), st));
+  BQ_CUDA(cudaMemsetAsync(sw->ws.barrier, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&A};
   BQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3((unsigned)G), dim3(NT), args, dyn, st));
   return BQ_OK;

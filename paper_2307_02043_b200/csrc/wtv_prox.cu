@@ -1011,9 +1011,10 @@ int launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t st) {
   A.x = (T*)D.x;
   A.beta_io = D.beta;
   A.report = (bq_wtv_report*)D.report;
-  A.partials = ctx->ws.partials;
-  A.red = (double*)ctx->ws.ctl;
-  A.bar = ctx->ws.barrier;
+  BQ_STREAM_WS(sw, ctx, st);
+  A.partials = sw->ws.partials;
+  A.red = (double*)sw->ws.ctl;
+  A.bar = sw->ws.barrier;
   A.vec = (A.N % 4 == 0) && aligned16(D.a) && aligned16(D.d) && aligned16(D.U) && aligned16(D.lo_arr) &&
           aligned16(D.hi_arr);
 
@@ -1032,7 +1033,7 @@ int launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t st) {
   A.nty = (A.K2 + TY - 1) / TY;
   A.tile_planes = (long long)A.ntx * A.nty * A.K3;
 
-  BQ_CUDA(cudaMemsetAsync(ctx->ws.barrier, 0, 2 * sizeof(unsigned), st));
+  BQ_CUDA(cudaMemsetAsync(sw->ws.barrier, 0, 2 * sizeof(unsigned), st));
   void* args[] = {&A};
   BQ_CUDA(cudaLaunchCooperativeKernel((void*)kern, dim3(G), dim3(NT), args, 0, st));
   return BQ_OK;

@@ -2,7 +2,8 @@
 
 Reference: ``/root/reference/pkg/src/tvqn/dual_tv_solver.py``
   * ``DualTvProblem`` (:25-79): same fields, defaults and validation; omega
-    defaults to 1/tau (scalar metric) or 1/min(d) (per-voxel diagonal, D-6).
+    defaults to 1/tau (scalar metric) or to the bound of
+    ``DiagPlusLowRank.default_omega`` (per-voxel diagonal, D-6).
   * ``DualSolveReport`` (:82-92): same fields.
   * ``dual_step_size`` (:155-158): 1 / (4 ndim omega reg).
   * ``solve(prob, eps=1e-5, max_iter=100, accelerated=True)`` (:161-250):
@@ -11,7 +12,8 @@ Reference: ``/root/reference/pkg/src/tvqn/dual_tv_solver.py``
     momentum, with every stop/accept decision on the device).
 
 numpy inputs give numpy outputs (float64 compute); torch CUDA inputs give
-torch outputs in their dtype (float32 or float64).  ``solve_async`` is the
+torch outputs in their dtype (float32 or float64); the arithmetic runs in the
+metric's dtype (where U and d live), v is cast to it.  ``solve_async`` is the
 GPU-resident variant that leaves the report on the device.
 """
 
@@ -46,7 +48,7 @@ class DualTvProblem:
         if self.reg < 0:
             raise ValueError("reg must be nonnegative")
         if self.omega is None:
-            self.omega = 1.0 / self.w.min_diag()
+            self.omega = self.w.default_omega()
         if not self.omega > 0:
             raise ValueError("omega must be positive")
         if self.beta_warm is not None and not is_torch(self.beta_warm):
@@ -91,6 +93,9 @@ def _launch(prob: DualTvProblem, v: torch.Tensor, ws: ProxWorkspace, eps, max_it
         raise ValueError(f"expected {g.size} entries, got {v.numel()}")
     if w.rank and w.dim != g.size:
         raise ValueError(f"dimension mismatch: metric is {w.dim}, grid is {g.size}")
+    if (w.rank or w.d is not None) and w.dtype != ws.dtype:
+        # the kernel reads U and d in the descriptor's dtype
+        raise ValueError(f"metric dtype {w.dtype} differs from the workspace dtype {ws.dtype}")
     lo, hi, lo_a, hi_a = prob.box.device_args(ws.dtype, ws.device)
     desc = _abi.WtvDesc()
     desc.ndim = g.ndim
@@ -163,9 +168,9 @@ def read_report(ws: ProxWorkspace) -> _abi.WtvReport:
 def solve(prob: DualTvProblem, eps=1e-5, max_iter=100, accelerated=True) -> DualSolveReport:
     """Drop-in for ``tvqn.dual_tv_solver.solve`` (dual_tv_solver.py:161-250)."""
     _check_args(prob, eps, max_iter)
+    # compute in the metric's dtype (U and d live there); v is cast to it and
+    # torch outputs come back in v's own dtype
     dtype = prob.w.dtype
-    if is_torch(prob.v) and prob.v.dtype in (torch.float32, torch.float64):
-        dtype = prob.v.dtype
     ws = ProxWorkspace(prob.grid, dtype, prob.w.device)
     solve_async(prob, ws, eps, max_iter, accelerated)
     rep = read_report(ws)
@@ -178,6 +183,10 @@ def solve(prob: DualTvProblem, eps=1e-5, max_iter=100, accelerated=True) -> Dual
             p_star = np.asarray(prob.warm_start)
     else:
         p_star = out_like(like, ws.p)
+    if is_torch(like) and like.dtype in (torch.float32, torch.float64) and like.dtype != dtype:
+        ws.x, ws.p = ws.x.to(like.dtype), ws.p.to(like.dtype)
+        if prob.reg != 0.0:
+            p_star = ws.p
     return DualSolveReport(
         x=out_like(like, ws.x),
         p_star=p_star,

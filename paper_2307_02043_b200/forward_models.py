@@ -5,7 +5,8 @@ Mirror of ``tvqn.forward_models`` (``/root/reference/pkg/src/tvqn/forward_models
 * ``ViewProblem`` (:25-83): forward / jacobian_vec / adjoint_vec / value /
   gradient / self_check with the reference's semantics (numpy in, numpy out).
 * ``spectrum_masks`` (:94-136), ``make_phantom`` (:242-282), ``snr_db``
-  (:219-228): host-side input construction (same algorithms, same RNG use).
+  (:219-228): host-side input construction, re-exported from ``fixtures``
+  (restated laws, same RNG use).
 * ``make_linear_views`` / ``make_nonlinear_views`` (:153-215): the views of
   one call form a ``DctViewSet`` whose operators run in libbq (exact
   orthonormal DCT per axis, 3-point smoother, pointwise chain rule); the
@@ -30,85 +31,8 @@ from . import _abi
 from ._tensors import default_device, is_torch, out_like, to_dev
 from .tv_ops import Grid, TvMode, tv_value
 
-_CONE_MAX = math.radians(20.0)
-
-
-# ---------------------------------------------------------------------------
-# host-side construction (input data, not the hot path)
-# ---------------------------------------------------------------------------
-def spectrum_masks(grid: Grid, n_views, mask_fraction):
-    """Binary per-view frequency masks and the missing cone (forward_models.py:94-136)."""
-    if n_views < 1:
-        raise ValueError("need at least one view")
-    if not 0.0 < mask_fraction <= 1.0:
-        raise ValueError("mask_fraction must lie in (0, 1]")
-    n = grid.size
-    if grid.ndim == 1:
-        idx = np.arange(n)
-        return [(idx % n_views == v) | (idx == 0) for v in range(n_views)], np.zeros(n, dtype=bool)
-    axes = [np.arange(k, dtype=float) / max(k - 1, 1) for k in grid.dims]
-    mesh = np.meshgrid(*axes, indexing="ij")
-    radial = np.sqrt(sum(c * c for c in mesh[:-1]))
-    ang = grid.from_nd(np.arctan2(radial, mesh[-1]))
-    dc = np.zeros(n, dtype=bool)
-    dc[0] = True
-    phi_cone = _CONE_MAX * (1.0 - mask_fraction)
-    cone = (ang < phi_cone) & ~dc
-    span = math.pi / 2.0 - phi_cone
-    width = span * max(mask_fraction, 1.0 / n_views)
-    out = []
-    for v in range(n_views):
-        centre = phi_cone + (v + 0.5) * span / n_views
-        out.append(((np.abs(ang - centre) <= width / 2.0 + 1e-12) & ~cone) | dc)
-    return out, cone
-
-
-@dataclass(frozen=True, eq=False)
-class Phantom:
-    grid: Grid
-    values: np.ndarray
-    eta_m: float
-    eta_max: float
-    spheres: tuple
-
-
-def make_phantom(grid: Grid, kind="spheres", eta_m=1.333, eta_max=1.363, seed=0):
-    """Nested-sphere (or cube) phantom (forward_models.py:242-282)."""
-    if eta_max < eta_m:
-        raise ValueError("eta_max must be >= eta_m")
-    rng = np.random.default_rng(seed)
-    mesh = np.meshgrid(*[(np.arange(k, dtype=float) + 0.5) / k for k in grid.dims], indexing="ij")
-    vol = np.full(grid.dims, eta_m, dtype=float)
-    if kind == "spheres":
-        ns = 3
-        levels = eta_m + (eta_max - eta_m) * np.linspace(1.0 / ns, 1.0, ns)
-        centres = 0.3 + 0.4 * rng.random((ns, grid.ndim))
-        radii = np.linspace(0.32, 0.10, ns) * (0.8 + 0.4 * rng.random(ns))
-        spheres = []
-        for c, r, lev in zip(centres, radii, levels):
-            d2 = sum((mesh[i] - c[i]) ** 2 for i in range(grid.ndim))
-            vol[d2 <= r * r] = lev
-            spheres.append((tuple(c), float(r), float(lev)))
-    elif kind == "cube":
-        inside = np.ones(grid.dims, dtype=bool)
-        for c in mesh:
-            inside &= (c > 0.3) & (c < 0.7)
-        vol[inside] = eta_max
-        spheres = [((0.5,) * grid.ndim, 0.2, eta_max)]
-    else:
-        raise ValueError(f"unknown phantom kind: {kind!r}")
-    return Phantom(grid=grid, values=grid.from_nd(vol), eta_m=eta_m, eta_max=eta_max, spheres=tuple(spheres))
-
-
-def snr_db(x, x_ref):
-    x = x.detach().cpu().numpy() if is_torch(x) else np.asarray(x, dtype=float)
-    x_ref = x_ref.detach().cpu().numpy() if is_torch(x_ref) else np.asarray(x_ref, dtype=float)
-    if x.shape != x_ref.shape:
-        raise ValueError("shapes must match")
-    err = np.linalg.norm(x - x_ref)
-    if err == 0.0:
-        return math.inf
-    return 20.0 * math.log10(np.linalg.norm(x_ref) / err)
+# host-side input construction (restated reference laws, not the hot path)
+from .fixtures import Phantom, make_phantom, snr_db, spectrum_masks  # noqa: E402,F401
 
 
 # ---------------------------------------------------------------------------

@@ -64,6 +64,9 @@ def compute_v_k(slots, w: DiagPlusLowRank, step):
     """v = W^-1 sum_t (tau_t x_t + u_t (u_t^T x_t) - step g_t) (solvers.py:80-89)."""
     if len(slots) > 8:
         raise ValueError("at most 8 slots (BQ_MAX_RANK)")
+    if w.d is not None:
+        # the reference's aggregated metric is tau I + U U^T (solvers.py:67-77); bq_vk has no d
+        raise ValueError("compute_v_k needs a scalar-tau metric (aggregate_metric), not a per-voxel diagonal")
     dtype, dev = w.dtype, w.device
     xs = [to_dev(s.x, dtype, dev) for s in slots]
     gs = [to_dev(s.grad, dtype, dev) for s in slots]

@@ -85,8 +85,10 @@ class DiagPlusLowRank:
             if not self._dmin > 0:  # (NaN fails too, like (d > 0).all())
                 raise ValueError("diagonal d must be positive")
             host = host[1:]
+        self._gram_host = None
         if self.rank:
             g = host.reshape(self.rank, self.rank)
+            self._gram_host = g
             cap = np.eye(self.rank) + self.sign * (g / self.tau if self.d is None else g)
             try:
                 np.linalg.cholesky(cap)
@@ -114,6 +116,22 @@ class DiagPlusLowRank:
         if self.d is None:
             return self.tau
         return self._dmin if self._dmin is not None else float(self.d.min().item())
+
+    def default_omega(self) -> float:
+        """omega = 1/lambda_min lower bound used as the FGP default (D-6).
+
+        Scalar tau: 1/tau, the reference default (dual_tv_solver.py:73-74), kept
+        for parity.  Per-voxel d: 1/min(d) for sign +1 (W >= D); for sign -1,
+        W = D^1/2 (I - M) D^1/2 with eig(M) = eig(U^T D^-1 U) = eig(gram), so
+        lambda_min(W) >= min(d) (1 - lambda_max(gram)) > 0 (positive because W is
+        positive definite, checked at construction)."""
+        if self.d is None:
+            return 1.0 / self.tau
+        lo = self.min_diag()
+        if self.sign < 0 and self.rank:
+            lam = float(np.linalg.eigvalsh(self._gram_host)[-1])
+            lo *= 1.0 - lam
+        return 1.0 / lo
 
     def dense(self, n=None):
         n = self.dim if n is None else n

@@ -99,3 +99,15 @@ def test_diag_metric_construction_checks():
     big[0, 0] = 10.0  # I - U^T D^-1 U / 1 is not PD
     with pytest.raises(ValueError, match="positive definite"):
         DiagPlusLowRank(1.0, big, sign=-1, d=d, dtype=torch.float64)
+
+
+def test_compute_v_k_rejects_per_voxel_diagonal():
+    """bq_vk has no d: a per-voxel metric is refused instead of dividing by tau = 0."""
+    from paper_2307_02043_b200.wpm import DiagPlusLowRank
+
+    n = 64
+    rng = np.random.default_rng(2)
+    slots = [M.SubsetSlot(x=rng.standard_normal(n), grad=rng.standard_normal(n), hess=H.Sr1Estimate(tau=1.0))]
+    w = DiagPlusLowRank(1.0, rng.standard_normal((n, 1)) / 8, d=rng.uniform(0.5, 2, n))
+    with pytest.raises(ValueError):
+        M.compute_v_k(slots, w, 1.0)

@@ -250,3 +250,75 @@ def test_large_grid_fused_matches_general_kernel(monkeypatch, dims, r, dtype, to
     assert fused.iterations == general.iterations == 30
     assert rel_l2(fused.x.double().cpu().numpy(), general.x.double().cpu().numpy()) <= tol
     assert rel_l2(fused.p_star.double().cpu().numpy(), general.p_star.double().cpu().numpy()) <= tol
+
+
+def test_mixed_dtype_inputs_compute_in_metric_dtype():
+    """numpy (fp64) metric with a torch fp32 v: the arithmetic runs in the metric's
+    dtype (U and d live there), the outputs come back in v's dtype."""
+    d, u, v = _diag_problem(9, (24, 20, 16), 1)
+    ref = O.fgp_prox((24, 20, 16), v, O.Metric(U=u, d=d), reg=0.05, eps=1e-300, max_iter=30)
+    vt = torch.tensor(v, dtype=torch.float32, device="cuda")
+    rep = D.solve(D.DualTvProblem(grid=bq.Grid((24, 20, 16)), v=vt, w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05),
+                  eps=1e-300, max_iter=30)
+    assert rep.x.dtype == torch.float32 and rep.p_star.dtype == torch.float32
+    # v rounded to fp32 on input; everything after it in fp64
+    ref32 = O.fgp_prox((24, 20, 16), vt.double().cpu().numpy(), O.Metric(U=u, d=d), reg=0.05, eps=1e-300,
+                       max_iter=30)
+    assert rel_l2(rep.x.double().cpu().numpy(), ref32["x"]) <= 1e-6
+    assert rel_l2(rep.x.double().cpu().numpy(), ref["x"]) <= F32_TOL
+    # fp32 metric with numpy (fp64) v: computes in fp32
+    w32 = W.DiagPlusLowRank(1.0, torch.tensor(u, dtype=torch.float32, device="cuda"),
+                            d=torch.tensor(d, dtype=torch.float32, device="cuda"))
+    rep2 = D.solve(D.DualTvProblem(grid=bq.Grid((24, 20, 16)), v=v, w=w32, reg=0.05), eps=1e-300, max_iter=30)
+    assert isinstance(rep2.x, np.ndarray)
+    assert rel_l2(rep2.x, ref["x"]) <= F32_TOL
+    # a workspace in another dtype than the metric is refused
+    ws = D.ProxWorkspace(bq.Grid((24, 20, 16)), torch.float32, torch.device("cuda", 0))
+    with pytest.raises(ValueError):
+        D.solve_async(D.DualTvProblem(grid=bq.Grid((24, 20, 16)), v=vt, w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05),
+                      ws)
+
+
+def test_concurrent_streams_do_not_share_reduction_scratch():
+    """A prox on a small grid (fewer blocks than SMs) on one stream and metric
+    gram reductions on another stream of the same context run concurrently; each
+    stream has its own partials / arrival counters, so both results are exact."""
+    d, u, v = _diag_problem(13, (32, 16, 8), 2)
+    prob = D.DualTvProblem(grid=bq.Grid((32, 16, 8)), v=torch.tensor(v, device="cuda"),
+                           w=W.DiagPlusLowRank(1.0, u, d=d), reg=0.05)
+    solo = D.solve(prob, eps=1e-300, max_iter=80)
+    g = torch.Generator(device="cuda").manual_seed(3)
+    U2 = torch.randn(1 << 20, 4, generator=g, device="cuda", dtype=torch.float64) / 1024.0
+    w_solo = W.DiagPlusLowRank(2.0, U2)
+    side = torch.cuda.Stream()
+    grams = []
+    ws = D.ProxWorkspace(prob.grid, torch.float64, torch.device("cuda", 0))
+    torch.cuda.synchronize()
+    D.solve_async(prob, ws, eps=1e-300, max_iter=80)
+    with torch.cuda.stream(side):
+        for _ in range(20):
+            grams.append(W.DiagPlusLowRank(2.0, U2).gram.clone())
+    torch.cuda.synchronize()
+    assert torch.equal(ws.x, solo.x) and torch.equal(ws.p, solo.p_star)
+    for gr in grams:
+        assert torch.equal(gr, w_solo.gram)
+
+
+def test_default_omega_for_negative_sign_diag_metric():
+    """W = diag(d) - u u^T: omega defaults to 1/(min(d) (1 - lambda_max(U^T D^-1 U))),
+    a valid bound on 1/lambda_min(W) (1/min(d) is not), and the solve converges."""
+    rng = np.random.default_rng(4)
+    n = 12 * 10 * 8
+    d = rng.uniform(0.5, 2.0, n)
+    u = rng.standard_normal((n, 1)) * 0.6 / np.sqrt(n / 2.0)
+    w = W.DiagPlusLowRank(1.0, u, sign=-1, d=d)
+    lam_min = np.linalg.eigvalsh(w.dense())[0]
+    assert w.default_omega() >= 1.0 / lam_min * (1 - 1e-12)
+    assert w.default_omega() > 1.0 / d.min()
+    v = rng.standard_normal(n)
+    prob = D.DualTvProblem(grid=bq.Grid((12, 10, 8)), v=v, w=w, reg=0.05)
+    rep = D.solve(prob, eps=1e-8, max_iter=2000)
+    ref = O.fgp_prox((12, 10, 8), v, O.Metric(U=u, d=d, sign=-1), reg=0.05, eps=1e-8, max_iter=2000,
+                     omega=prob.omega)
+    assert rep.converged and ref["converged"] and rep.iterations == ref["iterations"]
+    assert rel_l2(rep.x, ref["x"]) <= F64_TOL
