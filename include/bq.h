@@ -137,6 +137,70 @@ int bq_wpm_box(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign
                int32_t newton_max_iter, void* x_out, void* a_scratch, void* report, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * z-slab-sharded prox: one rank's passes (dual_tv_solver.py:221-239 over a
+ * slab of planes [z0, z1) of a 3-D grid split along dims[2]).  The host runs
+ * the FGP / Newton control and the NCCL steps between the passes
+ * (paper_2307_02043_b200/slab_prox.py).  All buffers are the rank's local
+ * slab (N = K1*K2*L voxels); halos are single K1*K2 planes.
+ * ------------------------------------------------------------------------ */
+typedef struct {
+  int32_t dtype;         /* BQ_F32 / BQ_F64 for every field */
+  int32_t mode;          /* BQ_TV_ISO / BQ_TV_ANISO */
+  int32_t rank;          /* columns of U, 0..BQ_MAX_RANK */
+  int32_t sign;          /* +1 / -1 */
+  int64_t K1, K2, L;     /* slab: L planes of K1 x K2 */
+  int32_t first, last;   /* the slab holds global plane 0 / K3-1 */
+  double tau;            /* scalar diagonal when d == NULL */
+  double reg;            /* TV weight */
+  double lo, hi;         /* scalar box */
+  const void* d;         /* local per-voxel diagonal or NULL */
+  const void* U;         /* rank x N local */
+  const void* v;         /* N local */
+} bq_slab_desc;
+
+/* t = D^-1 div(F) over the slab (F: 3 x N; halo_below = F_z of plane z0-1,
+ * NULL when first); s_out (device, rank doubles) = U^T t (local sum). */
+int bq_slab_div(bq_ctx* ctx, const bq_slab_desc* desc, const void* field, const void* halo_below,
+                void* t_out, double* s_out, void* stream);
+/* Newton residual / Jacobian partials at beta (host arrays c, beta: rank doubles;
+ * c = cap^-1 s_global): out (device) = [U^T (w - clamp z) (rank) ;
+ * lower triangle of sum_inside U_c U_c' / d (or / 1 with scalar tau)]. */
+int bq_slab_newton(bq_ctx* ctx, const bq_slab_desc* desc, const void* t, const double* c,
+                   const double* beta, double* out, void* stream);
+/* q = clamp(z(beta)) over the slab. */
+int bq_slab_q(bq_ctx* ctx, const bq_slab_desc* desc, const void* t, const double* c, const double* beta,
+              void* q_out, void* stream);
+/* P_next = project(Pbar + step grad q) (halo_above = q of plane z1, NULL when
+ * last), Pbar_next = P_next + momentum (P_next - P), norms_out (device, 2
+ * doubles) = local ||P_next - P||^2, ||P||^2. */
+int bq_slab_dual(bq_ctx* ctx, const bq_slab_desc* desc, const void* pbar, const void* p, const void* q,
+                 const void* halo_above, double step, double momentum, void* p_next, void* pbar_next,
+                 double* norms_out, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Standalone TV stencils (tv_ops.py:107-180); the prox kernels fuse them.
+ * ------------------------------------------------------------------------ */
+/* out = D^axis x (adjoint = 0) or (D^axis)^T x (adjoint = 1); axis 1-based. */
+int bq_tv_diff(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64_t* dims, int32_t axis,
+               int32_t adjoint, const void* x, void* out, void* stream);
+/* p_out (ndim x N) = [D^1 x; ...; D^ndim x]  (gradient_stack / dual_adjoint). */
+int bq_tv_grad_stack(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64_t* dims, const void* x,
+                     void* p_out, void* stream);
+/* out (N) = sum_a (D^a)^T p_a  (dual_divergence). */
+int bq_tv_divergence(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64_t* dims, const void* p,
+                     void* out, void* stream);
+/* out = project_dual(p): per-voxel unit-ball (iso) or [-1, 1] clip (aniso). */
+int bq_tv_project_dual(bq_ctx* ctx, int32_t dtype, int32_t ndim, int64_t n, int32_t mode, const void* p,
+                       void* out, void* stream);
+/* Structured-WPM residual phi(beta) = U^T (x - clamp(x - sign D^-1 U beta)) + beta and
+ * the generalized Jacobian I + sign U_A^T D_A^-1 U_A (wpm.py:150-167):
+ * beta (device, rank doubles) -> phi_out (device, rank), jac_out (device, rank*rank
+ * row-major, may be NULL). */
+int bq_wpm_phi(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign, double tau,
+               const void* d, const void* U, const void* x, double lo, double hi, const void* lo_arr,
+               const void* hi_arr, const double* beta, double* phi_out, double* jac_out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * Metric algebra (W = diag(d) + sign U U^T), deterministic fixed-order reductions.
  * ------------------------------------------------------------------------ */
 /* gram_out (device, rank*rank doubles, row-major) = U^T D^-1 U  (D = tau I when d == NULL). */

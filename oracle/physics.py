@@ -40,7 +40,22 @@ from __future__ import annotations
 import math
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
+import scipy.fft as _sfft
+
+# all host cores for the padded transforms (scipy's pocketfft; the result
+# differs from numpy.fft only by rounding)
+_W = int(os.environ.get("BQ_ORACLE_FFT_WORKERS", "0")) or (os.cpu_count() or 1)
+
+
+def _fftn(a):
+    return _sfft.fftn(a, workers=_W)
+
+
+def _ifftn(a):
+    return _sfft.ifftn(a, workers=_W)
 
 
 @dataclass(frozen=True)
@@ -73,7 +88,7 @@ def green_kernel_hat(s: Setup, dtype=np.complex128):
         K = s.h ** 3 * np.exp(1j * kb * r) / (4.0 * math.pi * r)
     a = s.h * (3.0 / (4.0 * math.pi)) ** (1.0 / 3.0)
     K[0, 0, 0] = (np.exp(1j * kb * a) * (1.0 - 1j * kb * a) - 1.0) / kb ** 2
-    return np.fft.fftn(K).astype(dtype)
+    return _fftn(K).astype(dtype)
 
 
 def incident(s: Setup, view: int):
@@ -99,7 +114,7 @@ class Green:
 
     def apply_full(self, v):
         """G v on the padded grid (targets anywhere in planes 0..n)."""
-        return np.fft.ifftn(self.Kh * np.fft.fftn(self._pad(v)))
+        return _ifftn(self.Kh * _fftn(self._pad(v)))
 
     def dom(self, v):
         n = self.s.n
@@ -111,7 +126,7 @@ class Green:
 
     def _adj_from_padded(self, buf):
         n = self.s.n
-        return np.fft.ifftn(np.conj(self.Kh) * np.fft.fftn(buf))[:n, :n, :n].reshape(-1)
+        return _ifftn(np.conj(self.Kh) * _fftn(buf))[:n, :n, :n].reshape(-1)
 
     def dom_adj(self, w):
         return self._adj_from_padded(self._pad(w))

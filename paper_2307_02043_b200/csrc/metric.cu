@@ -16,6 +16,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "reduce.cuh"
 
 namespace bq {
 namespace {
@@ -23,47 +24,11 @@ namespace {
 constexpr int NT = 256;
 constexpr int MAXB = 1184;  // 148 SMs x 8
 
-struct RedWs {
-  double* partials;  // MAXB * kMaxVals
-  unsigned* count;
-};
-
-// Returns true in the last block; red[0..nv) then holds the totals (smem).
-template <int NACC>
-__device__ bool last_block_reduce(const double (&acc)[NACC], int nv, RedWs ws, double* red,
-                                  double* scr) {
-  __shared__ double s_bv[kMaxVals];
-  __shared__ int s_last;
-  block_sum_to<NT, NACC>(acc, nv, s_bv, scr);
-  if (threadIdx.x < nv) ws.partials[(size_t)blockIdx.x * kMaxVals + threadIdx.x] = s_bv[threadIdx.x];
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence();
-    unsigned old = atomicAdd(ws.count, 1u);
-    s_last = (old == gridDim.x - 1);
-    if (s_last) __threadfence();
-  }
-  __syncthreads();
-  if (!s_last) return false;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  for (int k = warp; k < nv; k += NT / 32) {
-    double s = 0.0;
-    for (unsigned b = lane; b < gridDim.x; b += 32) s += __ldcg(&ws.partials[(size_t)b * kMaxVals + k]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) s += __shfl_down_sync(0xffffffffu, s, o);
-    if (lane == 0) red[k] = s;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) *ws.count = 0;  // ready for the next launch
-  return true;
-}
-
 int grid_for(bq_ctx* ctx, long long n) {
   long long want = (n + 4LL * NT - 1) / (4LL * NT);
   return (int)std::max<long long>(1, std::min<long long>(want, std::min(MAXB, ctx->num_sms * 4)));
 }
 
-RedWs red_ws(StreamWs* sw) { return RedWs{sw->ws.partials, sw->ws.barrier + 4}; }
 
 // cap = I + sign gram_scaled ; chol in place (lower).  Single thread.
 __device__ bool cap_chol(const double* gram, int r, int sign, double tau, bool diag, double* L) {
@@ -117,7 +82,7 @@ __global__ void __launch_bounds__(NT) gram_kernel(long long n, const T* __restri
 #pragma unroll
       for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += d ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
   }
-  if (last_block_reduce<NA>(acc, R * (R + 1) / 2, ws, red, scr) && threadIdx.x == 0) {
+  if (last_block_reduce<NT, NA>(acc, R * (R + 1) / 2, ws, red, scr) && threadIdx.x == 0) {
     int k = 0;
     for (int c = 0; c < R; ++c)
       for (int c2 = 0; c2 <= c; ++c2, ++k) out[c * R + c2] = out[c2 * R + c] = red[k];
@@ -140,7 +105,7 @@ __global__ void __launch_bounds__(NT) utx_kernel(long long n, const T* __restric
 #pragma unroll
     for (int c = 0; c < R; ++c) acc[c] += (double)U[c * n + j] * (double)xv;
   }
-  if (last_block_reduce<R>(acc, R, ws, red, scr) && threadIdx.x < R) out[threadIdx.x] = red[threadIdx.x];
+  if (last_block_reduce<NT, R>(acc, R, ws, red, scr) && threadIdx.x < R) out[threadIdx.x] = red[threadIdx.x];
 }
 
 // pass 2: out = W x = D x + sign U (U^T x)      (apply)
@@ -201,7 +166,7 @@ __global__ void __launch_bounds__(NT) dots_kernel(long long n, DotPtrs P, double
 #pragma unroll
     for (int k = 0; k < C; ++k) acc[k] += (double)((const T*)P.a[k])[j] * (double)((const T*)P.b[k])[j];
   }
-  if (last_block_reduce<C>(acc, C, ws, red, scr) && threadIdx.x < C) out[threadIdx.x] = red[threadIdx.x];
+  if (last_block_reduce<NT, C>(acc, C, ws, red, scr) && threadIdx.x < C) out[threadIdx.x] = red[threadIdx.x];
 }
 
 // ------------------------------- SR1 --------------------------------------
@@ -219,7 +184,7 @@ __global__ void __launch_bounds__(NT) sr1_pass1(long long n, const T* __restrict
     acc[1] += mv * mv;
     acc[2] += (sv != 0.0) ? 1.0 : 0.0;
   }
-  if (last_block_reduce<3>(acc, 3, ws, red, scr) && threadIdx.x == 0) {
+  if (last_block_reduce<NT, 3>(acc, 3, ws, red, scr) && threadIdx.x == 0) {
     // hessian_sr1.py:90-95
     const double sm = red[0], mm = red[1];
     est[2] = sm;
@@ -256,7 +221,7 @@ __global__ void __launch_bounds__(NT) sr1_pass2(long long n, const T* __restrict
       acc[2] += (double)r * (double)r;
     }
   }
-  if (last_block_reduce<3>(acc, 3, ws, red, scr) && threadIdx.x == 0 && und < 0.0) {
+  if (last_block_reduce<NT, 3>(acc, 3, ws, red, scr) && threadIdx.x == 0 && und < 0.0) {
     // hessian_sr1.py:96-100 skip rule
     const double curv = red[0], ns = sqrt(red[1]), nr = sqrt(red[2]);
     est[3] = curv;
@@ -296,7 +261,7 @@ __global__ void __launch_bounds__(NT) vk_pass1(long long n, int count, VkPtrs P,
     for (int k = 0; k < 8; ++k)
       if (k < count && P.u[k]) acc[k] += (double)((const T*)P.u[k])[j] * (double)((const T*)P.x[k])[j];
   }
-  if (last_block_reduce<8>(acc, count, ws, red, scr) && threadIdx.x < count) out[threadIdx.x] = red[threadIdx.x];
+  if (last_block_reduce<NT, 8>(acc, count, ws, red, scr) && threadIdx.x < count) out[threadIdx.x] = red[threadIdx.x];
 }
 // pass 2: acc = sum_t (tau_t x_t + u_t (u_t^T x_t) - step g_t) (solvers.py:86-88), plus
 //         Woodbury rhs = U_w^T acc (U_w = aggregated columns)
@@ -328,7 +293,7 @@ __global__ void __launch_bounds__(NT) vk_pass2(long long n, int count, VkPtrs P,
 #pragma unroll
     for (int c = 0; c < R; ++c) acc[c] += (double)Uw[c * n + j] * (double)a;
   }
-  if (last_block_reduce<(R > 0 ? R : 1)>(acc, R, ws, red, scr) && threadIdx.x < R) rhs[threadIdx.x] = red[threadIdx.x];
+  if (last_block_reduce<NT, (R > 0 ? R : 1)>(acc, R, ws, red, scr) && threadIdx.x < R) rhs[threadIdx.x] = red[threadIdx.x];
 }
 
 // ------------------------------- TV value ---------------------------------
@@ -356,13 +321,67 @@ __global__ void __launch_bounds__(NT) tv_kernel(int ndim, int K1, int K2, int K3
       acc[0] += fabs((double)g1) + fabs((double)g2) + fabs((double)g3);
     }
   }
-  if (last_block_reduce<1>(acc, 1, ws, red, scr) && threadIdx.x == 0) out[0] = red[0];
+  if (last_block_reduce<NT, 1>(acc, 1, ws, red, scr) && threadIdx.x == 0) out[0] = red[0];
 }
 
 }  // namespace
 }  // namespace bq
 
 using namespace bq;
+
+
+// ---------------------------- wpm phi ---------------------------------------
+// phi(beta) = U^T (x - clamp(x - sign D^-1 U beta)) + beta and the generalized
+// Jacobian I + sign U_A^T D_A^-1 U_A over the strictly-inside set (wpm.py:150-167).
+template <typename T, int R>
+__global__ void __launch_bounds__(NT) phi_kernel(long long n, int sign, double tau, const T* __restrict__ d,
+                                                 const T* __restrict__ U, const T* __restrict__ x, double lo,
+                                                 double hi, const T* __restrict__ lo_a, const T* __restrict__ hi_a,
+                                                 const double* beta, double* phi_out, double* jac_out, RedWs ws) {
+  constexpr int NV = R + R * (R + 1) / 2;
+  __shared__ double red[kMaxVals];
+  __shared__ double scr[(NT / 32) * kMaxVals];
+  __shared__ T b[R];
+  if (threadIdx.x < R) b[threadIdx.x] = (T)beta[threadIdx.x];
+  __syncthreads();
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < n; j += (long long)gridDim.x * NT) {
+    T u[R];
+    T ub = (T)0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      u[k] = U[k * n + j];
+      ub += u[k] * b[k];
+    }
+    const T xv = x[j];
+    const T z = d ? xv - (T)sign * ub / d[j] : xv - (T)sign * ub / (T)tau;  // wpm.py:145-147
+    const T l = lo_a ? lo_a[j] : (T)lo;
+    const T h = hi_a ? hi_a[j] : (T)hi;
+    const T r = xv - min(max(z, l), h);
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += (double)(u[k] * r);
+    if (z > l && z < h) {
+      int m = R;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int k2 = 0; k2 <= k; ++k2, ++m) acc[m] += d ? (double)(u[k] * u[k2] / d[j]) : (double)(u[k] * u[k2]);
+    }
+  }
+  if (last_block_reduce<NT, NV>(acc, NV, ws, red, scr) && threadIdx.x == 0) {
+    for (int k = 0; k < R; ++k) phi_out[k] = red[k] + beta[k];
+    if (jac_out) {
+      int m = R;
+      for (int k = 0; k < R; ++k)
+        for (int k2 = 0; k2 <= k; ++k2, ++m) {
+          const double g = d ? red[m] : red[m] / tau;
+          jac_out[k * R + k2] = jac_out[k2 * R + k] = (k == k2 ? 1.0 : 0.0) + sign * g;
+        }
+    }
+  }
+}
 
 #define RANK_SWITCH(r, BODY)                       \
   switch (r) {                                     \
@@ -552,6 +571,29 @@ extern "C" int bq_tv_value(bq_ctx* ctx, int32_t dtype, int32_t ndim, const int64
   else
     tv_kernel<double><<<G, NT, 0, st>>>(ndim, (int)dims[0], (int)dims[1], (int)dims[2], mode, (const double*)x, out,
                                         ws);
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+extern "C" int bq_wpm_phi(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign, double tau,
+                          const void* d, const void* U, const void* x, double lo, double hi, const void* lo_arr,
+                          const void* hi_arr, const double* beta, double* phi_out, double* jac_out, void* stream) {
+  BQ_CHECK(ctx && U && x && beta && phi_out && n > 0, BQ_EINVAL, "bq_wpm_phi: bad arguments");
+  BQ_CHECK(d || tau > 0, BQ_EINVAL, "tau must be positive");
+  BQ_CHECK(sign == 1 || sign == -1, BQ_EINVAL, "sign must be +/-1");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = grid_for(ctx, n);
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
+  if (dtype == BQ_F32) {
+    RANK_SWITCH(rank, (phi_kernel<float, R><<<G, NT, 0, st>>>(n, sign, tau, (const float*)d, (const float*)U,
+                                                               (const float*)x, lo, hi, (const float*)lo_arr,
+                                                               (const float*)hi_arr, beta, phi_out, jac_out, ws)));
+  } else {
+    RANK_SWITCH(rank, (phi_kernel<double, R><<<G, NT, 0, st>>>(n, sign, tau, (const double*)d, (const double*)U,
+                                                                (const double*)x, lo, hi, (const double*)lo_arr,
+                                                                (const double*)hi_arr, beta, phi_out, jac_out, ws)));
+  }
   BQ_CUDA(cudaGetLastError());
   return BQ_OK;
 }

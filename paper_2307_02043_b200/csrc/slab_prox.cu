@@ -1,0 +1,364 @@
+// slab_prox.cu — one rank's passes of the z-slab-sharded weighted-TV prox.
+//
+// The FGP loop of dual_tv_solver.py:221-239 (and the structured projection of
+// wpm.py:145-231 inside it) over a volume split along dims[2] into contiguous
+// slabs, one per GPU.  Each FGP iteration is four stream-ordered passes over
+// the rank's slab, with the cross-rank steps between them issued by the host
+// (paper_2307_02043_b200/slab_prox.py) on the NCCL communicator:
+//
+//   bq_slab_div     t = D^-1 div(Pbar), s = U^T t           needs Pbar_z of plane z0-1 (halo from below)
+//                   -> all-reduce(s, r doubles);  c = cap^-1 s on the host
+//   bq_slab_newton  phi = U^T (w - clamp(z)), H = U_A^T D_A^-1 U_A at beta
+//                   with w = v - reg (t - sign D^-1 U c), z = w - sign D^-1 U beta
+//                   -> all-reduce(phi, H: r + r(r+1)/2 doubles) per Newton step
+//   bq_slab_q       q = clamp(z(beta*))
+//                   -> q of plane z1 from the rank above (halo)
+//   bq_slab_dual    P_next = project(Pbar + step grad q), ||P_next - P||^2, ||P||^2,
+//                   Pbar_next = P_next + m (P_next - P)     -> all-reduce(2 doubles)
+//
+// Per-block partial sums are reduced in block order by the last block
+// (deterministic); every rank holds bit-identical scalars after the
+// all-reduce, so the host controller (Newton accept / Levenberg / best
+// residual, the FISTA t-sequence, the rel-change stop) takes the same branch
+// on every rank.  Layout as the single-GPU prox: flat Fortran order over
+// (K1, K2, L) for the local slab, U as rank contiguous local N-vectors, the
+// dual field as 3 contiguous local N-vectors.
+#include <algorithm>
+
+#include "common.cuh"
+#include "reduce.cuh"
+
+namespace bq {
+namespace {
+
+constexpr int NT = 256;
+
+struct SlabArgs {
+  long long N;      // local voxels K1*K2*L
+  long long plane;  // K1*K2
+  int K1, K2, L;
+  int first, last;  // slab holds global plane 0 / K3-1
+  int rank, sign, iso;
+  double tau, reg, lo, hi;
+  const void* d;
+  const void* U;
+  const void* v;
+  double c[BQ_MAX_RANK];     // cap^-1 (U^T D^-1 div)  (Woodbury coefficient, global)
+  double beta[BQ_MAX_RANK];  // Newton point
+};
+
+template <typename T>
+__device__ __forceinline__ T inv_d(const SlabArgs& A, long long j) {
+  return A.d ? (T)1 / ((const T*)A.d)[j] : (T)(1.0 / A.tau);
+}
+
+// w_j = v_j - reg (t_j - sign D^-1 U c)   (dual_tv_solver.py:119-123 with the Woodbury inverse)
+template <typename T, int R>
+__device__ __forceinline__ T center(const SlabArgs& A, const T* __restrict__ t, long long j, T idj) {
+  const T* U = (const T*)A.U;
+  T uc = (T)0;
+#pragma unroll
+  for (int k = 0; k < R; ++k) uc += U[k * A.N + j] * (T)A.c[k];
+  const T corr = (R > 0) ? t[j] - (T)A.sign * uc * idj : t[j];
+  return ((const T*)A.v)[j] - (T)A.reg * corr;
+}
+
+// ---------------------------------------------------------------------------
+// t = D^-1 div(F), s = U^T t    (F = Pbar or P; halo = F_z of global plane z0-1)
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(NT) div_kernel(SlabArgs A, const T* __restrict__ F, const T* __restrict__ halo,
+                                                 T* __restrict__ t, double* s_out, RedWs ws) {
+  __shared__ double red[kMaxVals];
+  __shared__ double scr[(NT / 32) * kMaxVals];
+  constexpr int NA = R > 0 ? R : 1;
+  double acc[NA];
+#pragma unroll
+  for (int k = 0; k < NA; ++k) acc[k] = 0.0;
+  const T* Fx = F;
+  const T* Fy = F + A.N;
+  const T* Fz = F + 2 * A.N;
+  const T* U = (const T*)A.U;
+  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < A.N; j += (long long)gridDim.x * NT) {
+    const int ix = (int)(j % A.K1);
+    const int iy = (int)((j / A.K1) % A.K2);
+    const int iz = (int)(j / A.plane);
+    // sum_a (D^a)^T F_a, term order of tv_ops.py:129-131 per axis, axes accumulated from 0
+    T dv = (T)0;
+    {
+      T o = (T)0;
+      if (ix < A.K1 - 1) o -= Fx[j];
+      if (ix >= 1) o += Fx[j - 1];
+      dv += o;
+    }
+    {
+      T o = (T)0;
+      if (iy < A.K2 - 1) o -= Fy[j];
+      if (iy >= 1) o += Fy[j - A.K1];
+      dv += o;
+    }
+    {
+      T o = (T)0;
+      if (!(A.last && iz == A.L - 1)) o -= Fz[j];
+      if (iz >= 1) o += Fz[j - A.plane];
+      else if (!A.first) o += halo[j];  // plane z0-1 of the rank below
+      dv += o;
+    }
+    const T tj = dv * inv_d<T>(A, j);
+    t[j] = tj;
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += (double)U[k * A.N + j] * (double)tj;
+  }
+  if (R > 0) {
+    if (last_block_reduce<NT, NA>(acc, R, ws, red, scr) && threadIdx.x < R) s_out[threadIdx.x] = red[threadIdx.x];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Newton residual and generalized Jacobian at beta (wpm.py:150-167):
+//   out[0..R)            sum_j U_c (w_j - clamp(z_j))
+//   out[R + tri(c, c')]  sum_{j inside} U_c U_c' * (1/d_j or 1: the host divides by tau)
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(NT) newton_kernel(SlabArgs A, const T* __restrict__ t, double* out, RedWs ws) {
+  __shared__ double red[kMaxVals];
+  __shared__ double scr[(NT / 32) * kMaxVals];
+  constexpr int NV = R + R * (R + 1) / 2;
+  double acc[NV];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) acc[k] = 0.0;
+  const T* U = (const T*)A.U;
+  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < A.N; j += (long long)gridDim.x * NT) {
+    const T idj = inv_d<T>(A, j);
+    const T w = center<T, R>(A, t, j, idj);
+    T u[R];
+    T ub = (T)0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) {
+      u[k] = U[k * A.N + j];
+      ub += u[k] * (T)A.beta[k];
+    }
+    const T z = A.d ? w - (T)A.sign * ub * idj : w - (T)A.sign * ub / (T)A.tau;
+    const T q = min(max(z, (T)A.lo), (T)A.hi);
+    const T r = w - q;
+#pragma unroll
+    for (int k = 0; k < R; ++k) acc[k] += (double)(u[k] * r);
+    if (z > (T)A.lo && z < (T)A.hi) {  // ties count as outside (wpm.py:161-167)
+      const T sc = A.d ? idj : (T)1;
+      int m = R;
+#pragma unroll
+      for (int k = 0; k < R; ++k)
+#pragma unroll
+        for (int k2 = 0; k2 <= k; ++k2, ++m) acc[m] += (double)(u[k] * u[k2] * sc);
+    }
+  }
+  if (last_block_reduce<NT, NV>(acc, NV, ws, red, scr) && threadIdx.x < NV) out[threadIdx.x] = red[threadIdx.x];
+}
+
+// q = clamp(z(beta))   (wpm.py:246-253)
+template <typename T, int R>
+__global__ void __launch_bounds__(NT) q_kernel(SlabArgs A, const T* __restrict__ t, T* __restrict__ q) {
+  const T* U = (const T*)A.U;
+  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < A.N; j += (long long)gridDim.x * NT) {
+    const T idj = inv_d<T>(A, j);
+    const T w = center<T, R>(A, t, j, idj);
+    T ub = (T)0;
+#pragma unroll
+    for (int k = 0; k < R; ++k) ub += U[k * A.N + j] * (T)A.beta[k];
+    const T z = (R == 0) ? w : (A.d ? w - (T)A.sign * ub * idj : w - (T)A.sign * ub / (T)A.tau);
+    q[j] = min(max(z, (T)A.lo), (T)A.hi);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// dual update (dual_tv_solver.py:227-239): P_next = project(Pbar + step grad q)
+// norms: ||P_next - P||^2, ||P||^2 ; Pbar_next = P_next + m (P_next - P)
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(NT) dual_kernel(SlabArgs A, const T* __restrict__ pbar, const T* __restrict__ p,
+                                                  const T* __restrict__ q, const T* __restrict__ halo_q,
+                                                  double step, double mom, T* __restrict__ pn,
+                                                  T* __restrict__ pbn, double* norms, RedWs ws) {
+  __shared__ double red[kMaxVals];
+  __shared__ double scr[(NT / 32) * kMaxVals];
+  double acc[2] = {0.0, 0.0};
+  const long long N = A.N;
+  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < N; j += (long long)gridDim.x * NT) {
+    const int ix = (int)(j % A.K1);
+    const int iy = (int)((j / A.K1) % A.K2);
+    const int iz = (int)(j / A.plane);
+    const T qj = q[j];
+    T g[3];
+    g[0] = ix < A.K1 - 1 ? q[j + 1] - qj : (T)0;
+    g[1] = iy < A.K2 - 1 ? q[j + A.K1] - qj : (T)0;
+    if (iz < A.L - 1)
+      g[2] = q[j + A.plane] - qj;
+    else
+      g[2] = A.last ? (T)0 : halo_q[j - (long long)(A.L - 1) * A.plane] - qj;
+    T w[3];
+#pragma unroll
+    for (int a = 0; a < 3; ++a) w[a] = pbar[a * N + j] + (T)step * g[a];
+    if (A.iso) {
+      const T den = max(sqrt(w[0] * w[0] + w[1] * w[1] + w[2] * w[2]), (T)1);  // tv_ops.py:177-179
+#pragma unroll
+      for (int a = 0; a < 3; ++a) w[a] = w[a] / den;
+    } else {
+#pragma unroll
+      for (int a = 0; a < 3; ++a) w[a] = min(max(w[a], (T)-1), (T)1);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const T pa = p[a * N + j];
+      const T dlt = w[a] - pa;
+      acc[0] += (double)dlt * (double)dlt;
+      acc[1] += (double)pa * (double)pa;
+      pn[a * N + j] = w[a];
+      pbn[a * N + j] = w[a] + (T)mom * dlt;
+    }
+  }
+  if (last_block_reduce<NT, 2>(acc, 2, ws, red, scr) && threadIdx.x < 2) norms[threadIdx.x] = red[threadIdx.x];
+}
+
+template <typename T, int R>
+void launch_newton(int G, cudaStream_t st, const SlabArgs& A, const T* t, double* out, RedWs ws) {
+  if constexpr (R > 0) newton_kernel<T, R><<<G, NT, 0, st>>>(A, t, out, ws);
+}
+
+#define SLAB_RANK_SWITCH(r, BODY)                  \
+  switch (r) {                                     \
+    case 0: { constexpr int R = 0; BODY; } break;  \
+    case 1: { constexpr int R = 1; BODY; } break;  \
+    case 2: { constexpr int R = 2; BODY; } break;  \
+    case 3: { constexpr int R = 3; BODY; } break;  \
+    case 4: { constexpr int R = 4; BODY; } break;  \
+    case 5: { constexpr int R = 5; BODY; } break;  \
+    case 6: { constexpr int R = 6; BODY; } break;  \
+    case 7: { constexpr int R = 7; BODY; } break;  \
+    case 8: { constexpr int R = 8; BODY; } break;  \
+    default: set_error("rank %d outside [0, 8]", r); return BQ_EINVAL; \
+  }
+
+int make_args(const bq_slab_desc* D, const double* c, const double* beta, SlabArgs& A) {
+  BQ_CHECK(D && D->K1 >= 1 && D->K2 >= 1 && D->L >= 1, BQ_EINVAL, "bq_slab: bad slab geometry");
+  BQ_CHECK(D->rank >= 0 && D->rank <= BQ_MAX_RANK, BQ_EINVAL, "bq_slab: rank %d outside [0, 8]", D->rank);
+  BQ_CHECK(D->rank == 0 || D->U, BQ_EINVAL, "bq_slab: U required for rank > 0");
+  BQ_CHECK(D->d || D->tau > 0, BQ_EINVAL, "bq_slab: tau must be positive");
+  BQ_CHECK(D->sign == 1 || D->sign == -1, BQ_EINVAL, "bq_slab: sign must be +/-1");
+  BQ_CHECK(D->dtype == BQ_F32 || D->dtype == BQ_F64, BQ_EINVAL, "bq_slab: bad dtype");
+  A = SlabArgs{};
+  A.K1 = (int)D->K1;
+  A.K2 = (int)D->K2;
+  A.L = (int)D->L;
+  A.plane = D->K1 * D->K2;
+  A.N = A.plane * D->L;
+  A.first = D->first;
+  A.last = D->last;
+  A.rank = D->rank;
+  A.sign = D->sign;
+  A.iso = D->mode == BQ_TV_ISO;
+  A.tau = D->tau;
+  A.reg = D->reg;
+  A.lo = D->lo;
+  A.hi = D->hi;
+  A.d = D->d;
+  A.U = D->U;
+  A.v = D->v;
+  for (int k = 0; k < D->rank; ++k) {
+    A.c[k] = c ? c[k] : 0.0;
+    A.beta[k] = beta ? beta[k] : 0.0;
+  }
+  return BQ_OK;
+}
+
+int blocks(bq_ctx* ctx, long long n) {
+  long long want = (n + 4LL * NT - 1) / (4LL * NT);
+  return (int)std::max<long long>(1, std::min<long long>(want, std::min(1184, ctx->num_sms * 4)));
+}
+
+}  // namespace
+}  // namespace bq
+
+using namespace bq;
+
+extern "C" int bq_slab_div(bq_ctx* ctx, const bq_slab_desc* desc, const void* field, const void* halo_below,
+                           void* t_out, double* s_out, void* stream) {
+  SlabArgs A;
+  int rc = make_args(desc, nullptr, nullptr, A);
+  if (rc) return rc;
+  BQ_CHECK(ctx && field && t_out && (A.first || halo_below) && (A.rank == 0 || s_out), BQ_EINVAL,
+           "bq_slab_div: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
+  const int G = blocks(ctx, A.N);
+  if (desc->dtype == BQ_F32) {
+    SLAB_RANK_SWITCH(A.rank, (div_kernel<float, R><<<G, NT, 0, st>>>(A, (const float*)field, (const float*)halo_below,
+                                                                      (float*)t_out, s_out, ws)));
+  } else {
+    SLAB_RANK_SWITCH(A.rank, (div_kernel<double, R><<<G, NT, 0, st>>>(A, (const double*)field,
+                                                                       (const double*)halo_below, (double*)t_out,
+                                                                       s_out, ws)));
+  }
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+extern "C" int bq_slab_newton(bq_ctx* ctx, const bq_slab_desc* desc, const void* t, const double* c,
+                              const double* beta, double* out, void* stream) {
+  SlabArgs A;
+  int rc = make_args(desc, c, beta, A);
+  if (rc) return rc;
+  BQ_CHECK(ctx && t && out && A.rank >= 1 && c && beta, BQ_EINVAL, "bq_slab_newton: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
+  const int G = blocks(ctx, A.N);
+  if (desc->dtype == BQ_F32) {
+    SLAB_RANK_SWITCH(A.rank, (launch_newton<float, R>(G, st, A, (const float*)t, out, ws)));
+  } else {
+    SLAB_RANK_SWITCH(A.rank, (launch_newton<double, R>(G, st, A, (const double*)t, out, ws)));
+  }
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+extern "C" int bq_slab_q(bq_ctx* ctx, const bq_slab_desc* desc, const void* t, const double* c, const double* beta,
+                         void* q_out, void* stream) {
+  SlabArgs A;
+  int rc = make_args(desc, c, beta, A);
+  if (rc) return rc;
+  BQ_CHECK(ctx && t && q_out && (A.rank == 0 || (c && beta)), BQ_EINVAL, "bq_slab_q: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int G = blocks(ctx, A.N);
+  if (desc->dtype == BQ_F32) {
+    SLAB_RANK_SWITCH(A.rank, (q_kernel<float, R><<<G, NT, 0, st>>>(A, (const float*)t, (float*)q_out)));
+  } else {
+    SLAB_RANK_SWITCH(A.rank, (q_kernel<double, R><<<G, NT, 0, st>>>(A, (const double*)t, (double*)q_out)));
+  }
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+extern "C" int bq_slab_dual(bq_ctx* ctx, const bq_slab_desc* desc, const void* pbar, const void* p, const void* q,
+                            const void* halo_above, double step, double momentum, void* p_next, void* pbar_next,
+                            double* norms_out, void* stream) {
+  SlabArgs A;
+  int rc = make_args(desc, nullptr, nullptr, A);
+  if (rc) return rc;
+  BQ_CHECK(ctx && pbar && p && q && p_next && pbar_next && norms_out && (A.last || halo_above), BQ_EINVAL,
+           "bq_slab_dual: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  BQ_STREAM_WS(sw, ctx, st);
+  RedWs ws = red_ws(sw);
+  const int G = blocks(ctx, A.N);
+  if (desc->dtype == BQ_F32)
+    dual_kernel<float><<<G, NT, 0, st>>>(A, (const float*)pbar, (const float*)p, (const float*)q,
+                                         (const float*)halo_above, step, momentum, (float*)p_next, (float*)pbar_next,
+                                         norms_out, ws);
+  else
+    dual_kernel<double><<<G, NT, 0, st>>>(A, (const double*)pbar, (const double*)p, (const double*)q,
+                                          (const double*)halo_above, step, momentum, (double*)p_next,
+                                          (double*)pbar_next, norms_out, ws);
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}

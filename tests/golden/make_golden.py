@@ -31,8 +31,13 @@ def _import_reference():
     return tv_ops, wpm, dual_tv_solver, hessian_sr1, solvers, forward_models, oracles
 
 
-def main():
+def main(which=None):
     tv_ops, wpm, dts, sr1, solvers, fm, oracles = _import_reference()
+    if which:
+        for w in which:
+            {"config1": make_config1_golden, "config3s": make_config3_small_golden,
+             "baselines": make_baselines_golden}[w](tv_ops, wpm, solvers, fm)
+        return
     Grid, TvMode = tv_ops.Grid, tv_ops.TvMode
     out = {}
 
@@ -267,6 +272,19 @@ def make_baselines_golden(tv_ops, wpm, solvers, fm):
     print(f"wrote {OUT / 'baselines_golden.npz'} ({len(out)} arrays)")
 
 
+def scaled_adjoint_x0(views, box, N):
+    """Numpy statement of ``solvers.scaled_adjoint_initializer`` (the device
+    initial guess for the physics views): g0 = mean_rho J^T y_rho at x = 0,
+    alpha = ||g0||^2 / <g0, mean_rho J^T J g0>, x0 = clamp(alpha g0)."""
+    zero = np.zeros(N)
+    L = len(views)
+    g0 = sum(v.adjoint_vec(zero, v.y) for v in views) / L
+    hg = sum(v.adjoint_vec(zero, v.jacobian_vec(zero, g0)) for v in views) / L
+    den = float(g0 @ hg)
+    alpha = float(g0 @ g0) / den if den > 0 else 0.0
+    return np.clip(alpha * g0, box.lower, box.upper)
+
+
 def make_config1_golden(tv_ops, wpm, solvers, fm):
     """Config 1 end to end: the REFERENCE bqnpm_run driving the builder's CPU
     first-Born oracle (oracle/physics.py, complex128) through the reference's
@@ -291,13 +309,14 @@ def make_config1_golden(tv_ops, wpm, solvers, fm):
     grid = tv_ops.Grid((n, n, n))
     box = wpm.BoxSet(0.0, 0.1)
     t0 = time.time()
-    x0 = solvers.default_initializer(views, grid, box)
+    x0 = scaled_adjoint_x0(views, box, n ** 3)
     parts = solvers.partition_views(L, 4)
     alphas = solvers.estimate_subset_lipschitz(views, parts, x0, 30, 1.05, 0)
     cfg = solvers.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=20, box=box, seed=0, alphas=alphas)
     x, tr = solvers.bqnpm_run(views, grid, cfg, x0=x0, ground_truth=xgt)
     out = {"c1_y": np.array(ys), "c1_xgt": xgt, "c1_x0": x0, "c1_alphas": alphas, "c1_x": x,
-           "c1_cost": tr.column("cost"), "c1_inner": tr.column("inner_iters"), "c1_snr": tr.column("snr_db")}
+           "c1_cost": tr.column("cost"), "c1_inner": tr.column("inner_iters"), "c1_snr": tr.column("snr_db"),
+           "c1_x0_reference_initializer": solvers.default_initializer(views, grid, box)}
     np.savez_compressed(OUT / "config1_golden.npz", **out)
     print(f"wrote config1_golden.npz in {time.time() - t0:.1f} s; final SNR {tr.column('snr_db')[-1]:.2f} dB")
 
@@ -340,4 +359,4 @@ def make_config3_small_golden(tv_ops, wpm, solvers, fm):
 
 
 if __name__ == "__main__":
-    main()
+    main(sys.argv[1:])
