@@ -53,6 +53,15 @@ EXPORTS = (
     "bq_ls_grad_accum",
     "bq_ls_potential",
     "bq_cscale_real",
+    "bq_slab_div",
+    "bq_slab_newton",
+    "bq_slab_q",
+    "bq_slab_dual",
+    "bq_tv_diff",
+    "bq_tv_grad_stack",
+    "bq_tv_divergence",
+    "bq_tv_project_dual",
+    "bq_wpm_phi",
 )
 
 
@@ -108,6 +117,27 @@ class WtvReport(C.Structure):
 
 REPORT_BYTES = C.sizeof(WtvReport)
 
+
+class SlabDesc(C.Structure):
+    _fields_ = [
+        ("dtype", C.c_int32),
+        ("mode", C.c_int32),
+        ("rank", C.c_int32),
+        ("sign", C.c_int32),
+        ("K1", C.c_int64),
+        ("K2", C.c_int64),
+        ("L", C.c_int64),
+        ("first", C.c_int32),
+        ("last", C.c_int32),
+        ("tau", C.c_double),
+        ("reg", C.c_double),
+        ("lo", C.c_double),
+        ("hi", C.c_double),
+        ("d", C.c_void_p),
+        ("U", C.c_void_p),
+        ("v", C.c_void_p),
+    ]
+
 _P = C.c_void_p
 _I32 = C.c_int32
 _I64 = C.c_int64
@@ -145,6 +175,15 @@ _SIGS = {
     "bq_cscale_real": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
     "bq_ls_grad_accum": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _D, _P, _I32, _P]),
     "bq_ls_potential": (C.c_int, [_P, _I32, _I64, _P, _D, _D, _I32, _P, _P, _P]),
+    "bq_slab_div": (C.c_int, [_P, C.POINTER(SlabDesc), _P, _P, _P, _P, _P]),
+    "bq_slab_newton": (C.c_int, [_P, C.POINTER(SlabDesc), _P, C.POINTER(_D), C.POINTER(_D), _P, _P]),
+    "bq_slab_q": (C.c_int, [_P, C.POINTER(SlabDesc), _P, C.POINTER(_D), C.POINTER(_D), _P, _P]),
+    "bq_slab_dual": (C.c_int, [_P, C.POINTER(SlabDesc), _P, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
+    "bq_tv_diff": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _I32, _I32, _P, _P, _P]),
+    "bq_tv_grad_stack": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _P, _P, _P]),
+    "bq_tv_divergence": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _P, _P, _P]),
+    "bq_tv_project_dual": (C.c_int, [_P, _I32, _I32, _I64, _I32, _P, _P, _P]),
+    "bq_wpm_phi": (C.c_int, [_P, _I32, _I64, _I32, _I32, _D, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P, _P]),
 }
 
 _lib = None

@@ -26,8 +26,8 @@ import torch
 
 from . import _abi
 from ._tensors import is_torch, out_like, to_dev
-from .tv_ops import Grid, TvMode
-from .wpm import BoxSet, DiagPlusLowRank
+from .tv_ops import Grid, TvMode, dual_adjoint, dual_divergence, tv_value
+from .wpm import BoxSet, DiagPlusLowRank, apply_metric, apply_metric_inverse, wpm_box
 
 
 @dataclass
@@ -65,6 +65,69 @@ class DualSolveReport:
     converged: bool
     newton_iterations: int = 0
     beta_star: object = None
+
+
+def metric_min_eig_inverse(w: DiagPlusLowRank, iters=50, seed=0):
+    """1/lambda_min(W) by inverse power iteration through the device Woodbury
+    inverse (dual_tv_solver.py:95-116)."""
+    n = w.dim
+    if n == 0 or w.rank == 0:
+        return 1.0 / w.tau if w.d is None else w.default_omega()
+    rng = np.random.default_rng(seed)
+    v = rng.standard_normal(n)
+    v /= np.linalg.norm(v)
+    vt = to_dev(v, w.dtype, w.device)
+    mu = 1.0 / w.tau if w.d is None else w.default_omega()
+    for _ in range(iters):
+        z = apply_metric_inverse(w, vt)
+        mu = float(torch.dot(vt.double(), z.double()).item())
+        nz = float(torch.linalg.vector_norm(z.double()).item())
+        if nz == 0.0:
+            break
+        vt = z / nz
+    return mu
+
+
+def w_of_p(prob: DualTvProblem, p):
+    """Centre shift w(P) = v - reg W^-1 d(P) (dual_tv_solver.py:119-123), on the device."""
+    if prob.reg == 0.0:
+        return prob.v if is_torch(prob.v) else np.asarray(prob.v, dtype=float)
+    v = to_dev(prob.v, prob.w.dtype, prob.w.device)
+    pt = to_dev(p, prob.w.dtype, prob.w.device)
+    out = v - prob.reg * apply_metric_inverse(prob.w, dual_divergence(prob.grid, pt))
+    return out_like(prob.v, out)
+
+
+def _prox_of(prob: DualTvProblem, p, beta0=None):
+    return wpm_box(w_of_p(prob, p), prob.w, prob.box, beta0=beta0, eps=prob.newton_eps,
+                   max_iter=prob.newton_max_iter, full_output=True)
+
+
+def dual_gradient(prob: DualTvProblem, p):
+    """-2 reg [D^1 q; ...; D^d q], q = wpm_box(w(P)) (dual_tv_solver.py:138-144)."""
+    if prob.reg == 0.0:
+        z = torch.zeros(prob.grid.ndim, prob.grid.size, dtype=prob.w.dtype, device=prob.w.device)
+        return out_like(prob.v, z)
+    q, _ = _prox_of(prob, to_dev(p, prob.w.dtype, prob.w.device))
+    return out_like(prob.v, -2.0 * prob.reg * dual_adjoint(prob.grid, q))
+
+
+def dual_objective(prob: DualTvProblem, p):
+    """||w(P)||_W^2 - ||w(P) - prox(w(P))||_W^2 (dual_tv_solver.py:147-152)."""
+    wp = to_dev(w_of_p(prob, to_dev(p, prob.w.dtype, prob.w.device)), prob.w.dtype, prob.w.device)
+    q, _ = _prox_of(prob, to_dev(p, prob.w.dtype, prob.w.device))
+    diff = wp - q
+    a = torch.dot(wp.double(), apply_metric(prob.w, wp).double())
+    b = torch.dot(diff.double(), apply_metric(prob.w, diff).double())
+    return float((a - b).item())
+
+
+def primal_objective(prob: DualTvProblem, x):
+    """1/2 ||x - v||_W^2 + reg TV(x) (dual_tv_solver.py:253-260)."""
+    xt = to_dev(x, prob.w.dtype, prob.w.device)
+    diff = xt - to_dev(prob.v, prob.w.dtype, prob.w.device)
+    quad = 0.5 * float(torch.dot(diff.double(), apply_metric(prob.w, diff).double()).item())
+    return quad + prob.reg * tv_value(prob.grid, xt, prob.mode)
 
 
 def dual_step_size(prob: DualTvProblem) -> float:
@@ -198,5 +261,6 @@ def solve(prob: DualTvProblem, eps=1e-5, max_iter=100, accelerated=True) -> Dual
     )
 
 
-__all__ = ["DualTvProblem", "DualSolveReport", "dual_step_size", "solve", "solve_async",
-           "ProxWorkspace", "read_report"]
+__all__ = ["DualTvProblem", "DualSolveReport", "metric_min_eig_inverse", "w_of_p", "dual_gradient",
+           "dual_objective", "dual_step_size", "solve", "primal_objective", "solve_async", "ProxWorkspace",
+           "read_report"]

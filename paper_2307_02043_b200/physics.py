@@ -274,6 +274,44 @@ class ScatterView:
     def value(self, x):
         return float(self.viewset.costs([self.view_id], self._x(x))[0].item())
 
+    def jacobian_vec(self, x, v):
+        """J(x) v as real-packed [Re; Im] detector data (the JVP of ``forward``)."""
+        vs = self.viewset
+        xt = self._x(x)
+        vt = to_dev(v, vs.rdtype, vs.device).reshape(-1)
+        return out_like(v, vs.pack(vs.jvp([self.view_id], xt, vt))[0])
+
+    def self_check(self, n, rng, adj_tol=1e-10, grad_tol=1e-4, x_scale=0.02):
+        """The reference's plugin check (forward_models.py:66-83): adjoint identity
+        <J v, z> = <v, J^T z> and a central finite-difference gradient test,
+        same draw order from `rng` (x, v, z, then the direction).  Raises
+        RuntimeError on failure.
+
+        Differences, both forced by the physics: x is the drawn normal vector
+        times `x_scale` (x is a refractive-index contrast, O(0.01-0.1); a unit
+        contrast makes the Lippmann-Schwinger series diverge), and a complex64
+        view set checks at its own precision (adjoint >= 1e-4, gradient >= 1e-2,
+        h = 1e-3) instead of the fp64 tolerances."""
+        vs = self.viewset
+        x = rng.standard_normal(n) * x_scale
+        v = rng.standard_normal(n)
+        z = rng.standard_normal(2 * vs.n * vs.n)
+        single = vs.cdtype == torch.complex64
+        adj_tol = max(adj_tol, 1e-4) if single else adj_tol
+        grad_tol = max(grad_tol, 1e-2) if single else grad_tol
+        lhs = float(np.dot(self.jacobian_vec(x, v), z))
+        rhs = float(np.dot(v, self.adjoint_vec(x, z)))
+        if abs(lhs - rhs) > adj_tol * max(1.0, abs(lhs), abs(rhs)):
+            raise RuntimeError(f"view {self.view_id}: adjoint test failed ({lhs} vs {rhs})")
+        g = self.gradient(x)
+        h = 1e-3 * x_scale if single else 1e-6 * x_scale
+        d = rng.standard_normal(n)
+        d /= np.linalg.norm(d)
+        fd = (self.value(x + h * d) - self.value(x - h * d)) / (2 * h)
+        an = float(np.dot(g, d))
+        if abs(fd - an) > grad_tol * max(1.0, abs(fd), abs(an)):
+            raise RuntimeError(f"view {self.view_id}: gradient test failed ({an} vs {fd})")
+
     def adjoint_vec(self, x, z):
         vs = self.viewset
         xt = self._x(x)
@@ -285,9 +323,12 @@ class ScatterView:
         return out_like(z, grad)
 
 
-def make_scatter_views(n, n_views, model="ls", x_gt=None, noise_snr_db=None, seed=0, **kw):
+def make_scatter_views(n, n_views, model="ls", x_gt=None, noise_snr_db=None, seed=0, self_check=False, **kw):
     """Views with synthetic measurements y = H(x_gt) (+ complex Gaussian noise at
-    the given SNR, 20 log10(||y|| / ||e||), as forward_models.py:186-191)."""
+    the given SNR, 20 log10(||y|| / ||e||), as forward_models.py:186-191).
+    ``self_check`` runs every view's ``ViewProblem.self_check`` after the data is
+    drawn, as the reference's view factory does (forward_models.py:193); off by
+    default because at n = 128 each check is several LS solves."""
     vs = ScatterViewSet(n, n_views, model=model, **kw)
     rng = np.random.default_rng(seed)
     if x_gt is not None:
@@ -300,7 +341,11 @@ def make_scatter_views(n, n_views, model="ls", x_gt=None, noise_snr_db=None, see
                 e = rng.standard_normal(vs.y.shape[1])
                 scale = float(torch.linalg.vector_norm(vs.y[l].double()).item()) / np.linalg.norm(e)
                 vs.y[l] += to_dev(e * scale * 10.0 ** (-noise_snr_db / 20.0), vs.rdtype, vs.device)
-    return [ScatterView(vs, l) for l in range(n_views)], vs
+    views = [ScatterView(vs, l) for l in range(n_views)]
+    if self_check:
+        for view in views:
+            view.self_check(vs.N, rng)
+    return views, vs
 
 
 __all__ = ["ScatterViewSet", "ScatterView", "make_scatter_views"]

@@ -13,6 +13,9 @@ Mirror of the reference ``tvqn.wpm`` surface used on the hot path
 * ``BoxSet`` (:109-133), ``prox_box_diag`` (:136-142).
 * ``wpm_box`` (:234-253) -> ``bq_wpm_box`` (device semi-smooth Newton with
   the reference's best-residual / Levenberg rules, all decisions on device).
+* ``phi`` (:150-158) -> ``bq_wpm_phi`` (residual and generalized Jacobian in
+  one reduction pass); ``semismooth_newton`` (:170-231) is ``bq_wpm_box``'s
+  Newton returning beta; ``moreau_envelope`` (:256-260).
 
 Storage: U lives on the device as ``rank`` contiguous N-vectors (shape
 (r, N)), the coalesced layout of every kernel.
@@ -256,7 +259,65 @@ def wpm_box(x, w: DiagPlusLowRank, box: BoxSet, beta0=None, eps=1e-6, max_iter=5
     return u, info
 
 
+def _phi_call(beta, x, w: DiagPlusLowRank, box: BoxSet, jac: bool):
+    if w.rank < 1:
+        raise ValueError("phi requires a rank >= 1 metric")
+    xt = to_dev(x, w.dtype, w.device)
+    if xt.numel() != w.dim:
+        raise ValueError(f"dimension mismatch: metric is {w.dim}, vector is {xt.numel()}")
+    lo, hi, lo_a, hi_a = box.device_args(w.dtype, w.device)
+    b = to_dev(beta, torch.float64, w.device).reshape(-1)
+    if b.numel() != w.rank:
+        raise ValueError(f"beta must have {w.rank} entries")
+    out = torch.empty(w.rank, dtype=torch.float64, device=w.device)
+    h = torch.empty(w.rank, w.rank, dtype=torch.float64, device=w.device) if jac else None
+    lib = _abi.load_library()
+    _abi.check(
+        lib.bq_wpm_phi(_abi.ctx_for(w.device), _abi.dtype_code(w.dtype), xt.numel(), w.rank, w.sign,
+                       w.tau if w.d is None else 0.0, _abi.ptr(w.d), _abi.ptr(w.Ut), xt.data_ptr(), lo, hi,
+                       _abi.ptr(lo_a), _abi.ptr(hi_a), b.data_ptr(), out.data_ptr(), _abi.ptr(h),
+                       _abi.stream_ptr(w.device)),
+        "phi",
+    )
+    return out, h
+
+
+def phi(beta, x, w: DiagPlusLowRank, box: BoxSet):
+    """phi(beta) = U^T (x - clamp(x - sign D^-1 U beta)) + beta (wpm.py:150-158), on the device."""
+    out, _ = _phi_call(beta, x, w, box, False)
+    return out_like(beta if is_torch(beta) else x, out)
+
+
+def newton_matrix(beta, x, w: DiagPlusLowRank, box: BoxSet):
+    """The generalized Jacobian I + sign U_A^T D_A^-1 U_A at beta (wpm.py:161-167;
+    the reference takes the shifted point z, here beta and x define it)."""
+    _, h = _phi_call(beta, x, w, box, True)
+    return out_like(beta if is_torch(beta) else x, h)
+
+
+def semismooth_newton(x, w: DiagPlusLowRank, box: BoxSet, beta0=None, eps=1e-6, max_iter=50, full_output=False):
+    """Root of phi by the device semi-smooth Newton (wpm.py:170-231): the same
+    iteration, best-residual return and Levenberg fallback as ``wpm_box``."""
+    if w.rank < 1:
+        raise ValueError("semismooth_newton requires a rank >= 1 metric")
+    _, info = wpm_box(x, w, box, beta0=beta0, eps=eps, max_iter=max_iter, full_output=True)
+    beta = info.pop("beta")
+    return (beta, info) if full_output else beta
+
+
+def moreau_envelope(x, w: DiagPlusLowRank, box: BoxSet, **kwargs):
+    """1/2 ||u - x||_W^2 at u = wpm_box(x) (wpm.py:256-260)."""
+    xt = to_dev(x, w.dtype, w.device)
+    u = wpm_box(xt, w, box, **kwargs)
+    diff = u - xt
+    return 0.5 * float(torch.dot(diff.double(), apply_metric(w, diff).double()).item())
+
+
 __all__ = [
+    "phi",
+    "newton_matrix",
+    "semismooth_newton",
+    "moreau_envelope",
     "DiagPlusLowRank",
     "BoxSet",
     "apply_metric",

@@ -42,8 +42,9 @@ def test_struct_layout_matches_header(tmp_path):
     src = tmp_path / "layout.c"
     src.write_text(
         '#include <stdio.h>\n#include <stddef.h>\n#include "bq.h"\n'
-        "int main(void){printf(\"%zu %zu %zu %zu\\n\", sizeof(bq_wtv_desc), sizeof(bq_wtv_report),"
-        " offsetof(bq_wtv_desc, report), offsetof(bq_wtv_report, newton_residual));return 0;}\n"
+        "int main(void){printf(\"%zu %zu %zu %zu %zu %zu\\n\", sizeof(bq_wtv_desc), sizeof(bq_wtv_report),"
+        " offsetof(bq_wtv_desc, report), offsetof(bq_wtv_report, newton_residual), sizeof(bq_slab_desc),"
+        " offsetof(bq_slab_desc, tau));return 0;}\n"
     )
     exe = tmp_path / "layout"
     subprocess.run([cc, "-I", str(HEADER.parent), str(src), "-o", str(exe)], check=True)
@@ -53,4 +54,6 @@ def test_struct_layout_matches_header(tmp_path):
         ctypes.sizeof(_abi.WtvReport),
         _abi.WtvDesc.report.offset,
         _abi.WtvReport.newton_residual.offset,
+        ctypes.sizeof(_abi.SlabDesc),
+        _abi.SlabDesc.tau.offset,
     ]
