@@ -88,18 +88,24 @@ def metric_min_eig_inverse(w: DiagPlusLowRank, iters=50, seed=0):
     return mu
 
 
+def _w_of_p_dev(prob: DualTvProblem, p) -> torch.Tensor:
+    v = to_dev(prob.v, prob.w.dtype, prob.w.device)
+    if prob.reg == 0.0:
+        return v
+    pt = to_dev(p, prob.w.dtype, prob.w.device)
+    return v - prob.reg * apply_metric_inverse(prob.w, dual_divergence(prob.grid, pt))
+
+
 def w_of_p(prob: DualTvProblem, p):
     """Centre shift w(P) = v - reg W^-1 d(P) (dual_tv_solver.py:119-123), on the device."""
-    if prob.reg == 0.0:
-        return prob.v if is_torch(prob.v) else np.asarray(prob.v, dtype=float)
-    v = to_dev(prob.v, prob.w.dtype, prob.w.device)
-    pt = to_dev(p, prob.w.dtype, prob.w.device)
-    out = v - prob.reg * apply_metric_inverse(prob.w, dual_divergence(prob.grid, pt))
-    return out_like(prob.v, out)
+    if prob.reg == 0.0 and not is_torch(prob.v):
+        return np.asarray(prob.v, dtype=float)
+    return out_like(prob.v, _w_of_p_dev(prob, p))
 
 
 def _prox_of(prob: DualTvProblem, p, beta0=None):
-    return wpm_box(w_of_p(prob, p), prob.w, prob.box, beta0=beta0, eps=prob.newton_eps,
+    """(q, info) with q a device tensor."""
+    return wpm_box(_w_of_p_dev(prob, p), prob.w, prob.box, beta0=beta0, eps=prob.newton_eps,
                    max_iter=prob.newton_max_iter, full_output=True)
 
 
@@ -114,7 +120,7 @@ def dual_gradient(prob: DualTvProblem, p):
 
 def dual_objective(prob: DualTvProblem, p):
     """||w(P)||_W^2 - ||w(P) - prox(w(P))||_W^2 (dual_tv_solver.py:147-152)."""
-    wp = to_dev(w_of_p(prob, to_dev(p, prob.w.dtype, prob.w.device)), prob.w.dtype, prob.w.device)
+    wp = _w_of_p_dev(prob, p)
     q, _ = _prox_of(prob, to_dev(p, prob.w.dtype, prob.w.device))
     diff = wp - q
     a = torch.dot(wp.double(), apply_metric(prob.w, wp).double())

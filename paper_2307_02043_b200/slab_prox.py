@@ -1,0 +1,406 @@
+"""z-slab-sharded weighted-TV prox (north star (4); config 5).
+
+The FGP dual iteration of ``tvqn.dual_tv_solver.solve``
+(``/root/reference/pkg/src/tvqn/dual_tv_solver.py:161-250``) with its
+structured projection (``wpm.py:145-253``) over a 3-D volume split along
+dims[2] into contiguous slabs of planes, one slab per GPU.  Per FGP
+iteration and rank (``csrc/slab_prox.cu`` passes, host control here):
+
+  1. ``bq_slab_div``    t = D^-1 div(Pbar) over the slab; needs Pbar_z of the
+                        plane just below the slab (1-plane halo from rank-1)
+                        -> all-reduce s = U^T t (r doubles); c = cap^-1 s
+  2. ``bq_slab_newton`` Newton residual / Jacobian at beta -> all-reduce of
+                        r + r(r+1)/2 doubles per Newton step; the controller
+                        (accept, best residual, Levenberg) runs identically
+                        on every rank on the all-reduced scalars
+  3. ``bq_slab_q``      q = clamp(z(beta*)); q of the plane just above the slab
+                        comes from rank+1 (1-plane halo)
+  4. ``bq_slab_dual``   P_next, Pbar_next and the two norms -> all-reduce of 2
+                        doubles; the rel-change stop and the FISTA t-sequence
+                        are decided on the all-reduced values
+
+Communication budget per FGP iteration at K1 x K2 planes of s-byte words:
+two halo planes (Pbar_z up, q down; 2 K1 K2 s bytes each way), and
+2 + (newton steps + 1) all-reduces of <= 46 doubles.  At 256^3 fp32 the
+halos are 256 KB per neighbour per iteration.
+
+Sharding is by slabs of one process: ``SlabGroup`` holds the slabs this
+process owns (one per rank under torchrun; several in one process for the
+single-GPU loopback test) and reduces their partials locally before the
+cross-process all-reduce, so the same control code runs in every layout.
+The per-slab compute is a backend object: ``DeviceSlabs`` (libbq, the
+product path) -- the CPU tests plug a numpy backend into the same control
+code to check it with gloo.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _abi
+from ._tensors import to_dev
+from .tv_ops import TvMode
+
+_LEVENBERG = 1e-8  # wpm.py:21
+
+
+def slab_bounds(k3: int, world: int):
+    """Contiguous plane ranges [z0, z1) per rank (sizes differ by <= 1)."""
+    base, extra = divmod(k3, world)
+    out, z = [], 0
+    for r in range(world):
+        n = base + (1 if r < extra else 0)
+        out.append((z, z + n))
+        z += n
+    return out
+
+
+@dataclass
+class SlabReport:
+    x: torch.Tensor            # this process's slabs of x, concatenated along z
+    p_star: torch.Tensor       # (3, local N)
+    iterations: int
+    rel_change: float
+    converged: bool
+    newton_iterations: int
+    beta_star: np.ndarray
+
+
+class Comm:
+    """Cross-process steps: all-reduce(sum) of small vectors, plane exchange with
+    the neighbouring ranks.  world == 1 (or no process group): no-ops."""
+
+    def __init__(self, group=None):
+        self.group = group
+        if dist.is_available() and dist.is_initialized():
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        else:
+            self.rank, self.world = 0, 1
+
+    def allreduce(self, t: torch.Tensor) -> torch.Tensor:
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+        return t
+
+    def _peer(self, r):
+        return dist.get_global_rank(self.group, r) if self.group is not None else r
+
+    def shift(self, send: torch.Tensor, recv: torch.Tensor, up: bool):
+        """Send `send` to rank+1 (up) or rank-1 (down) and receive the matching plane
+        from the opposite neighbour into `recv` (edge ranks skip the missing side)."""
+        if self.world == 1:
+            return
+        ops = []
+        dst = self.rank + 1 if up else self.rank - 1
+        src = self.rank - 1 if up else self.rank + 1
+        if 0 <= dst < self.world:
+            ops.append(dist.P2POp(dist.isend, send.contiguous(), self._peer(dst), self.group))
+        if 0 <= src < self.world:
+            ops.append(dist.P2POp(dist.irecv, recv, self._peer(src), self.group))
+        if ops:
+            for req in dist.batch_isend_irecv(ops):
+                req.wait()
+
+
+class SlabGroup:
+    """The slabs one process owns, with their global placement.
+
+    `slabs` are consecutive in z; slab i of this process covers planes
+    bounds[i].  A backend implements the four passes on one slab."""
+
+    def __init__(self, backend, comm: Comm, dims, bounds, k3):
+        self.be, self.comm = backend, comm
+        self.dims, self.bounds, self.k3 = tuple(dims), list(bounds), int(k3)
+        self.plane = dims[0] * dims[1]
+
+    # ---- cross-slab plumbing -------------------------------------------------
+    def reduce(self, parts):
+        """Sum of per-slab partial vectors (local slab order), then across ranks."""
+        tot = parts[0].clone()
+        for p in parts[1:]:
+            tot += p
+        return self.comm.allreduce(tot)
+
+    def halo_up(self, planes):
+        """planes[i] = the top plane slab i sends upward; returns, per slab, the plane
+        received from below (None for the global first slab)."""
+        n = len(planes)
+        out = [None] * n
+        for i in range(1, n):
+            out[i] = planes[i - 1]
+        if self.comm.world > 1:
+            recv = torch.empty_like(planes[0])
+            self.comm.shift(planes[-1], recv, up=True)
+            if self.bounds[0][0] > 0:
+                out[0] = recv
+        return out
+
+    def halo_down(self, planes):
+        """planes[i] = the bottom plane slab i sends downward; returns, per slab, the
+        plane received from above (None for the global last slab)."""
+        n = len(planes)
+        out = [None] * n
+        for i in range(n - 1):
+            out[i] = planes[i + 1]
+        if self.comm.world > 1:
+            recv = torch.empty_like(planes[0])
+            self.comm.shift(planes[0], recv, up=False)
+            if self.bounds[-1][1] < self.k3:
+                out[-1] = recv
+        return out
+
+
+def _newton(sg: SlabGroup, t, c, beta, rank, sign, tau, scalar, eps, max_iter):
+    """Semi-smooth Newton of wpm.py:170-231 on all-reduced residuals."""
+    best_res, best_beta = math.inf, beta
+    conv = False
+    iters = 0
+    tri = [(i, j) for i in range(rank) for j in range(i + 1)]
+    for iters in range(max_iter + 1):
+        part = sg.reduce([sg.be.newton(s, t[s], c, beta) for s in range(len(t))]).cpu().numpy()
+        res_vec = part[:rank] + beta
+        res = float(np.linalg.norm(res_vec))
+        if res < best_res:
+            best_res, best_beta = res, beta
+        if res <= eps:
+            conv = True
+            break
+        if iters == max_iter:
+            break
+        g = np.zeros((rank, rank))
+        for k, (i, j) in enumerate(tri):
+            g[i, j] = g[j, i] = part[rank + k]
+        h = np.eye(rank) + sign * (g / tau if scalar else g)
+        try:
+            step = np.linalg.solve(h, res_vec)
+        except np.linalg.LinAlgError:
+            mu = _LEVENBERG * np.linalg.norm(h, np.inf)
+            step = np.linalg.solve(h + mu * np.eye(rank), res_vec)
+        beta = beta - step
+    return best_beta, iters, best_res, conv
+
+
+def slab_solve(sg: SlabGroup, *, rank, sign, tau, scalar, gram, reg, step, eps=1e-5, max_iter=100,
+               accelerated=True, newton_eps=1e-6, newton_max_iter=50, beta0=None, p0=None):
+    """FGP loop of dual_tv_solver.py:161-250 over the slabs of `sg` (every rank
+    calls it with its own slabs; all control decisions are replicated)."""
+    if eps <= 0:
+        raise ValueError("eps must be positive")
+    if max_iter < 1:
+        raise ValueError("max_iter must be >= 1")
+    be = sg.be
+    ns = len(sg.bounds)
+    beta = np.zeros(rank) if (beta0 is None or np.shape(beta0)[0] != rank) else np.asarray(beta0, float).copy()
+    cap_l = None
+    if rank:
+        cap = np.eye(rank) + sign * (gram / tau if scalar else gram)
+        cap_l = np.linalg.cholesky(cap)
+
+    def coef(field, halos):
+        """t = D^-1 div(field) per slab and c = cap^-1 U^T t (global)."""
+        out = [be.div(s, field[s], halos[s]) for s in range(ns)]
+        t = [o[0] for o in out]
+        if rank:
+            sv = sg.reduce([o[1] for o in out]).cpu().numpy()
+            c = np.linalg.solve(cap_l.T, np.linalg.solve(cap_l, sv))
+        else:
+            c = np.zeros(0)
+        return t, c
+
+    def prox_of(field, beta):
+        if reg == 0.0:
+            t = [be.zeros(s) for s in range(ns)]
+            c = np.zeros(rank)
+        else:
+            halos = sg.halo_up([be.top_plane_z(field[s]) for s in range(ns)])
+            t, c = coef(field, halos)
+        if rank:
+            beta, it, res, conv = _newton(sg, t, c, beta, rank, sign, tau, scalar, newton_eps, newton_max_iter)
+        else:
+            it, res, conv = 0, 0.0, True
+        q = [be.q(s, t[s], c, beta) for s in range(ns)]
+        return q, beta, it, res, conv
+
+    p = [be.dual_field(s, None if p0 is None else p0[s]) for s in range(ns)]
+    if reg == 0.0:
+        q, beta, it, _, _ = prox_of(p, beta)
+        return SlabReport(x=be.concat(q), p_star=be.concat_dual(p), iterations=1, rel_change=0.0, converged=True,
+                          newton_iterations=it, beta_star=beta)
+    pbar = [x.clone() for x in p]
+    tk = 1.0
+    newton_total = 0
+    rel = math.inf
+    converged = False
+    iterations = 0
+    for iterations in range(1, max_iter + 1):
+        q, beta, it, _, _ = prox_of(pbar, beta)
+        newton_total += it
+        qh = sg.halo_down([be.bottom_plane(q[s]) for s in range(ns)])
+        t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * tk * tk))
+        mom = (tk - 1.0) / t_next if accelerated else 0.0
+        outs = [be.dual(s, pbar[s], p[s], q[s], qh[s], step, mom) for s in range(ns)]
+        norms = sg.reduce([o[2] for o in outs]).cpu().numpy()
+        num, den = math.sqrt(norms[0]), math.sqrt(norms[1])
+        rel = 0.0 if num == 0.0 else (num / den if den > 0.0 else math.inf)
+        p = [o[0] for o in outs]
+        if rel < eps:
+            converged = True
+            break
+        pbar = [o[1] for o in outs]
+        tk = t_next if accelerated else tk
+    q, beta, it, _, _ = prox_of(p, beta)
+    newton_total += it
+    return SlabReport(x=be.concat(q), p_star=be.concat_dual(p), iterations=iterations, rel_change=float(rel),
+                      converged=converged, newton_iterations=newton_total, beta_star=beta)
+
+
+class DeviceSlabs:
+    """libbq passes (csrc/slab_prox.cu) on this process's slabs.
+
+    v_parts / d_parts / U_parts: per slab, the local v (N_s), the optional
+    per-voxel diagonal (N_s) and U as (rank, N_s) -- device tensors of one
+    dtype; planes are contiguous, so a slab is a contiguous range of the
+    global flat vector."""
+
+    def __init__(self, dims, bounds, k3, dtype, device, v_parts, U_parts, d_parts=None, *, rank, sign, tau, reg,
+                 lo, hi, mode=TvMode.ISOTROPIC):
+        self.K1, self.K2 = int(dims[0]), int(dims[1])
+        self.plane = self.K1 * self.K2
+        self.dtype, self.device = dtype, device
+        self.lib = _abi.load_library()
+        self.ctx = _abi.ctx_for(device)
+        self.v = [to_dev(v, dtype, device) for v in v_parts]
+        self.U = [to_dev(u, dtype, device).reshape(rank, -1).contiguous() if rank else None for u in U_parts]
+        self.d = [to_dev(d, dtype, device) if d is not None else None for d in (d_parts or [None] * len(bounds))]
+        self.descs = []
+        for s, (z0, z1) in enumerate(bounds):
+            D = _abi.SlabDesc()
+            D.dtype = _abi.dtype_code(dtype)
+            D.mode = TvMode.parse(mode).code
+            D.rank, D.sign = rank, sign
+            D.K1, D.K2, D.L = self.K1, self.K2, z1 - z0
+            D.first, D.last = int(z0 == 0), int(z1 == k3)
+            D.tau = float(tau) if self.d[s] is None else 0.0
+            D.reg, D.lo, D.hi = float(reg), float(lo), float(hi)
+            D.d = _abi.ptr(self.d[s])
+            D.U = _abi.ptr(self.U[s])
+            D.v = self.v[s].data_ptr()
+            self.descs.append(D)
+        self.rank = rank
+        self._dots = torch.empty(len(bounds), 64, dtype=torch.float64, device=device)
+
+    def _st(self):
+        return _abi.stream_ptr(self.device)
+
+    def _n(self, s):
+        return self.v[s].numel()
+
+    @staticmethod
+    def _arr(vals):
+        return (C_DOUBLE8)(*(list(vals) + [0.0] * (8 - len(vals))))
+
+    def zeros(self, s):
+        return torch.zeros(self._n(s), dtype=self.dtype, device=self.device)
+
+    def dual_field(self, s, init):
+        if init is None:
+            return torch.zeros(3, self._n(s), dtype=self.dtype, device=self.device)
+        return to_dev(init, self.dtype, self.device).reshape(3, self._n(s)).clone()
+
+    def top_plane_z(self, field):
+        return field[2, -self.plane:].contiguous()
+
+    def bottom_plane(self, q):
+        return q[: self.plane].contiguous()
+
+    def div(self, s, field, halo):
+        t = torch.empty(self._n(s), dtype=self.dtype, device=self.device)
+        sv = self._dots[s, :8]
+        _abi.check(self.lib.bq_slab_div(self.ctx, self.descs[s], field.data_ptr(), _abi.ptr(halo), t.data_ptr(),
+                                        sv.data_ptr() if self.rank else None, self._st()), "slab div")
+        return t, sv[: self.rank].clone()
+
+    def newton(self, s, t, c, beta):
+        nv = self.rank + self.rank * (self.rank + 1) // 2
+        out = self._dots[s, 8:8 + nv]
+        _abi.check(self.lib.bq_slab_newton(self.ctx, self.descs[s], t.data_ptr(), self._arr(c), self._arr(beta),
+                                           out.data_ptr(), self._st()), "slab newton")
+        return out.clone()
+
+    def q(self, s, t, c, beta):
+        q = torch.empty(self._n(s), dtype=self.dtype, device=self.device)
+        _abi.check(self.lib.bq_slab_q(self.ctx, self.descs[s], t.data_ptr(), self._arr(c), self._arr(beta),
+                                      q.data_ptr(), self._st()), "slab q")
+        return q
+
+    def dual(self, s, pbar, p, q, halo, step, mom):
+        pn = torch.empty_like(p)
+        pbn = torch.empty_like(p)
+        nrm = self._dots[s, 60:62]
+        _abi.check(self.lib.bq_slab_dual(self.ctx, self.descs[s], pbar.data_ptr(), p.data_ptr(), q.data_ptr(),
+                                         _abi.ptr(halo), float(step), float(mom), pn.data_ptr(), pbn.data_ptr(),
+                                         nrm.data_ptr(), self._st()), "slab dual")
+        return pn, pbn, nrm.clone()
+
+    def concat(self, parts):
+        return torch.cat(parts)
+
+    def concat_dual(self, parts):
+        return torch.cat(parts, dim=1)
+
+
+import ctypes as _C  # noqa: E402
+
+C_DOUBLE8 = _C.c_double * 8
+
+
+def solve_sharded(grid, v, w, reg, box, *, group=None, slabs_per_rank=1, mode=TvMode.ISOTROPIC, omega=None,
+                  eps=1e-5, max_iter=100, accelerated=True, newton_eps=1e-6, newton_max_iter=50, beta0=None,
+                  dtype=None, device=None):
+    """Sharded counterpart of ``dual_tv_solver.solve`` for a 3-D grid.
+
+    Every rank of `group` passes the same GLOBAL problem description (grid, and
+    v / w / box as full arrays it can slice, or device tensors) and gets back
+    its own slabs of x and P*.  `slabs_per_rank` > 1 splits each rank's share
+    further (the single-GPU loopback layout).  Box bounds must be scalars.
+    Returns (SlabReport, [(z0, z1) per local slab])."""
+    from .wpm import DiagPlusLowRank  # noqa: F401  (type of w)
+
+    if grid.ndim != 3:
+        raise ValueError("the z-slab prox shards 3-D grids")
+    if isinstance(box.lower, np.ndarray) or isinstance(box.upper, np.ndarray):
+        raise ValueError("the z-slab prox takes scalar box bounds")
+    comm = Comm(group)
+    k1, k2, k3 = grid.dims
+    allb = slab_bounds(k3, comm.world * slabs_per_rank)
+    mine = allb[comm.rank * slabs_per_rank:(comm.rank + 1) * slabs_per_rank]
+    if any(z1 <= z0 for z0, z1 in mine):
+        raise ValueError(f"{k3} planes cannot give every slab at least one plane")
+    dtype = dtype or w.dtype
+    device = device or w.device
+    plane = k1 * k2
+    vt = to_dev(v, dtype, device)
+    v_parts = [vt[z0 * plane:z1 * plane] for z0, z1 in mine]
+    U_parts = [w.Ut[:, z0 * plane:z1 * plane] if w.rank else None for z0, z1 in mine]
+    d_parts = [w.d[z0 * plane:z1 * plane] for z0, z1 in mine] if w.d is not None else None
+    gram = None
+    if w.rank:
+        gram = w.gram.reshape(w.rank, w.rank).cpu().numpy()  # U^T D^-1 U (global, from the metric)
+    be = DeviceSlabs(grid.dims, mine, k3, dtype, device, v_parts, U_parts, d_parts, rank=w.rank, sign=w.sign,
+                     tau=w.tau if w.d is None else 1.0, reg=reg, lo=box.lower, hi=box.upper, mode=mode)
+    if omega is None:
+        omega = w.default_omega()
+    step = 1.0 / (4.0 * 3 * omega * reg) if reg > 0 else 0.0
+    sg = SlabGroup(be, comm, grid.dims, mine, k3)
+    rep = slab_solve(sg, rank=w.rank, sign=w.sign, tau=w.tau if w.d is None else 1.0, scalar=w.d is None,
+                     gram=gram, reg=reg, step=step, eps=eps, max_iter=max_iter, accelerated=accelerated,
+                     newton_eps=newton_eps, newton_max_iter=newton_max_iter, beta0=beta0)
+    return rep, mine
+
+
+__all__ = ["slab_bounds", "Comm", "SlabGroup", "slab_solve", "DeviceSlabs", "solve_sharded", "SlabReport"]

@@ -38,6 +38,8 @@ class TvMode(enum.Enum):
     def parse(cls, value):
         if isinstance(value, TvMode):
             return value
+        if isinstance(value, enum.Enum):  # e.g. the reference's own tvqn.tv_ops.TvMode (drop-in)
+            value = value.value
         table = {
             "iso": cls.ISOTROPIC,
             "isotropic": cls.ISOTROPIC,

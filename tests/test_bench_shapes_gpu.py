@@ -41,12 +41,12 @@ def _probe(n):
     return np.random.default_rng(PROBE_SEED).integers(0, 2, n).astype(float) * 2.0 - 1.0
 
 
-def check_summary(z, prefix, got, tol):
+def check_summary(z, prefix, got, tol, stride=STRIDE):
     """Strided-sample relative L2 <= tol, |norm| and |sum| relative <= tol, and the
     random-sign probe within 10 sigma of a tol-sized error (std of sum s_i e_i = ||e||)."""
     got = np.asarray(got, dtype=float).reshape(-1)
     ref_norm = float(z[prefix + "_norm"])
-    assert rel_l2(got[::STRIDE], z[prefix + "_sample"]) <= tol
+    assert rel_l2(got[::stride], z[prefix + "_sample"]) <= tol
     assert abs(np.linalg.norm(got) - ref_norm) <= tol * ref_norm
     assert abs(got.sum() - float(z[prefix + "_sum"])) <= 10 * tol * ref_norm
     assert abs(got @ _probe(got.size) - float(z[prefix + "_probe"])) <= 10 * tol * ref_norm
@@ -78,14 +78,14 @@ def test_config2_headline_fp32_vs_port(prox128, config2):
     rep = D.solve(_config2_problem(config2, torch.float32), eps=1e-300, max_iter=100)
     assert rep.iterations == 100
     check_summary(prox128, "diag_x", rep.x.double().cpu().numpy(), 1e-4)
-    check_summary(prox128, "diag_p", rep.p_star.double().cpu().numpy(), 1e-4)
+    check_summary(prox128, "diag_p", rep.p_star.double().cpu().numpy(), 1e-4, stride=3 * STRIDE)
     assert float(rep.x.min()) >= 0.0
 
 
 def test_config2_fp64_twin_vs_port(prox128, config2):
     rep = D.solve(_config2_problem(config2, torch.float64), eps=1e-300, max_iter=100)
     check_summary(prox128, "diag_x", rep.x.cpu().numpy(), 1e-10)
-    check_summary(prox128, "diag_p", rep.p_star.cpu().numpy(), 1e-10)
+    check_summary(prox128, "diag_p", rep.p_star.cpu().numpy(), 1e-10, stride=3 * STRIDE)
     assert rep.newton_iterations == int(prox128["diag_newton"])
     assert abs(float(rep.beta_star[0]) - float(prox128["diag_beta"][0])) <= 1e-8 * max(1.0, abs(float(prox128["diag_beta"][0])))
 
@@ -95,7 +95,7 @@ def test_config2_scalar_tau_twin_vs_reference_solve(prox128, config2, dtype, tol
     """W = 1.25 I + u u^T at 128^3: the reference's own solve is the fixture."""
     rep = D.solve(_config2_problem(config2, dtype, twin=True), eps=1e-300, max_iter=100)
     check_summary(prox128, "twin_x", rep.x.double().cpu().numpy(), tol)
-    check_summary(prox128, "twin_p", rep.p_star.double().cpu().numpy(), tol)
+    check_summary(prox128, "twin_p", rep.p_star.double().cpu().numpy(), tol, stride=3 * STRIDE)
     if dtype == torch.float64:
         assert rep.newton_iterations == int(prox128["twin_newton"])
 
