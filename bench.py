@@ -8,9 +8,13 @@ A "step" is one full prox solve (one persistent-kernel launch).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--n 128]
 
---impl reference times the CPU restatement of the reference algorithm
-(oracle/prox.py, the reference package itself cannot travel to the GPU box)
-on a bounded sample of the same workload; under torchrun only rank 0 runs it.
+--impl reference times the reference algorithm on the host cores: each step
+is one WHOLE 100-iteration solve of the same config-2 workload by the numpy
+port (oracle/prox.py: the reference's dual_tv_solver.solve extended to the
+per-voxel diagonal, which the reference cannot represent), one solve per core
+in parallel worker processes; beside it, the unmodified reference
+tvqn.dual_tv_solver.solve (installed under baseline/_ref) on the scalar-tau
+twin.  Under torchrun only rank 0 runs it.
 """
 
 from __future__ import annotations
@@ -133,53 +137,141 @@ def dist_env():
 
 
 # ---------------------------------------------------------------------------
-# reference arm: CPU restatement on the host cores
+# CPU legs: whole 100-iteration solves on all host cores
 # ---------------------------------------------------------------------------
-def cpu_prox_sample(inp, iters: int):
-    from oracle import prox as O
+_CPU = {}
 
+
+def _cpu_init(n, kind, barrier):
+    """Pool initializer: one BLAS thread per process (the work is elementwise; the
+    parallelism is one solve per core), inputs built once per worker."""
+    try:
+        from threadpoolctl import threadpool_limits
+
+        threadpool_limits(1)
+    except Exception:
+        pass
+    from paper_2307_02043_b200.configs import config2_inputs
+
+    _CPU["inp"] = config2_inputs(n)
+    _CPU["kind"] = kind
+    _CPU["barrier"] = barrier
+
+
+def _cpu_solve(_):
+    """One whole solve: 'port' = oracle/prox.py on the config-2 metric
+    diag(d) + u u^T; 'reference' = the unmodified tvqn.dual_tv_solver.solve
+    (baseline/_ref) on the scalar-tau twin 1.25 I + u u^T (the reference cannot
+    represent a per-voxel diagonal)."""
+    inp = _CPU["inp"]
     n = inp["n"]
-    w = O.Metric(U=inp["u"][:, None], d=inp["d"])
-    t0 = time.perf_counter()
-    O.fgp_prox((n, n, n), inp["v"], w, reg=inp["reg"], eps=1e-300, max_iter=iters)
-    dt = time.perf_counter() - t0
-    return n ** 3 * iters / dt, dt
+    if _CPU.get("barrier") is not None:
+        try:
+            _CPU["barrier"].wait(timeout=600)
+        except Exception:
+            pass
+        _CPU["barrier"] = None  # only the first round starts together
+    t0 = time.time()
+    if _CPU["kind"] == "port":
+        from oracle import prox as O
+
+        r = O.fgp_prox((n, n, n), inp["v"], O.Metric(U=inp["u"][:, None], d=inp["d"]), reg=inp["reg"],
+                       eps=1e-300, max_iter=inp["iters"])
+        its = r["iterations"]
+    else:
+        sys.path.insert(0, str(ROOT / "baseline" / "_ref"))
+        from tvqn import dual_tv_solver as DTS
+        from tvqn.tv_ops import Grid
+        from tvqn.wpm import BoxSet, DiagPlusLowRank
+
+        prob = DTS.DualTvProblem(grid=Grid((n, n, n)), v=inp["v"], w=DiagPlusLowRank(inp["tau_twin"], inp["u"][:, None]),
+                                 reg=inp["reg"], box=BoxSet(0.0, np.inf))
+        its = DTS.solve(prob, eps=1e-300, max_iter=inp["iters"]).iterations
+    return t0, time.time(), int(its)
+
+
+def host_facts():
+    facts = {"os_cpu_count": os.cpu_count()}
+    try:
+        facts["affinity"] = sorted(os.sched_getaffinity(0))
+    except Exception:
+        facts["affinity"] = None
+    try:
+        from threadpoolctl import threadpool_info
+
+        facts["threadpoolctl"] = [{k: i.get(k) for k in ("internal_api", "num_threads", "version")}
+                                  for i in threadpool_info()]
+    except Exception as exc:
+        facts["threadpoolctl"] = f"unavailable: {exc}"
+    try:
+        facts["cpu_model"] = next(line.split(":", 1)[1].strip() for line in open("/proc/cpuinfo")
+                                  if line.startswith("model name"))
+    except Exception:
+        pass
+    return facts
+
+
+def cpu_whole_solves(n, kind, solves, procs=None):
+    """`solves` whole 100-iteration solves of `kind` over `procs` worker processes
+    (default: every core in the affinity mask), one BLAS thread each.  The first
+    round starts behind a barrier; returns (voxel*iter/s over the wall span from
+    the first start to the last end, per-solve seconds, procs)."""
+    import multiprocessing as mp
+
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:
+        cores = os.cpu_count() or 1
+    solves = solves or cores
+    procs = max(1, min(procs or cores, solves))
+    ctx = mp.get_context("spawn")
+    with ctx.Manager() as mgr:
+        barrier = mgr.Barrier(procs)
+        with ctx.Pool(procs, initializer=_cpu_init, initargs=(n, kind, barrier)) as pool:
+            res = pool.map(_cpu_solve, range(solves), chunksize=1)
+    t0 = min(r[0] for r in res)
+    t1 = max(r[1] for r in res)
+    iters = sum(r[2] for r in res)
+    return n ** 3 * iters / (t1 - t0), [r[1] - r[0] for r in res], procs
 
 
 def run_reference(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    from paper_2307_02043_b200.configs import config2_inputs
-
-    inp = config2_inputs(args.n)
-    vals = []
-    sample_iters = args.cpu_iters
-    for _ in range(args.warmup):
-        cpu_prox_sample(inp, 1)
-    t_all = time.perf_counter()
-    for _ in range(args.steps):
-        v, _ = cpu_prox_sample(inp, sample_iters)
-        vals.append(v)
-    wall = time.perf_counter() - t_all
-    value = float(np.median(vals))
-    sample = f"config-2 prox {args.n}^3 f64 diag(d)+uu^T, {sample_iters} FGP iterations per step (numpy port)"
+    n = args.n
+    solves = max(1, args.steps)
+    value, per, procs = cpu_whole_solves(n, "port", solves)
+    ref_twin = None
+    if (ROOT / "baseline" / "_ref" / "tvqn").exists():
+        tv, tper, tprocs = cpu_whole_solves(n, "reference", procs)
+        ref_twin = {"value": tv, "unit": UNIT, "solves": len(tper), "median_s_per_solve": float(np.median(tper)),
+                    "cores": tprocs, "kind": "reference",
+                    "workload": f"the UNMODIFIED tvqn.dual_tv_solver.solve (baseline/_ref) on the scalar-tau twin "
+                                f"W = 1.25 I + u u^T of config 2, {n}^3 f64, 100 FGP iterations"}
+    sample = (f"{solves} whole config-2 solves ({n}^3 f64 diag(d)+uu^T, 100 FGP iterations each; numpy port "
+              f"oracle/prox.py, the reference algorithm extended to diag(d)) on {procs} worker processes, one BLAS "
+              f"thread each; median {np.median(per):.1f} s per solve")
     line = {
         "impl": "reference",
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * wall / max(args.steps, 1), "higher_is_better": True,
+        "warmup": args.warmup, "ms_per_step": 1e3 * float(np.median(per)), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (seeded config-2 box phantom + N(0,1) noise)",
-        # the same workload as the device arm (a voxel*iter of one 100-iteration solve);
-        # each step times a bounded sample of its FGP iterations
-        "config": {"workload": f"config2 wTV prox {args.n}^3 W=diag(d)+uu^T iso TV reg 0.05 box [0,inf), "
-                               f"100 FGP iterations per step",
-                   "sample_iters_per_step": sample_iters, "parallelism": "host cores x1 (numpy port)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "port", "sample": sample},
+        "config": config2_config(n, 100),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": "port", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "reference_twin": ref_twin,
+        "host": host_facts(),
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+
+
+def config2_config(n, iters):
+    """The workload description both arms print (identical, so the configs compare equal)."""
+    return {"workload": f"config2 wTV prox {n}^3 W=diag(d)+uu^T iso TV reg 0.05 box [0,inf), "
+                        f"{iters} FGP iterations per step"}
 
 
 # ---------------------------------------------------------------------------
@@ -372,9 +464,14 @@ def run_ours(args):
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e = float(t.item())
 
-    ls = None
+    ls = ls5 = None
     if not args.no_ls:
-        ls = ls_measure(args, dev, ws)  # collective at N > 1
+        ls = ls_measure(args, dev, ws, config=4)  # collective at N > 1
+        if not args.no_ls5:
+            ls5 = ls_measure(args, dev, ws, config=5)
+    sharded = None
+    if not args.no_sharded:
+        sharded = prox_sharded_measure(dev, ws)  # halo exchange + all-reduces at N > 1
     more = None
     if rank == 0 and not args.no_more:
         more = prox_variants(dev, flush)
@@ -398,18 +495,19 @@ def run_ours(args):
                 traffic = None
         cpu = None
         if ws == 1 and not args.no_cpu:
-            inp64 = inp
-            cv, cdt = cpu_prox_sample(inp64, args.cpu_iters)
-            cpu = {"value": cv, "unit": UNIT, "cores": 1, "kind": "port",
-                   "sample": f"config-2 prox {n}^3 f64 diag(d)+uu^T, {args.cpu_iters} FGP iterations "
-                             f"(numpy port, {cdt:.1f} s)"}
+            cv, per, procs = cpu_whole_solves(n, "port", args.cpu_solves)
+            cpu = {"value": cv, "unit": UNIT, "cores": procs, "kind": "port",
+                   "sample": f"{len(per)} whole config-2 solves ({n}^3 f64 diag(d)+uu^T, 100 FGP iterations; numpy "
+                             f"port oracle/prox.py) on {procs} worker processes, one BLAS thread each; median "
+                             f"{np.median(per):.1f} s per solve",
+                   "host": host_facts()}
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": max(args.warmup, 3), "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic (seeded config-2 box phantom + N(0,1) noise)",
-            "config": {"workload": f"config2 wTV prox {n}^3 W=diag(d)+uu^T iso TV reg 0.05 box [0,inf), "
-                                   f"{iters} FGP iterations per step",
-                       "l2": "flushed (256 MB write) between timed steps", "parallelism": f"replicas x{ws}"},
+            "config": config2_config(n, iters),
+            "l2": "flushed (256 MB write) between timed steps",
+            "parallelism": f"replicas x{ws} (the prox is replicated on every rank; SURVEY 8e)",
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
                          "peak_source": peak_kind, "algorithmic_bytes_per_voxel_iter": bpv},
@@ -423,6 +521,8 @@ def run_ours(args):
                     "serial_ms_per_step": e2e_serial},
             "gpu_launches": args.steps,
             "ls": ls,
+            "ls_config5": ls5,
+            "prox_sharded": sharded,
             "prox_more": more,
             "bqnpm_loop": loop,
             "clocks": sampler.summary(),
@@ -489,24 +589,37 @@ def prox_variants(dev, flush):
     return out
 
 
-def ls_measure(args, dev, ws=1):
+LS_CONFIGS = {
+    # config 4: n = 128 (padded 256^3), L = 64 on a 40 deg cone, 12 ellipsoids dn ~ U[0.01, 0.1], 25 dB,
+    # one 16-view subset (K_s = 4)
+    4: dict(n=128, L=64, theta=40.0, batch=16, subset=16, phantom=("ellipsoids", 12, 0.01, 0.1, 4000), seed=4001),
+    # config 5: n = 256 (padded 512^3), L = 120, cell-like nested ellipsoids dn ~ U[0.005, 0.06], 25 dB,
+    # one 30-view subset (K_s = 4)
+    5: dict(n=256, L=120, theta=40.0, batch=30, subset=30, phantom=("cell", 0, 0.005, 0.06, 5000), seed=5001),
+}
+
+
+def ls_measure(args, dev, ws=1, config=4):
     """Secondary metric (BASELINE 'views*voxels/s of LS forward+adjoint'): one
-    subset gradient of config 4 (n=128 padded to 256^3, c64, 16 of 64 views on a
-    40 deg cone, 12 ellipsoids dn~U[0.01,0.1], 25 dB) at x = x_gt / 2."""
+    subset gradient of an LS configuration (LS_CONFIGS) at x = x_gt / 2, c64,
+    BiCGSTAB tol 1e-6.  N > 1: view-sharded -- each rank takes a
+    contiguous chunk of the subset, one NCCL all-reduce of the N-vector
+    gradient; the time is the max over ranks."""
     import torch
 
     from paper_2307_02043_b200 import physics as PH
-    from paper_2307_02043_b200.configs import ls_phantom
+    from paper_2307_02043_b200.configs import cell_phantom, ls_phantom
 
-    n = args.ls_n
-    xgt = ls_phantom(n, 12, 0.01, 0.1, seed=4000)
-    views, vs = PH.make_scatter_views(n, 64, model="ls", x_gt=xgt, noise_snr_db=25.0, seed=4001, theta_deg=40.0,
-                                      batch=16, max_iter=500, device=dev)
+    c = LS_CONFIGS[config]
+    n, L = c["n"], c["L"]
+    kind, shapes, lo, hi, pseed = c["phantom"]
+    xgt = ls_phantom(n, shapes, lo, hi, seed=pseed) if kind == "ellipsoids" else cell_phantom(n, pseed, lo, hi)
+    views, vs = PH.make_scatter_views(n, L, model="ls", x_gt=xgt, noise_snr_db=25.0, seed=c["seed"],
+                                      theta_deg=c["theta"], batch=c["batch"], max_iter=500, device=dev)
     x = torch.tensor(0.5 * xgt, dtype=torch.float32, device=dev)
-    idx = list(range(0, 64, 4))
+    ks = L // c["subset"]
+    idx = list(range(0, L, ks))[: c["subset"]]
     if ws > 1:
-        # view-sharded (SURVEY 8e): each rank takes a contiguous chunk of the subset,
-        # one NCCL all-reduce of the gradient; the time is the max over ranks
         import torch.distributed as dist
 
         from paper_2307_02043_b200 import dist as DI
@@ -522,6 +635,8 @@ def ls_measure(args, dev, ws=1):
         vs.iters_forward.clear()
         vs.iters_adjoint.clear()
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        if ws > 1:
+            dist.barrier()
         torch.cuda.synchronize(dev)
         s.record()
         grad()
@@ -548,14 +663,67 @@ def ls_measure(args, dev, ws=1):
     peak, _ = hbm_peak()
     peak *= ws  # whole-job bytes over ws GPUs
     achieved = vv * bpv / (ms * 1e-3) / 1e9
-    return {"metric": "LS forward+adjoint views*voxels/s", "value": vv / (ms * 1e-3), "unit": "view*voxel/s",
-            "ms_per_subset_gradient": ms, "views": len(idx), "n": n, "padded": 2 * n, "dtype": "c64",
-            "n_gpus": ws, "scaling": "strong", "parallelism": f"view-sharded x{ws}, one all-reduce",
-            "K_f": Kf, "K_a": Ka,
+    return {"config": config, "metric": "LS forward+adjoint views*voxels/s", "value": vv / (ms * 1e-3),
+            "unit": "view*voxel/s", "ms_per_subset_gradient": ms, "views": len(idx), "n": n, "padded": 2 * n,
+            "dtype": "c64", "n_gpus": ws, "scaling": "strong",
+            "parallelism": f"view-sharded x{ws}, one all-reduce of the gradient", "K_f": Kf, "K_a": Ka,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "algorithmic_bytes_per_view_voxel": bpv, "bytes_per_matvec_per_voxel": b_mv,
                          "green_path": "pruned line passes" if pruned else "padded cuFFT"},
-            "data": "synthetic (seeded ellipsoid phantom, 25 dB noise), x = x_gt/2"}
+            "data": f"synthetic (seeded {kind} phantom, 25 dB noise), x = x_gt/2"}
+
+
+def prox_sharded_measure(dev, ws, n=256, reps=3):
+    """The z-slab-sharded prox (slab_prox.py; north star (4), config 5): the
+    config-2 law at n^3 fp32 (W = diag(d) + u u^T, iso TV 0.05, box [0, inf),
+    100 FGP iterations) split along z over the ws ranks, one slab each, with the
+    1-plane halo exchanges and the scalar all-reduces on the NCCL communicator.
+    Strong scaling; the time is the max over ranks of CUDA events around the solve."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2307_02043_b200 as bq
+    from paper_2307_02043_b200 import slab_prox as SP
+    from paper_2307_02043_b200.configs import config2_inputs
+    from paper_2307_02043_b200.wpm import BoxSet, DiagPlusLowRank
+
+    inp = config2_inputs(n)
+    w = DiagPlusLowRank(1.0, torch.tensor(inp["u"][:, None], dtype=torch.float32, device=dev),
+                        d=torch.tensor(inp["d"], dtype=torch.float32, device=dev))
+    v = torch.tensor(inp["v"], dtype=torch.float32, device=dev)
+    sp = SP.ShardedProx(bq.Grid((n, n, n)), v, w, inp["reg"], BoxSet(0.0, np.inf))
+    rep = sp.run(eps=1e-300, max_iter=100)  # warm-up
+    ts = []
+    for _ in range(reps):
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        s.record()
+        rep = sp.run(eps=1e-300, max_iter=100)
+        e.record()
+        torch.cuda.synchronize(dev)
+        t = s.elapsed_time(e)
+        if ws > 1:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        ts.append(t)
+    ms = float(np.median(ts))
+    N = n ** 3
+    peak, _ = hbm_peak()
+    bpv = bytes_per_voxel_iter(4, 1, True)
+    achieved = bpv * N * 100 / (ms * 1e-3) / 1e9
+    z0, z1 = sp.bounds[0]
+    return {"workload": f"config-2 law at {n}^3 fp32, W = diag(d) + uu^T, 100 FGP iterations, z-slab sharded",
+            "n_gpus": ws, "scaling": "strong", "parallelism": f"z-slab x{ws} (planes {z0}..{z1} on rank 0)",
+            "ms_per_solve": ms, "value": N * 100 / (ms * 1e-3), "unit": UNIT,
+            "newton_steps": int(rep.newton_iterations),
+            "communication_per_fgp_iteration": {"halo_planes": 2, "halo_bytes_each": n * n * 4,
+                                                "allreduces": f"3 + Newton steps (~{rep.newton_iterations / 100 + 1:.2f})",
+                                                "allreduce_doubles_max": 3},
+            "roofline": {"achieved": achieved, "peak": peak * ws, "unit": "GB/s", "frac": achieved / (peak * ws),
+                         "algorithmic_bytes_per_voxel_iter": bpv}}
 
 
 def main():
@@ -565,12 +733,13 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--n", type=int, default=128)
-    ap.add_argument("--cpu-iters", type=int, default=8)
+    ap.add_argument("--cpu-solves", type=int, default=0, help="CPU-baseline solves (default: one per core)")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-ls", action="store_true")
     ap.add_argument("--no-more", action="store_true", help="skip the secondary prox shapes (256^3, rank 4)")
     ap.add_argument("--no-loop", action="store_true", help="skip the end-to-end BQNPM loop runs (bench/loop_bench.py)")
-    ap.add_argument("--ls-n", type=int, default=128)
+    ap.add_argument("--no-ls5", action="store_true", help="skip the config-5 LS subset gradient (n = 256)")
+    ap.add_argument("--no-sharded", action="store_true", help="skip the z-slab-sharded 256^3 prox")
     ap.add_argument("--ls-steps", type=int, default=2)
     args = ap.parse_args()
     if args.impl == "reference":

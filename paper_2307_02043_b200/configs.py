@@ -60,6 +60,36 @@ def ls_phantom(n: int, n_shapes: int, dn_lo: float, dn_hi: float, seed: int) -> 
     return vol.reshape(-1)
 
 
+def cell_phantom(n: int, seed: int, dn_lo: float = 0.005, dn_hi: float = 0.06) -> np.ndarray:
+    """Config 5: a cell-like nest of ellipsoids -- membrane shell,
+    cytoplasm, nucleus, two nucleoli -- with sorted dn ~ U[lo, hi] (inner levels
+    denser), random orientations; later (inner) shapes overwrite outer ones."""
+    rng = np.random.default_rng(seed)
+    c = (np.arange(n) + 0.5) / n
+    z, y, x = np.meshgrid(c, c, c, indexing="ij")
+    pts = np.stack([x, y, z], axis=-1)
+    vol = np.zeros((n, n, n))
+    levels = np.sort(rng.uniform(dn_lo, dn_hi, 4))
+    ctr = 0.5 + rng.uniform(-0.03, 0.03, 3)
+    q, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    ax = rng.uniform(0.33, 0.40, 3)
+
+    def fill(centre, axes, rot, val):
+        inside = np.sum((((pts - centre) @ rot) / axes) ** 2, axis=-1) <= 1.0
+        vol[inside] = val
+
+    fill(ctr, ax, q, levels[1])                 # membrane shell (outer ellipsoid) ...
+    fill(ctr, ax - 0.02, q, levels[0])          # ... hollowed by the cytoplasm
+    nq, _ = np.linalg.qr(rng.standard_normal((3, 3)))
+    nctr = ctr + rng.uniform(-0.06, 0.06, 3)
+    nax = ax * rng.uniform(0.35, 0.45, 3)
+    fill(nctr, nax, nq, levels[2])              # nucleus
+    for _ in range(2):                          # nucleoli
+        off = rng.uniform(-0.5, 0.5, 3) * nax
+        fill(nctr + off @ nq.T, nax * rng.uniform(0.2, 0.3, 3), nq, levels[3])
+    return vol.reshape(-1)
+
+
 def born_spheres_phantom(n: int, seed: int, n_spheres: int = 3, dn_lo: float = 0.01, dn_hi: float = 0.05):
     """Config 1: 3 random spheres (centres 0.3 + 0.4 U^3, radii linspace(0.32, 0.10, 3)
     (0.8 + 0.4 U) as box fractions -- the reference law, forward_models.py:262-263 --

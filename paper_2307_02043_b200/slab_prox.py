@@ -82,9 +82,18 @@ class Comm:
         else:
             self.rank, self.world = 0, 1
 
+    def _host_staged(self, t):
+        # gloo (the CPU tests, and bench.py's one-GPU functional mode) moves host tensors
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
     def allreduce(self, t: torch.Tensor) -> torch.Tensor:
         if self.world > 1:
-            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+            if self._host_staged(t):
+                h = t.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+                t.copy_(h)
+            else:
+                dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
         return t
 
     def _peer(self, r):
@@ -98,13 +107,18 @@ class Comm:
         ops = []
         dst = self.rank + 1 if up else self.rank - 1
         src = self.rank - 1 if up else self.rank + 1
+        staged = self._host_staged(recv)
+        snd = send.cpu() if staged else send.contiguous()
+        rcv = torch.empty(recv.shape, dtype=recv.dtype) if staged else recv
         if 0 <= dst < self.world:
-            ops.append(dist.P2POp(dist.isend, send.contiguous(), self._peer(dst), self.group))
+            ops.append(dist.P2POp(dist.isend, snd, self._peer(dst), self.group))
         if 0 <= src < self.world:
-            ops.append(dist.P2POp(dist.irecv, recv, self._peer(src), self.group))
+            ops.append(dist.P2POp(dist.irecv, rcv, self._peer(src), self.group))
         if ops:
             for req in dist.batch_isend_irecv(ops):
                 req.wait()
+        if staged and 0 <= src < self.world:
+            recv.copy_(rcv)
 
 
 class SlabGroup:
@@ -362,45 +376,61 @@ C_DOUBLE8 = _C.c_double * 8
 def solve_sharded(grid, v, w, reg, box, *, group=None, slabs_per_rank=1, mode=TvMode.ISOTROPIC, omega=None,
                   eps=1e-5, max_iter=100, accelerated=True, newton_eps=1e-6, newton_max_iter=50, beta0=None,
                   dtype=None, device=None):
+    sp = ShardedProx(grid, v, w, reg, box, group=group, slabs_per_rank=slabs_per_rank, mode=mode, omega=omega,
+                     dtype=dtype, device=device)
+    return sp.run(eps=eps, max_iter=max_iter, accelerated=accelerated, newton_eps=newton_eps,
+                  newton_max_iter=newton_max_iter, beta0=beta0), sp.bounds
+
+
+class ShardedProx:
     """Sharded counterpart of ``dual_tv_solver.solve`` for a 3-D grid.
 
     Every rank of `group` passes the same GLOBAL problem description (grid, and
     v / w / box as full arrays it can slice, or device tensors) and gets back
     its own slabs of x and P*.  `slabs_per_rank` > 1 splits each rank's share
     further (the single-GPU loopback layout).  Box bounds must be scalars.
-    Returns (SlabReport, [(z0, z1) per local slab])."""
-    from .wpm import DiagPlusLowRank  # noqa: F401  (type of w)
+    Returns (SlabReport, [(z0, z1) per local slab]).  ``ShardedProx`` is the
+    reusable form (slabs and device buffers set up once, ``run`` per solve)."""
 
-    if grid.ndim != 3:
-        raise ValueError("the z-slab prox shards 3-D grids")
-    if isinstance(box.lower, np.ndarray) or isinstance(box.upper, np.ndarray):
-        raise ValueError("the z-slab prox takes scalar box bounds")
-    comm = Comm(group)
-    k1, k2, k3 = grid.dims
-    allb = slab_bounds(k3, comm.world * slabs_per_rank)
-    mine = allb[comm.rank * slabs_per_rank:(comm.rank + 1) * slabs_per_rank]
-    if any(z1 <= z0 for z0, z1 in mine):
-        raise ValueError(f"{k3} planes cannot give every slab at least one plane")
-    dtype = dtype or w.dtype
-    device = device or w.device
-    plane = k1 * k2
-    vt = to_dev(v, dtype, device)
-    v_parts = [vt[z0 * plane:z1 * plane] for z0, z1 in mine]
-    U_parts = [w.Ut[:, z0 * plane:z1 * plane] if w.rank else None for z0, z1 in mine]
-    d_parts = [w.d[z0 * plane:z1 * plane] for z0, z1 in mine] if w.d is not None else None
-    gram = None
-    if w.rank:
-        gram = w.gram.reshape(w.rank, w.rank).cpu().numpy()  # U^T D^-1 U (global, from the metric)
-    be = DeviceSlabs(grid.dims, mine, k3, dtype, device, v_parts, U_parts, d_parts, rank=w.rank, sign=w.sign,
-                     tau=w.tau if w.d is None else 1.0, reg=reg, lo=box.lower, hi=box.upper, mode=mode)
-    if omega is None:
-        omega = w.default_omega()
-    step = 1.0 / (4.0 * 3 * omega * reg) if reg > 0 else 0.0
-    sg = SlabGroup(be, comm, grid.dims, mine, k3)
-    rep = slab_solve(sg, rank=w.rank, sign=w.sign, tau=w.tau if w.d is None else 1.0, scalar=w.d is None,
-                     gram=gram, reg=reg, step=step, eps=eps, max_iter=max_iter, accelerated=accelerated,
-                     newton_eps=newton_eps, newton_max_iter=newton_max_iter, beta0=beta0)
-    return rep, mine
+    def __init__(self, grid, v, w, reg, box, *, group=None, slabs_per_rank=1, mode=TvMode.ISOTROPIC, omega=None,
+                 dtype=None, device=None):
+        self._setup(grid, v, w, reg, box, group, slabs_per_rank, mode, omega, dtype, device)
+
+    def _setup(self, grid, v, w, reg, box, group, slabs_per_rank, mode, omega, dtype, device):
+        if grid.ndim != 3:
+            raise ValueError("the z-slab prox shards 3-D grids")
+        if isinstance(box.lower, np.ndarray) or isinstance(box.upper, np.ndarray):
+            raise ValueError("the z-slab prox takes scalar box bounds")
+        comm = Comm(group)
+        k1, k2, k3 = grid.dims
+        allb = slab_bounds(k3, comm.world * slabs_per_rank)
+        mine = allb[comm.rank * slabs_per_rank:(comm.rank + 1) * slabs_per_rank]
+        if any(z1 <= z0 for z0, z1 in mine):
+            raise ValueError(f"{k3} planes cannot give every slab at least one plane")
+        dtype = dtype or w.dtype
+        device = device or w.device
+        plane = k1 * k2
+        vt = to_dev(v, dtype, device)
+        v_parts = [vt[z0 * plane:z1 * plane] for z0, z1 in mine]
+        U_parts = [w.Ut[:, z0 * plane:z1 * plane] if w.rank else None for z0, z1 in mine]
+        d_parts = [w.d[z0 * plane:z1 * plane] for z0, z1 in mine] if w.d is not None else None
+        gram = None
+        if w.rank:
+            gram = w.gram.reshape(w.rank, w.rank).cpu().numpy()  # U^T D^-1 U (global, from the metric)
+        be = DeviceSlabs(grid.dims, mine, k3, dtype, device, v_parts, U_parts, d_parts, rank=w.rank, sign=w.sign,
+                         tau=w.tau if w.d is None else 1.0, reg=reg, lo=box.lower, hi=box.upper, mode=mode)
+        if omega is None:
+            omega = w.default_omega()
+        self.step = 1.0 / (4.0 * 3 * omega * reg) if reg > 0 else 0.0
+        self.sg = SlabGroup(be, comm, grid.dims, mine, k3)
+        self.bounds = mine
+        self.kw = dict(rank=w.rank, sign=w.sign, tau=w.tau if w.d is None else 1.0, scalar=w.d is None, gram=gram,
+                       reg=reg)
+
+    def run(self, eps=1e-5, max_iter=100, accelerated=True, newton_eps=1e-6, newton_max_iter=50, beta0=None):
+        return slab_solve(self.sg, step=self.step, eps=eps, max_iter=max_iter, accelerated=accelerated,
+                          newton_eps=newton_eps, newton_max_iter=newton_max_iter, beta0=beta0, **self.kw)
 
 
-__all__ = ["slab_bounds", "Comm", "SlabGroup", "slab_solve", "DeviceSlabs", "solve_sharded", "SlabReport"]
+__all__ = ["slab_bounds", "Comm", "SlabGroup", "slab_solve", "DeviceSlabs", "solve_sharded", "ShardedProx",
+           "SlabReport"]
