@@ -36,7 +36,7 @@ def main(which=None):
     if which:
         for w in which:
             {"config1": make_config1_golden, "config3s": make_config3_small_golden,
-             "baselines": make_baselines_golden}[w](tv_ops, wpm, solvers, fm)
+             "baselines": make_baselines_golden, "formats": make_formats_golden}[w](tv_ops, wpm, solvers, fm)
         return
     Grid, TvMode = tv_ops.Grid, tv_ops.TvMode
     out = {}
@@ -247,6 +247,22 @@ def main(which=None):
     make_config1_golden(tv_ops, wpm, solvers, fm)
     make_config3_small_golden(tv_ops, wpm, solvers, fm)
     make_baselines_golden(tv_ops, wpm, solvers, fm)
+
+
+def make_formats_golden(tv_ops, wpm, solvers, fm):
+    """Files written by the REFERENCE harness itself (experiment_cli.py:35-137):
+    a TVQNVOL1 volume and a "tvqn-trace v1" CSV, for byte-level format parity."""
+    from tvqn import experiment_cli as E
+
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((5, 4, 3))
+    E.dump_volume(x, OUT / "ref_volume_5x4x3.tvqnvol")
+    tr = solvers.IterationTrace(solver="bqnpm")
+    for k in range(4):
+        tr.rows.append(solvers.TraceRow(iteration=k, cost=float(1 / (k + 1) + 1e-13 * k), snr_db=float(3.25 * k + 1 / 3),
+                                        elapsed_s=0.125 * k, inner_iters=7 * k, grad_evals=k, full_grad_evals=0))
+    E.write_trace(tr, OUT / "ref_trace_v1.csv")
+    np.savez(OUT / "ref_formats.npz", volume=x)
 
 
 def make_baselines_golden(tv_ops, wpm, solvers, fm):

@@ -167,3 +167,19 @@ def test_scatter_view_problem_surface():
         assert isinstance(views[0].jacobian_vec(x, dx), np.ndarray)
     views32, _ = PH.make_scatter_views(10, 3, model="ls", x_gt=x, dtype=torch.complex64, tol=1e-6, batch=3)
     views32[0].self_check(1000, np.random.default_rng(8))
+
+
+def test_volume_format_from_and_to_device(tmp_path):
+    """A device x (flat Fortran layout == C-order (K3, K2, K1) tensor) is written
+    with one D2H copy and reads back as the reference's n-d array."""
+    from pathlib import Path
+
+    from paper_2307_02043_b200 import formats as F
+
+    x = np.load(Path(__file__).parent / "golden" / "ref_formats.npz")["volume"]
+    xt = torch.tensor(x.reshape(-1, order="F"), device="cuda").reshape(3, 4, 5)
+    F.dump_volume(xt, tmp_path / "d.tvqnvol")
+    ref = (Path(__file__).parent / "golden" / "ref_volume_5x4x3.tvqnvol").read_bytes()
+    assert (tmp_path / "d.tvqnvol").read_bytes() == ref
+    back = F.load_volume(tmp_path / "d.tvqnvol", device="cuda")
+    assert back.is_cuda and torch.equal(back, xt.reshape(-1))
