@@ -106,6 +106,14 @@ typedef struct {
    * (third slot of the P ring, with p and pb), a2 = N (ping-pong of a). */
   void* p2;
   void* a2;
+  /* optional device scalars of a GPU-resident outer loop (NULL: use tau/step
+   * above): [0] tau (overrides `tau`; the dual step is then computed on the
+   * device as 1/(4 ndim (1/tau) reg), dual_tv_solver.py:155-158), [1] the
+   * effective rank of U (trailing columns are zero), [2] the effective rank of
+   * the previous solve -- the beta warm start is zeroed when [1] != [2]
+   * (dual_tv_solver.py:185-186) and [2] is set to [1] at the end.  Fused
+   * kernel only (K1 in {4..128 dividing 128, 256}, scalar bounds, d == NULL). */
+  double* dev_metric;
 } bq_wtv_desc;
 
 typedef struct {
@@ -135,6 +143,18 @@ int bq_wpm_box(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t sign
                const void* d, const void* U, const void* x, double lo, double hi,
                const void* lo_arr, const void* hi_arr, double* beta_inout, double newton_eps,
                int32_t newton_max_iter, void* x_out, void* a_scratch, void* report, void* stream);
+
+/* GPU-resident BQNPM step (k > K_s): the aggregated metric and v_k with every
+ * scalar on the device (solvers.py:67-89).  count (<= 8) slots in kappa order:
+ * host arrays of device pointers x_t, g_t, u_t (N; zeros for a rejected SR1
+ * term) and est_t (bq_sr1's device est: [0] tau_t, [1] has_u).  Writes Uc_out
+ * (count x N: the accepted u_t compacted in slot order, zero columns after),
+ * meta (device, >= 128 doubles: [0] tau_w = sum tau_t, [1] effective rank --
+ * the layout bq_wtv_desc::dev_metric reads; [2] is left to the prox) and
+ * v_out = W^-1 sum_t (tau_t x_t + u_t (u_t^T x_t) - step g_t), W = tau_w I + Uc Uc^T. */
+int bq_bqnpm_metric_vk(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const void* const* xs,
+                       const void* const* gs, const void* const* us, const double* const* ests, double step,
+                       void* Uc_out, double* meta, void* acc_scratch, void* v_out, void* stream);
 
 /* ---------------------------------------------------------------------------
  * z-slab-sharded prox: one rank's passes (dual_tv_solver.py:221-239 over a

@@ -62,6 +62,7 @@ EXPORTS = (
     "bq_tv_divergence",
     "bq_tv_project_dual",
     "bq_wpm_phi",
+    "bq_bqnpm_metric_vk",
 )
 
 
@@ -96,6 +97,7 @@ class WtvDesc(C.Structure):
         ("report", C.c_void_p),
         ("p2", C.c_void_p),
         ("a2", C.c_void_p),
+        ("dev_metric", C.c_void_p),
     ]
 
 
@@ -183,6 +185,8 @@ _SIGS = {
     "bq_tv_grad_stack": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _P, _P, _P]),
     "bq_tv_divergence": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _P, _P, _P]),
     "bq_tv_project_dual": (C.c_int, [_P, _I32, _I32, _I64, _I32, _P, _P, _P]),
+    "bq_bqnpm_metric_vk": (C.c_int, [_P, _I32, _I64, _I32, C.POINTER(_P), C.POINTER(_P), C.POINTER(_P),
+                                     C.POINTER(_P), _D, _P, _P, _P, _P, _P]),
     "bq_wpm_phi": (C.c_int, [_P, _I32, _I64, _I32, _I32, _D, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P, _P]),
 }
 

@@ -79,10 +79,20 @@ __global__ void __launch_bounds__(NT) div_kernel(SlabArgs A, const T* __restrict
   const T* Fy = F + A.N;
   const T* Fz = F + 2 * A.N;
   const T* U = (const T*)A.U;
-  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < A.N; j += (long long)gridDim.x * NT) {
-    const int ix = (int)(j % A.K1);
-    const int iy = (int)((j / A.K1) % A.K2);
-    const int iz = (int)(j / A.plane);
+  // groups of RB whole x-rows per block step (RB = NT / K1 for short rows): the
+  // coordinates come from 32-bit row arithmetic, no per-voxel 64-bit division
+  const int rows = A.K2 * A.L;
+  const int RB = A.K1 >= NT ? 1 : NT / A.K1;
+  const int span = RB * A.K1;
+  for (int row0 = blockIdx.x * RB; row0 < rows; row0 += gridDim.x * RB)
+  for (int e = threadIdx.x; e < span; e += NT) {
+    const int sub = e / A.K1;
+    const int ix = e - sub * A.K1;
+    const int row = row0 + sub;
+    if (row >= rows) break;
+    const int iy = row % A.K2;
+    const int iz = row / A.K2;
+    const long long j = (long long)row * A.K1 + ix;
     // sum_a (D^a)^T F_a, term order of tv_ops.py:129-131 per axis, axes accumulated from 0
     T dv = (T)0;
     {
@@ -183,10 +193,20 @@ __global__ void __launch_bounds__(NT) dual_kernel(SlabArgs A, const T* __restric
   __shared__ double scr[(NT / 32) * kMaxVals];
   double acc[2] = {0.0, 0.0};
   const long long N = A.N;
-  for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < N; j += (long long)gridDim.x * NT) {
-    const int ix = (int)(j % A.K1);
-    const int iy = (int)((j / A.K1) % A.K2);
-    const int iz = (int)(j / A.plane);
+  // groups of RB whole x-rows per block step (RB = NT / K1 for short rows): the
+  // coordinates come from 32-bit row arithmetic, no per-voxel 64-bit division
+  const int rows = A.K2 * A.L;
+  const int RB = A.K1 >= NT ? 1 : NT / A.K1;
+  const int span = RB * A.K1;
+  for (int row0 = blockIdx.x * RB; row0 < rows; row0 += gridDim.x * RB)
+  for (int e = threadIdx.x; e < span; e += NT) {
+    const int sub = e / A.K1;
+    const int ix = e - sub * A.K1;
+    const int row = row0 + sub;
+    if (row >= rows) break;
+    const int iy = row % A.K2;
+    const int iz = row / A.K2;
+    const long long j = (long long)row * A.K1 + ix;
     const T qj = q[j];
     T g[3];
     g[0] = ix < A.K1 - 1 ? q[j + 1] - qj : (T)0;
@@ -272,7 +292,13 @@ int make_args(const bq_slab_desc* D, const double* c, const double* beta, SlabAr
 
 int blocks(bq_ctx* ctx, long long n) {
   long long want = (n + 4LL * NT - 1) / (4LL * NT);
-  return (int)std::max<long long>(1, std::min<long long>(want, std::min(1184, ctx->num_sms * 4)));
+  return (int)std::max<long long>(1, std::min<long long>(want, std::min(1184, ctx->num_sms * 8)));
+}
+// row-mapped passes (div, dual): one block per x-row step
+int row_blocks(bq_ctx* ctx, const SlabArgs& A) {
+  const long long rb = A.K1 >= NT ? 1 : NT / A.K1;
+  const long long groups = ((long long)A.K2 * A.L + rb - 1) / rb;
+  return (int)std::max<long long>(1, std::min<long long>(groups, std::min(1184, ctx->num_sms * 8)));
 }
 
 }  // namespace
@@ -290,7 +316,7 @@ extern "C" int bq_slab_div(bq_ctx* ctx, const bq_slab_desc* desc, const void* fi
   cudaStream_t st = (cudaStream_t)stream;
   BQ_STREAM_WS(sw, ctx, st);
   RedWs ws = red_ws(sw);
-  const int G = blocks(ctx, A.N);
+  const int G = row_blocks(ctx, A);
   if (desc->dtype == BQ_F32) {
     SLAB_RANK_SWITCH(A.rank, (div_kernel<float, R><<<G, NT, 0, st>>>(A, (const float*)field, (const float*)halo_below,
                                                                       (float*)t_out, s_out, ws)));
@@ -350,7 +376,7 @@ extern "C" int bq_slab_dual(bq_ctx* ctx, const bq_slab_desc* desc, const void* p
   cudaStream_t st = (cudaStream_t)stream;
   BQ_STREAM_WS(sw, ctx, st);
   RedWs ws = red_ws(sw);
-  const int G = blocks(ctx, A.N);
+  const int G = row_blocks(ctx, A);
   if (desc->dtype == BQ_F32)
     dual_kernel<float><<<G, NT, 0, st>>>(A, (const float*)pbar, (const float*)p, (const float*)q,
                                          (const float*)halo_above, step, momentum, (float*)p_next, (float*)pbar_next,

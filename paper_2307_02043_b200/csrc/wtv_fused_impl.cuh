@@ -93,6 +93,7 @@ struct FCtl {
   double chol_rdiag[BQ_MAX_RANK];  // 1 / L_ii (the per-iteration solves multiply)
   double K0[BQ_MAX_RANK], Cin[36], Cout[36];
   double gram[36];  // setup U^T D^-1 U (raw partials): sum over all voxels of u s^T = sign * gsc(gram)
+  double tau;       // the launch's tau (host or dev_metric[0])
   unsigned long long t_last;
   unsigned long long phase_ns[8], phase_work_ns[8];
   int phase_cnt[8];
@@ -153,7 +154,21 @@ struct FArgs {
   double grow_min;            // minimum box growth factor of the near-list Newton
   double ndist_min;           // near lists longer than this take distributed (per-block + barrier) steps
   int pre_max;                // stages of the next FUSED pass prefetched across the barrier (<= nstage)
+  double* dev_metric;         // optional device [tau, rank_eff, rank_prev] (bq_wtv_desc::dev_metric)
 };
+
+// tau and the dual step of this launch: host values, or from the device
+// scalars of a GPU-resident outer loop (step as dual_tv_solver.py:155-158 with
+// omega = 1/tau, same operation order)
+template <typename T>
+__device__ __forceinline__ double eff_tau(const FArgs<T>& A) {
+  return A.dev_metric ? __ldcg(A.dev_metric) : A.tau;
+}
+template <typename T>
+__device__ __forceinline__ double eff_step(const FArgs<T>& A) {
+  if (!A.dev_metric) return A.step;
+  return A.reg > 0.0 ? 1.0 / (((4.0 * A.ndim) * (1.0 / __ldcg(A.dev_metric))) * A.reg) : 0.0;
+}
 
 // shared, per-block copy of what the passes read
 template <typename T>
@@ -386,7 +401,7 @@ struct Ctl {
 
   __device__ bool diag() const { return A.d != nullptr; }
   // gram-like reduced entry -> metric units (scalar metric divides by tau)
-  __device__ double gsc(double g) const { return diag() ? g : g / A.tau; }
+  __device__ double gsc(double g) const { return diag() ? g : g / c.tau; }
 
   __device__ void timeline(int phase, const double* red, bool passed_barrier) {
     const unsigned long long now = global_ns();
@@ -528,6 +543,7 @@ struct Ctl {
   __device__ void run(int phase, const double* red) {
     switch (phase) {
       case F_SETUP: {
+        c.tau = eff_tau(A);
         double cap[R > 0 ? R * R : 1];
         int k = 0;
         for (int i = 0; i < R; ++i)
@@ -546,8 +562,10 @@ struct Ctl {
         }
         for (int i = 0; i < R * R; ++i) c.chol[i] = cap[i];
         for (int i = 0; i < R; ++i) c.chol_rdiag[i] = 1.0 / cap[i * R + i];
+        // GPU-resident loop: the warm start is dropped when the effective rank changed
+        const bool keep = !A.dev_metric || __ldcg(A.dev_metric + 1) == __ldcg(A.dev_metric + 2);
         for (int i = 0; i < R; ++i) {
-          c.beta[i] = A.beta_io ? A.beta_io[i] : 0.0;
+          c.beta[i] = (A.beta_io && keep) ? A.beta_io[i] : 0.0;
           c.gw[i] = 0.0;
           c.gc[i] = -c.beta[i];  // gw == 0 when the warm start is zero
           c.gwid[i] = 0.0;       // forces one full Newton evaluation first
@@ -634,6 +652,7 @@ struct Ctl {
           rp->last_newton_converged = c.last_newton_conv;
           if (A.beta_io)
             for (int i = 0; i < R; ++i) A.beta_io[i] = c.beta[i];
+          if (A.dev_metric) A.dev_metric[2] = A.dev_metric[1];
           for (int i = 0; i < 6; ++i) {
             // [setup, div, newton (full pass), fused, final, newton (on-chip + distributed near list)]
             const int src = (i == 5) ? F_NLOCAL : i;
@@ -814,9 +833,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   T* __restrict__ Aout = A.abuf[sh.a_cur ^ 1];
   const T m_prev = sh.m_prev, m_cur = sh.m_cur;
   const bool div_p = sh.div_p;
-  const T step = (T)A.step, reg = (T)A.reg, sg = (T)A.sign;
+  const T step = (T)eff_step(A), reg = (T)A.reg, sg = (T)A.sign;
   const bool diag = A.d != nullptr;
-  const T itauT = diag ? (T)1 : rcp((T)A.tau);
+  const T itauT = diag ? (T)1 : rcp((T)eff_tau(A));
   const bool iso = A.mode == BQ_TV_ISO;
   StageMap<R> M;
   // p_{i-2} is always staged (unused while m_prev == 0) so that the layout does
@@ -1242,7 +1261,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   const long long tp_s = (long long)((A.K2 + (GWs - 1) * A.rpw - 1) / ((GWs - 1) * A.rpw)) * A.K3;
   const long long seg_begin_s = (long long)blockIdx.x * tp_s / gridDim.x;
   const long long seg_end_s = (long long)(blockIdx.x + 1) * tp_s / gridDim.x;
-  const Fields<T, R> F{A.d, A.U, A.lo_arr, A.hi_arr, N, (T)A.tau, (T)A.lo, (T)A.hi, (T)A.sign};
+  const Fields<T, R> F{A.d, A.U, A.lo_arr, A.hi_arr, N, (T)eff_tau(A), (T)A.lo, (T)A.hi, (T)A.sign};
   const int lpr = A.lpr, rpw = A.rpw;
   // standalone DIV pass: NG row groups of wpr warps, the last group is the halo
   const int NG = (RW + 1) / wpr;
@@ -1333,7 +1352,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       T* __restrict__ Aout = A.abuf[sh.a_cur ^ 1];
       const T m_prev = sh.m_prev, m_cur = sh.m_cur;
       const bool div_p = sh.div_p;
-      const T step = (T)A.step, reg = (T)A.reg;
+      const T step = (T)eff_step(A), reg = (T)A.reg;
       const bool iso = A.mode == BQ_TV_ISO;
       const bool single = sh.single;
       int ncnt = 0;
@@ -1949,6 +1968,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.N = D.dims[0] * D.dims[1] * D.dims[2];
   A.plane = D.dims[0] * D.dims[1];
   A.tau = D.tau;
+  A.dev_metric = D.dev_metric;
   A.reg = D.reg;
   A.step = D.step;
   A.eps = D.eps;

@@ -1064,7 +1064,8 @@ int validate(const bq_wtv_desc& D, bool wpm_only) {
   BQ_CHECK(D.dims[0] < (1 << 30) && D.dims[1] < (1 << 30) && D.dims[2] < (1 << 30), BQ_EINVAL, "side too large");
   BQ_CHECK(D.dtype == BQ_F32 || D.dtype == BQ_F64, BQ_EINVAL, "dtype must be BQ_F32 or BQ_F64");
   BQ_CHECK(D.sign == 1 || D.sign == -1, BQ_EINVAL, "sign must be +1 or -1, got %d", D.sign);
-  BQ_CHECK(D.d != nullptr || D.tau > 0, BQ_EINVAL, "tau must be positive, got %g", D.tau);
+  BQ_CHECK(D.d != nullptr || D.tau > 0 || D.dev_metric, BQ_EINVAL, "tau must be positive, got %g", D.tau);
+  BQ_CHECK(!D.dev_metric || (D.d == nullptr && !wpm_only), BQ_EINVAL, "dev_metric needs a scalar-tau prox");
   BQ_CHECK(D.reg >= 0, BQ_EINVAL, "reg must be nonnegative");
   BQ_CHECK(D.rank == 0 || D.U != nullptr, BQ_EINVAL, "U is required for rank > 0");
   BQ_CHECK(D.v && D.x && D.a && D.report, BQ_EINVAL, "v, x, a and report are required");
@@ -1074,7 +1075,7 @@ int validate(const bq_wtv_desc& D, bool wpm_only) {
     BQ_CHECK(D.max_iter >= 1, BQ_EINVAL, "max_iter must be >= 1");
     BQ_CHECK(D.p && D.pb, BQ_EINVAL, "p and pb are required");
     BQ_CHECK(D.mode == BQ_TV_ISO || D.mode == BQ_TV_ANISO, BQ_EINVAL, "bad TV mode");
-    BQ_CHECK(D.reg == 0 || D.step > 0, BQ_EINVAL, "step must be positive");
+    BQ_CHECK(D.reg == 0 || D.step > 0 || D.dev_metric, BQ_EINVAL, "step must be positive");
   }
   return BQ_OK;
 }
@@ -1092,6 +1093,8 @@ extern "C" int bq_wtv_prox(bq_ctx* ctx, const bq_wtv_desc* desc, void* stream) {
   BQ_CUDA(cudaSetDevice(ctx->device));
   cudaStream_t st = (cudaStream_t)stream;
   if (fused_eligible(*desc) && !getenv("BQ_PROX_GENERAL")) return fused_dispatch(ctx, *desc, 0, st);
+  BQ_CHECK(!desc->dev_metric, BQ_EINVAL, "bq_wtv_prox: dev_metric needs the fused kernel (K1 in {4..128 dividing "
+           "128, 256}, 16-byte aligned fields, scalar bounds)");
   return desc->dtype == BQ_F32 ? dispatch_rank<float>(ctx, *desc, 0, st)
                                : dispatch_rank<double>(ctx, *desc, 0, st);
 }

@@ -101,9 +101,18 @@ class DctViewSet:
                                           float(s), out.data_ptr(), self._stream()), "pointwise")
         return out
 
+    def _vid(self, views):
+        """Device view-id list, cached per subset (no host-to-device copy per call,
+        so a subset gradient can be captured in a CUDA graph)."""
+        key = tuple(views)
+        cache = self.__dict__.setdefault("_vid_cache", {})
+        if key not in cache:
+            cache[key] = torch.tensor(views, dtype=torch.int32, device=self.device)
+        return cache[key]
+
     def _combine(self, F, views, scale, want_r=True, want_cost=False):
         views = list(views)
-        vid = torch.tensor(views, dtype=torch.int32, device=self.device)
+        vid = self._vid(views)
         ys = _abi.ptr_array([self.y[v] for v in views])
         r = torch.empty_like(F) if want_r else None
         cost = torch.empty(len(views), dtype=torch.float64, device=self.device) if want_cost else None

@@ -93,9 +93,21 @@ class ScatterViewSet:
                     "potential")
         return f, fp
 
+    def _index(self, views):
+        """Device index of a view batch, cached (no host-to-device copy per call,
+        so a Born subset gradient can be captured in a CUDA graph)."""
+        key = tuple(int(v) for v in views)
+        cache = self.__dict__.setdefault("_idx_cache", {})
+        if key not in cache:
+            cache[key] = torch.tensor(key, dtype=torch.long, device=self.device)
+        return cache[key]
+
+    def _rows(self, t, views):
+        return t.index_select(0, self._index(views))
+
     def incident(self, views):
         B = len(views)
-        kv = self.kvec[list(views)].contiguous()
+        kv = self._rows(self.kvec, views).contiguous()
         out = torch.empty(B, self.N, dtype=self.cdtype, device=self.device)
         self._check(self.lib.bq_ls_incident(self.ctx, self.code, self.n, self.h, B, kv.data_ptr(), out.data_ptr(),
                                             self._st()), "incident")
@@ -188,7 +200,7 @@ class ScatterViewSet:
             u, it = self.total_field(f, vb)
             self.iters_forward.extend(int(k) for k in it)
             H = self.conv(2, f, u)
-            r = H - self.unpack(self.y[vb])
+            r = H - self.unpack(self._rows(self.y, vb))
             self.vjp_from_residual(x, vb, r, f, fp, u, grad, 1.0 / len(views), accumulate=not first)
             first = False
         return grad
@@ -237,7 +249,7 @@ class ScatterViewSet:
         for i in range(0, len(views), self.batch):
             vb = views[i:i + self.batch]
             u = self.incident(vb)  # f = 0: the total field is the incident one
-            self.vjp_from_residual(x0, vb, self.unpack(self.y[vb]), f, fp, u, out, 1.0 / len(views),
+            self.vjp_from_residual(x0, vb, self.unpack(self._rows(self.y, vb)), f, fp, u, out, 1.0 / len(views),
                                    accumulate=not first)
             first = False
         return out
@@ -247,7 +259,7 @@ class ScatterViewSet:
         out = []
         for i in range(0, len(views), self.batch):
             vb = views[i:i + self.batch]
-            d = self.forward(x, vb) - self.y[vb]
+            d = self.forward(x, vb) - self._rows(self.y, vb)
             out.append(0.5 * (d.double() ** 2).sum(dim=1))
         return torch.cat(out)
 

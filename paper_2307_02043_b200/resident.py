@@ -1,0 +1,282 @@
+"""GPU-resident BQNPM outer loop with CUDA-graph replay.
+
+The reference loop (``/root/reference/pkg/src/tvqn/solvers.py:253-317``)
+takes three host decisions per iteration k > K_s: whether the SR1 step is
+usable (``np.any(s)``), whether the SR1 term is accepted (which sets the rank
+of the aggregated metric), and -- through ``DiagPlusLowRank`` /
+``DualTvProblem`` -- the metric's tau and the dual step.  Here all three stay
+on the device:
+
+* ``bq_sr1`` decides accept / fallback on the device (a zero step gives
+  (alpha, no u), exactly the loop's ``not np.any(s)`` branch);
+* ``bq_bqnpm_metric_vk`` aggregates the slots into tau_w and a fixed
+  K_s-column U with the accepted columns compacted in slot order and zero
+  columns after (a zero column changes neither W, the Woodbury solve nor the
+  Newton iteration), and computes v_k;
+* the fused prox kernel reads tau_w and the effective rank from device memory
+  (``bq_wtv_desc::dev_metric``): it forms the dual step from tau_w exactly as
+  ``dual_step_size`` does and drops the beta warm start when the effective
+  rank changed (dual_tv_solver.py:185-186).
+
+So one iteration is a fixed sequence of launches with fixed pointers; it
+depends on k only through k mod K_s (the subset and the kappa slot order).
+The first 2 K_s iterations run eagerly on a side stream (they also size
+every lazily allocated workspace), then one CUDA graph per residue class is
+captured on that stream and replayed.  The trace (cost, SNR, inner
+iterations, elapsed device time) is recorded on the device and read once at
+the end, so the host never waits on the GPU inside the loop -- unless an
+``on_iteration`` callback is given, which needs each row as it happens.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import _abi
+from . import dual_tv_solver as dts
+from .fixtures import snr_db
+from .metric_ops import kappa
+from .tv_ops import tv_value_async
+
+# report field offsets (bq_wtv_report): iterations int32 at 0, status int32 at 12
+_REPORT_ITER = 0
+_REPORT_STATUS = 3
+
+
+def eligible(vs, grid, config, group) -> str:
+    """'' when the resident loop applies, else the reason it does not."""
+    from .physics import ScatterViewSet
+
+    if group is not None and torch.distributed.is_initialized() and torch.distributed.get_world_size(group) > 1:
+        return "view-sharded runs keep the all-reduce on the host"
+    if isinstance(vs, ScatterViewSet) and vs.model == "ls":
+        return "LS views: the BiCGSTAB iteration count is data dependent (host early exit)"
+    if not 2 <= config.subsets <= 8:
+        return "K_s outside 2..8"
+    if grid.ndim != 3:
+        return "the fused prox kernel is 3-D"
+    k1 = grid.dims[0]
+    if not ((4 <= k1 <= 128 and k1 % 4 == 0 and 128 % k1 == 0) or k1 == 256):
+        return "row length outside the fused prox kernel's set"
+    if isinstance(config.box.lower, np.ndarray) or isinstance(config.box.upper, np.ndarray):
+        return "per-voxel box bounds"
+    return ""
+
+
+class ResidentBqnpm:
+    def __init__(self, vs, views, grid, config, parts, alphas, use_graphs=True):
+        self.vs, self.views, self.grid, self.cfg = vs, views, grid, config
+        self.parts, self.alphas = parts, [float(a) for a in alphas]
+        self.ks = config.subsets
+        self.a = 1.0 if config.step is None else config.step
+        self.lam = config.tv_weight
+        dev, dt, n = vs.device, vs.dtype, grid.size
+        self.dev, self.dt, self.n = dev, dt, n
+        ks = self.ks
+        self.X = torch.zeros(ks, n, dtype=dt, device=dev)
+        self.G = torch.zeros(ks, n, dtype=dt, device=dev)
+        self.Us = torch.zeros(ks, n, dtype=dt, device=dev)
+        self.EST = torch.zeros(ks, 16, dtype=torch.float64, device=dev)
+        self.meta = torch.zeros(128, dtype=torch.float64, device=dev)
+        self.Uc = torch.zeros(ks, n, dtype=dt, device=dev)
+        self.acc = torch.empty(n, dtype=dt, device=dev)
+        self.v = torch.empty(n, dtype=dt, device=dev)
+        self.s = torch.empty(n, dtype=dt, device=dev)
+        self.m = torch.empty(n, dtype=dt, device=dev)
+        self.ws = dts.ProxWorkspace(grid, dt, dev)
+        self.lib = _abi.load_library()
+        self.ctx = _abi.ctx_for(dev)
+        self.stream = torch.cuda.Stream(dev)
+        self.use_graphs = use_graphs
+        self.graphs = {}
+        self.graph_error = None
+        lo, hi, _, _ = config.box.device_args(dt, dev)
+        self.lo, self.hi = lo, hi
+
+    # -- one iteration -------------------------------------------------------
+    def _desc(self, v, rank, U, tau, reg, dev_metric):
+        g, cfg, ws = self.grid, self.cfg, self.ws
+        d = _abi.WtvDesc()
+        d.ndim = g.ndim
+        d.dtype = _abi.dtype_code(self.dt)
+        d.dims[:] = g.dims3
+        d.mode = cfg.mode.code
+        d.rank = rank
+        d.sign = 1
+        d.accelerated = 1
+        d.tau = tau
+        d.reg = float(reg)
+        d.step = (1.0 / (4.0 * g.ndim * (1.0 / tau) * reg)) if (reg > 0 and tau > 0) else (1.0 if reg > 0 else 0.0)
+        d.eps = float(cfg.dual_eps)
+        d.max_iter = int(cfg.dual_max_iter)
+        d.newton_max_iter = int(cfg.newton_max_iter)
+        d.newton_eps = float(cfg.newton_eps)
+        d.lo, d.hi = self.lo, self.hi
+        d.lo_arr = d.hi_arr = d.d = None
+        d.U = U.data_ptr() if rank else None
+        d.v = v.data_ptr()
+        d.p, d.pb, d.p2 = ws.p.data_ptr(), ws.pb.data_ptr(), ws.p2.data_ptr()
+        d.a, d.a2, d.x = ws.a.data_ptr(), ws.a2.data_ptr(), ws.x.data_ptr()
+        d.beta = ws.beta.data_ptr()
+        d.report = ws.report.data_ptr()
+        d.dev_metric = dev_metric
+        return d
+
+    def _prox(self, desc):
+        _abi.check(self.lib.bq_wtv_prox(self.ctx, desc, _abi.stream_ptr(self.dev)), "bqnpm prox")
+
+    def warm_step(self, k):
+        """k <= K_s: single-subset step with B = alpha I, plain TV weight (solvers.py:279-296)."""
+        sigma = kappa(k, 1, self.ks)
+        x = self.ws.x
+        g = self.vs.subset_gradient(self._ids(sigma), x)
+        alpha = self.alphas[sigma - 1]
+        i = sigma - 1
+        self.X[i].copy_(x)
+        self.G[i].copy_(g)
+        self.Us[i].zero_()
+        self.EST[i].zero_()
+        self.EST[i, 0] = alpha
+        self.v.copy_(x - (self.a / alpha) * g)  # v = x - (a / tau) g, the reference's operation order
+        # rank-0 prox; the warm start P / beta is kept in the workspace
+        self._prox(self._desc(self.v, 0, None, alpha, self.a * self.lam, None))
+
+    def _ids(self, sigma):
+        return [self.views[i].view_id for i in self.parts[sigma - 1]]
+
+    def qn_step(self, k):
+        """k > K_s: one device-resident quasi-Newton iteration (solvers.py:281-312)."""
+        ks = self.ks
+        sigma = kappa(k, 1, ks)
+        i = sigma - 1
+        x = self.ws.x
+        g = self.vs.subset_gradient(self._ids(sigma), x)
+        if self.cfg.force_diagonal_metric:
+            self.Us[i].zero_()
+            self.EST[i].zero_()
+            self.EST[i, 0] = self.alphas[i]
+        else:
+            torch.sub(x, self.X[i], out=self.s)
+            torch.sub(g, self.G[i], out=self.m)
+            _abi.check(self.lib.bq_sr1(self.ctx, _abi.dtype_code(self.dt), self.n, self.s.data_ptr(), self.m.data_ptr(),
+                                       float(self.cfg.gamma), self.alphas[i], self.Us[i].data_ptr(),
+                                       self.EST[i].data_ptr(), _abi.stream_ptr(self.dev)), "bqnpm sr1")
+        self.X[i].copy_(x)
+        self.G[i].copy_(g)
+        order = [kappa(k, t, ks) - 1 for t in range(1, ks + 1)]
+        xs = _abi.ptr_array([self.X[o] for o in order])
+        gs = _abi.ptr_array([self.G[o] for o in order])
+        us = _abi.ptr_array([self.Us[o] for o in order])
+        es = _abi.ptr_array([self.EST[o] for o in order])
+        _abi.check(self.lib.bq_bqnpm_metric_vk(self.ctx, _abi.dtype_code(self.dt), self.n, ks, xs, gs, us, es,
+                                               float(self.a), self.Uc.data_ptr(), self.meta.data_ptr(),
+                                               self.acc.data_ptr(), self.v.data_ptr(), _abi.stream_ptr(self.dev)),
+                   "bqnpm metric / v_k")
+        self._prox(self._desc(self.v, ks, self.Uc, 1.0, self.a * ks * self.lam, self.meta.data_ptr()))
+
+    # -- trace on the device ---------------------------------------------------
+    def record(self, k):
+        vs = self.vs
+        ids = [v.view_id for v in self.views]
+        c = vs.costs(ids, self.ws.x).sum() / len(ids)
+        if self.lam:
+            c = c + self.lam * tv_value_async(self.grid, self.ws.x, self.cfg.mode)[0]
+        self.cost[k] = c
+        if self.gt is not None:
+            self.err2[k] = torch.sum((self.ws.x.double() - self.gt) ** 2)
+        if k > 0:
+            self.inner[k] = self.ws.report[_REPORT_ITER * 4:_REPORT_ITER * 4 + 4].view(torch.int32)[0]
+            self.status[k] = self.ws.report[_REPORT_STATUS * 4:_REPORT_STATUS * 4 + 4].view(torch.int32)[0]
+        self.events[k].record()
+
+    # -- the run ---------------------------------------------------------------
+    def run(self, x0, ground_truth, on_iteration, tracer):
+        cfg, ks = self.cfg, self.ks
+        K = cfg.max_outer
+        dev = self.dev
+        self.gt = None if ground_truth is None else torch.as_tensor(np.asarray(ground_truth, dtype=float),
+                                                                     device=dev)
+        self.cost = torch.zeros(K + 1, dtype=torch.float64, device=dev)
+        self.err2 = torch.zeros(K + 1, dtype=torch.float64, device=dev)
+        self.inner = torch.zeros(K + 1, dtype=torch.int32, device=dev)
+        self.status = torch.zeros(K + 1, dtype=torch.int32, device=dev)
+        self.events = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1)]
+        start = torch.cuda.Event(enable_timing=True)
+        main = torch.cuda.current_stream(dev)
+        self.stream.wait_stream(main)
+        with torch.cuda.stream(self.stream):
+            start.record()
+            self.ws.x.copy_(x0)
+            self.ws.p.zero_()
+            self.ws.beta.zero_()
+            self.record(0)
+            for k in range(1, K + 1):
+                if k <= ks:
+                    self.warm_step(k)
+                else:
+                    r = k % ks
+                    if self.use_graphs and k > 2 * ks and r not in self.graphs and self.graph_error is None:
+                        self._capture(k)
+                    if r in self.graphs:
+                        self.graphs[r].replay()
+                    else:
+                        self.qn_step(k)
+                self.record(k)
+                if on_iteration is not None:
+                    self._emit(k, start, tracer, on_iteration)
+        main.wait_stream(self.stream)
+        if on_iteration is None:
+            torch.cuda.synchronize(dev)
+            self._load_host()
+            for k in range(K + 1):
+                self._row(k, start, tracer)
+        st = self.status.cpu().numpy()
+        if np.any(st != 0):
+            _abi.check(int(st[np.nonzero(st)[0][0]]), "bqnpm prox")
+        return self.ws.x.clone()
+
+    def _capture(self, k):
+        r = k % self.ks
+        g = torch.cuda.CUDAGraph()
+        try:
+            with torch.cuda.graph(g, stream=self.stream):
+                self.qn_step(k)
+            self.graphs[r] = g
+        except Exception as exc:  # keep the eager resident path
+            self.graph_error = f"{type(exc).__name__}: {exc}"
+            torch.cuda.synchronize(self.dev)
+            raise RuntimeError(f"CUDA-graph capture of the BQNPM step failed: {self.graph_error}") from exc
+
+    def _load_host(self):
+        self._host = (self.cost.cpu().numpy(), self.err2.cpu().numpy(), self.inner.cpu().numpy())
+        self._gnorm = float(torch.linalg.vector_norm(self.gt).item()) if self.gt is not None else None
+
+    def _row(self, k, start, tracer):
+        from .solvers import TraceRow
+
+        cost, err2, inner = self._host
+        if self.gt is not None:
+            e = math.sqrt(float(err2[k]))
+            snr = math.inf if e == 0.0 else 20.0 * math.log10(self._gnorm / e)
+        else:
+            snr = float("nan")
+        tracer.grad_evals = k
+        row = TraceRow(iteration=k, cost=float(cost[k]), snr_db=snr,
+                       elapsed_s=start.elapsed_time(self.events[k]) * 1e-3, inner_iters=int(inner[k]),
+                       grad_evals=k, full_grad_evals=0)
+        tracer.trace.rows.append(row)
+        if not math.isfinite(row.cost):
+            raise FloatingPointError(f"bqnpm: cost diverged at iteration {k}")
+        return row
+
+    def _emit(self, k, start, tracer, on_iteration):
+        self.events[k].synchronize()
+        self._load_host()
+        row = self._row(k, start, tracer)
+        on_iteration(k, self.ws.x, row, {"metric_meta": self.meta} if k else {})
+
+
+__all__ = ["eligible", "ResidentBqnpm"]
