@@ -29,6 +29,29 @@ from paper_2307_02043_b200.tv_ops import Grid  # noqa: E402
 from paper_2307_02043_b200.wpm import BoxSet  # noqa: E402
 
 
+def loop_only(views, grid, cfg, xgt, reps, init=None):
+    """The outer iterations alone (x0 and the Lipschitz constants computed once,
+    outside the timing): the resident loop (device decisions, CUDA-graph replay)
+    against the host-decision loop, same inputs."""
+    x0 = init(views, grid, cfg.box) if init is not None else S.default_initializer(views, grid, cfg.box)
+    parts = S.partition_views(len(views), cfg.subsets)
+    al = S.estimate_subset_lipschitz(views, parts, x0, cfg.alpha_power_iters, cfg.alpha_safety, cfg.seed)
+    c2 = S.SolverConfig(**{**cfg.__dict__, "alphas": al})
+    out = {}
+    for name, res in (("resident", True), ("host_loop", False)):
+        S.bqnpm_run(views, grid, c2, x0=x0, resident=res)  # warm-up (plans, workspaces, graph capture)
+        ts = []
+        for _ in range(reps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            _, tr = S.bqnpm_run(views, grid, c2, x0=x0, resident=res)
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        out[name] = {"ms_per_outer": 1e3 * float(np.median(ts)) / cfg.max_outer,
+                     "graphs": int(getattr(tr, "graphs", 0))}
+    return out
+
+
 def timed_run(views, grid, cfg, xgt, reps, init=None, n_b=None):
     """`init`: initial-guess function (views, grid, box) -> x0, timed with the run
     (None: the loop's default initializer).  `n_b`: also report the SNR of the
@@ -64,12 +87,15 @@ def measure(reps=3):
     cfg = S.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=20, box=BoxSet(0.0, 0.1), seed=0)
     out["dct_32_L16_bqnpm20"] = timed_run(views, grid, cfg, xgt, reps)
     out["dct_32_L16_bqnpm20"]["reference_cpu_s"] = 4.93  # SURVEY 6, measured on the reference in the survey container
+    out["dct_32_L16_bqnpm20"]["iterations_only"] = loop_only(views, grid, cfg, xgt, reps)
     xgt1 = born_spheres_phantom(n, seed=1000)
     views1, _ = PH.make_scatter_views(n, 16, model="born", x_gt=xgt1, noise_snr_db=30.0, seed=1001,
                                       dtype=torch.complex128, theta_deg=35.0, batch=8)
     out["config1_born_32_L16_bqnpm20"] = timed_run(views1, grid, cfg, xgt1, reps, init=S.scaled_adjoint_initializer,
                                                    n_b=1.333)
     out["config1_born_32_L16_bqnpm20"]["init"] = "scaled_adjoint_initializer (timed)"
+    out["config1_born_32_L16_bqnpm20"]["iterations_only"] = loop_only(views1, grid, cfg, xgt1, reps,
+                                                                      init=S.scaled_adjoint_initializer)
     return out
 
 

@@ -92,6 +92,7 @@ class ResidentBqnpm:
         self.stream = torch.cuda.Stream(dev)
         self.use_graphs = use_graphs
         self.graphs = {}
+        self.seen = set()
         self.graph_error = None
         lo, hi, _, _ = config.box.device_args(dt, dev)
         self.lo, self.hi = lo, hi
@@ -212,14 +213,21 @@ class ResidentBqnpm:
             self.ws.x.copy_(x0)
             self.ws.p.zero_()
             self.ws.beta.zero_()
+            self.meta.zero_()
             self.record(0)
+            if on_iteration is not None:
+                self._emit(0, start, tracer, on_iteration)
             for k in range(1, K + 1):
                 if k <= ks:
                     self.warm_step(k)
                 else:
                     r = k % ks
-                    if self.use_graphs and k > 2 * ks and r not in self.graphs and self.graph_error is None:
+                    # the first pass of each residue runs eagerly (it sizes every lazily
+                    # allocated workspace), the next one is captured; cached instances
+                    # replay from k = K_s + 1
+                    if self.use_graphs and r in self.seen and r not in self.graphs and self.graph_error is None:
                         self._capture(k)
+                    self.seen.add(r)
                     if r in self.graphs:
                         self.graphs[r].replay()
                     else:
@@ -242,8 +250,13 @@ class ResidentBqnpm:
         r = k % self.ks
         g = torch.cuda.CUDAGraph()
         try:
-            with torch.cuda.graph(g, stream=self.stream):
+            # capture on the loop's own stream (its libbq workspace is already
+            # sized); the low-level API skips torch.cuda.graph's gc / cache flush
+            g.capture_begin()
+            try:
                 self.qn_step(k)
+            finally:
+                g.capture_end()
             self.graphs[r] = g
         except Exception as exc:  # keep the eager resident path
             self.graph_error = f"{type(exc).__name__}: {exc}"
@@ -279,4 +292,27 @@ class ResidentBqnpm:
         on_iteration(k, self.ws.x, row, {"metric_meta": self.meta} if k else {})
 
 
-__all__ = ["eligible", "ResidentBqnpm"]
+_CACHE = {}
+_CACHE_MAX = 4
+
+
+def for_run(vs, views, grid, config, parts, alphas, use_graphs=True):
+    """A ResidentBqnpm for this problem, reused (with its captured graphs) by later
+    runs with the same views, schedule, weights and Lipschitz constants -- the
+    graphs hold pointers to the instance's buffers and the host constants of
+    the kernels (alphas, gamma, a, lambda), so only an identical setup may reuse them."""
+    key = (id(vs), grid.dims, config.subsets, config.step, config.tv_weight, config.gamma, config.mode,
+           float(config.box.lower), float(config.box.upper), config.dual_eps, config.dual_max_iter,
+           config.newton_eps, config.newton_max_iter, config.force_diagonal_metric,
+           tuple(float(a) for a in alphas), tuple(tuple(int(i) for i in p) for p in parts),
+           tuple(v.view_id for v in views), use_graphs)
+    inst = _CACHE.get(key)
+    if inst is None or inst.vs is not vs:
+        inst = ResidentBqnpm(vs, views, grid, config, parts, alphas, use_graphs)
+        if len(_CACHE) >= _CACHE_MAX:
+            _CACHE.pop(next(iter(_CACHE)))
+        _CACHE[key] = inst
+    return inst
+
+
+__all__ = ["eligible", "ResidentBqnpm", "for_run"]
