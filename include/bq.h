@@ -176,6 +176,10 @@ typedef struct {
   const void* d;         /* local per-voxel diagonal or NULL */
   const void* U;         /* rank x N local */
   const void* v;         /* N local */
+  double* ctl;           /* optional device control block (>= 128 doubles, see
+                          * bq_slab_ctl): when set, the passes read c and beta
+                          * from it (the host arrays may be NULL) and
+                          * bq_slab_newton is a no-op once the Newton is done */
 } bq_slab_desc;
 
 /* t = D^-1 div(F) over the slab (F: 3 x N; halo_below = F_z of plane z0-1,
@@ -196,6 +200,24 @@ int bq_slab_q(bq_ctx* ctx, const bq_slab_desc* desc, const void* t, const double
 int bq_slab_dual(bq_ctx* ctx, const bq_slab_desc* desc, const void* pbar, const void* p, const void* q,
                  const void* halo_above, double step, double momentum, void* p_next, void* pbar_next,
                  double* norms_out, void* stream);
+
+/* Device control of the sharded solve (one thread; every rank runs it on the
+ * same all-reduced input, so every rank takes the same branch):
+ *   op 0 INIT    ctl <- cap Cholesky factor (`in`, rank x rank, row-major L) and
+ *                beta (`in` + 64), counters cleared
+ *   op 1 COEF    in = s (rank): c = cap^-1 s; Newton state reset (best = inf,
+ *                it = 0, done = rank == 0); beta saved for op 4
+ *   op 2 NEWTON  in = [U^T (w - clamp z) (rank); lower triangle of H]: one step of
+ *                wpm.py:207-224 (residual, best iterate, stop, Levenberg
+ *                fallback); when it stops, beta <- best beta, totals updated
+ *   op 3 NORMS   in = [||P_next - P||^2, ||P||^2]: rel-change (dual_tv_solver.py:
+ *                229-231), fgp_done when rel < eps
+ *   op 4 UNDO    drop a speculative iteration: beta and the Newton total as at op 1
+ * Layout (doubles): [0] done [1] it [2] best_res [3] newton_total [4] rel
+ * [5] fgp_done [6] last_it [8..15] beta [16..23] best beta [24..31] c
+ * [32..39] saved beta [40..103] Cholesky factor. */
+int bq_slab_ctl(bq_ctx* ctx, const bq_slab_desc* desc, int32_t op, const double* in, double newton_eps,
+                int32_t newton_max_iter, double eps, void* stream);
 
 /* ---------------------------------------------------------------------------
  * Standalone TV stencils (tv_ops.py:107-180); the prox kernels fuse them.

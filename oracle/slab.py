@@ -26,6 +26,7 @@ class NumpySlabs:
         self.d = [np.asarray(d[z0 * pl:z1 * pl], float) if d is not None else None for z0, z1 in bounds]
         self.rank, self.sign, self.tau, self.reg = rank, sign, tau, reg
         self.lo, self.hi, self.iso = lo, hi, iso
+        self.cb = {}
 
     # ---- helpers -------------------------------------------------------------
     def _L(self, s):
@@ -86,10 +87,64 @@ class NumpySlabs:
         sv = self.U[s].T @ t if self.rank else np.zeros(0)
         return torch.from_numpy(t), torch.from_numpy(np.asarray(sv, float))
 
-    def newton(self, s, t, c, beta):
+    # ---- control block: the numpy statement of bq_slab_ctl (csrc/slab_prox.cu) ----
+    def ctl(self, op, inp, newton_eps, newton_max_iter, eps):
+        r = self.rank
+        c = self.cb
+        a = None if inp is None else (inp.numpy() if isinstance(inp, torch.Tensor) else np.asarray(inp, float))
+        if op == 0:
+            c.update(L=a[: r * r].reshape(r, r) if r else None, beta=a[64:64 + r].copy(), total=0, fgp=0,
+                     rel=np.inf, done=r == 0)
+        elif op == 1:
+            c["coef"] = np.linalg.solve(c["L"].T, np.linalg.solve(c["L"], a[:r])) if r else np.zeros(0)
+            c.update(saved=c["beta"].copy(), best_beta=c["beta"].copy(), best=np.inf, it=0, last=0, done=r == 0)
+        elif op == 2:
+            if c["done"]:
+                return
+            res_vec = a[:r] + c["beta"]
+            res = float(np.linalg.norm(res_vec))
+            if res < c["best"]:
+                c["best"], c["best_beta"] = res, c["beta"].copy()
+            if res <= newton_eps or c["it"] == newton_max_iter:
+                c["beta"] = c["best_beta"].copy()
+                c["last"] = c["it"]
+                c["total"] += c["it"]
+                c["done"] = True
+                return
+            g = np.zeros((r, r))
+            k = r
+            for i in range(r):
+                for j in range(i + 1):
+                    g[i, j] = g[j, i] = a[k]
+                    k += 1
+            h = np.eye(r) + self.sign * (g / self.tau if self.d[0] is None else g)
+            try:
+                step = np.linalg.solve(h, res_vec)
+            except np.linalg.LinAlgError:
+                mu = 1e-8 * np.linalg.norm(h, np.inf)
+                step = np.linalg.solve(h + mu * np.eye(r), res_vec)
+            c["beta"] = c["beta"] - step
+            c["it"] += 1
+        elif op == 3:
+            num, den = np.sqrt(a[0]), np.sqrt(a[1])
+            c["rel"] = 0.0 if num == 0.0 else (num / den if den > 0.0 else np.inf)
+            c["fgp"] = c["rel"] < eps
+        elif op == 4:
+            c["beta"] = c["saved"].copy()
+            if c["done"]:
+                c["total"] -= c["last"]
+
+    def read_ctl(self):
+        c = self.cb
+        out = np.zeros(128)
+        out[0], out[1], out[3], out[4], out[5], out[6] = c["done"], c["it"], c["total"], c["rel"], c["fgp"], c["last"]
+        out[8:8 + self.rank] = c["beta"]
+        return out
+
+    def newton(self, s, t):
         t = t.numpy()
-        w = self._center(s, t, np.asarray(c))
-        z = self._z(s, w, np.asarray(beta))
+        w = self._center(s, t, self.cb["coef"])
+        z = self._z(s, w, self.cb["beta"])
         q = np.clip(z, self.lo, self.hi)
         U = self.U[s]
         phi = U.T @ (w - q)
@@ -99,9 +154,9 @@ class NumpySlabs:
         tri = [g[i, j] for i in range(self.rank) for j in range(i + 1)]
         return torch.from_numpy(np.concatenate([phi, tri]))
 
-    def q(self, s, t, c, beta):
-        w = self._center(s, t.numpy(), np.asarray(c))
-        return torch.from_numpy(np.clip(self._z(s, w, np.asarray(beta)), self.lo, self.hi))
+    def q(self, s, t):
+        w = self._center(s, t.numpy(), self.cb["coef"])
+        return torch.from_numpy(np.clip(self._z(s, w, self.cb["beta"]), self.lo, self.hi))
 
     def dual(self, s, pbar, p, q, halo, step, mom):
         z0, z1 = self.bounds[s]

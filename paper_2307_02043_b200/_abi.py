@@ -63,6 +63,7 @@ EXPORTS = (
     "bq_tv_project_dual",
     "bq_wpm_phi",
     "bq_bqnpm_metric_vk",
+    "bq_slab_ctl",
 )
 
 
@@ -138,6 +139,7 @@ class SlabDesc(C.Structure):
         ("d", C.c_void_p),
         ("U", C.c_void_p),
         ("v", C.c_void_p),
+        ("ctl", C.c_void_p),
     ]
 
 _P = C.c_void_p
@@ -180,6 +182,7 @@ _SIGS = {
     "bq_slab_div": (C.c_int, [_P, C.POINTER(SlabDesc), _P, _P, _P, _P, _P]),
     "bq_slab_newton": (C.c_int, [_P, C.POINTER(SlabDesc), _P, C.POINTER(_D), C.POINTER(_D), _P, _P]),
     "bq_slab_q": (C.c_int, [_P, C.POINTER(SlabDesc), _P, C.POINTER(_D), C.POINTER(_D), _P, _P]),
+    "bq_slab_ctl": (C.c_int, [_P, C.POINTER(SlabDesc), _I32, _P, _D, _I32, _D, _P]),
     "bq_slab_dual": (C.c_int, [_P, C.POINTER(SlabDesc), _P, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
     "bq_tv_diff": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _I32, _I32, _P, _P, _P]),
     "bq_tv_grad_stack": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _P, _P, _P]),

@@ -45,7 +45,21 @@ struct SlabArgs {
   const void* v;
   double c[BQ_MAX_RANK];     // cap^-1 (U^T D^-1 div)  (Woodbury coefficient, global)
   double beta[BQ_MAX_RANK];  // Newton point
+  const double* ctl;         // optional device control block: c and beta read from it
 };
+
+constexpr int C_DONE = 0, C_IT = 1, C_BEST = 2, C_TOTAL = 3, C_REL = 4, C_FGP = 5, C_LAST = 6, C_BETA = 8,
+              C_BBETA = 16, C_COEF = 24, C_SAVED = 32, C_CHOL = 40;
+
+// c and beta of this launch, in shared memory (from the control block when set)
+template <int R>
+__device__ __forceinline__ void load_cb(const SlabArgs& A, double* s_c, double* s_b) {
+  if (threadIdx.x < R) {
+    s_c[threadIdx.x] = A.ctl ? A.ctl[C_COEF + threadIdx.x] : A.c[threadIdx.x];
+    s_b[threadIdx.x] = A.ctl ? A.ctl[C_BETA + threadIdx.x] : A.beta[threadIdx.x];
+  }
+  __syncthreads();
+}
 
 template <typename T>
 __device__ __forceinline__ T inv_d(const SlabArgs& A, long long j) {
@@ -54,11 +68,11 @@ __device__ __forceinline__ T inv_d(const SlabArgs& A, long long j) {
 
 // w_j = v_j - reg (t_j - sign D^-1 U c)   (dual_tv_solver.py:119-123 with the Woodbury inverse)
 template <typename T, int R>
-__device__ __forceinline__ T center(const SlabArgs& A, const T* __restrict__ t, long long j, T idj) {
+__device__ __forceinline__ T center(const SlabArgs& A, const double* cf, const T* __restrict__ t, long long j, T idj) {
   const T* U = (const T*)A.U;
   T uc = (T)0;
 #pragma unroll
-  for (int k = 0; k < R; ++k) uc += U[k * A.N + j] * (T)A.c[k];
+  for (int k = 0; k < R; ++k) uc += U[k * A.N + j] * (T)cf[k];
   const T corr = (R > 0) ? t[j] - (T)A.sign * uc * idj : t[j];
   return ((const T*)A.v)[j] - (T)A.reg * corr;
 }
@@ -133,6 +147,9 @@ template <typename T, int R>
 __global__ void __launch_bounds__(NT) newton_kernel(SlabArgs A, const T* __restrict__ t, double* out, RedWs ws) {
   __shared__ double red[kMaxVals];
   __shared__ double scr[(NT / 32) * kMaxVals];
+  __shared__ double s_c[R], s_b[R];
+  if (A.ctl && A.ctl[C_DONE] != 0.0) return;  // uniform: the Newton already stopped
+  load_cb<R>(A, s_c, s_b);
   constexpr int NV = R + R * (R + 1) / 2;
   double acc[NV];
 #pragma unroll
@@ -140,13 +157,13 @@ __global__ void __launch_bounds__(NT) newton_kernel(SlabArgs A, const T* __restr
   const T* U = (const T*)A.U;
   for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < A.N; j += (long long)gridDim.x * NT) {
     const T idj = inv_d<T>(A, j);
-    const T w = center<T, R>(A, t, j, idj);
+    const T w = center<T, R>(A, s_c, t, j, idj);
     T u[R];
     T ub = (T)0;
 #pragma unroll
     for (int k = 0; k < R; ++k) {
       u[k] = U[k * A.N + j];
-      ub += u[k] * (T)A.beta[k];
+      ub += u[k] * (T)s_b[k];
     }
     const T z = A.d ? w - (T)A.sign * ub * idj : w - (T)A.sign * ub / (T)A.tau;
     const T q = min(max(z, (T)A.lo), (T)A.hi);
@@ -168,13 +185,16 @@ __global__ void __launch_bounds__(NT) newton_kernel(SlabArgs A, const T* __restr
 // q = clamp(z(beta))   (wpm.py:246-253)
 template <typename T, int R>
 __global__ void __launch_bounds__(NT) q_kernel(SlabArgs A, const T* __restrict__ t, T* __restrict__ q) {
+  constexpr int RR = R > 0 ? R : 1;
+  __shared__ double s_c[RR], s_b[RR];
+  load_cb<R>(A, s_c, s_b);
   const T* U = (const T*)A.U;
   for (long long j = (long long)blockIdx.x * NT + threadIdx.x; j < A.N; j += (long long)gridDim.x * NT) {
     const T idj = inv_d<T>(A, j);
-    const T w = center<T, R>(A, t, j, idj);
+    const T w = center<T, R>(A, s_c, t, j, idj);
     T ub = (T)0;
 #pragma unroll
-    for (int k = 0; k < R; ++k) ub += U[k * A.N + j] * (T)A.beta[k];
+    for (int k = 0; k < R; ++k) ub += U[k * A.N + j] * (T)s_b[k];
     const T z = (R == 0) ? w : (A.d ? w - (T)A.sign * ub * idj : w - (T)A.sign * ub / (T)A.tau);
     q[j] = min(max(z, (T)A.lo), (T)A.hi);
   }
@@ -239,6 +259,137 @@ __global__ void __launch_bounds__(NT) dual_kernel(SlabArgs A, const T* __restric
   if (last_block_reduce<NT, 2>(acc, 2, ws, red, scr) && threadIdx.x < 2) norms[threadIdx.x] = red[threadIdx.x];
 }
 
+// ---------------------------------------------------------------------------
+// device control (bq_slab_ctl): one thread, the reference's scalar logic
+// ---------------------------------------------------------------------------
+__device__ bool lu_solve(double* h, double* b, int r) {
+  for (int k = 0; k < r; ++k) {  // partial pivoting; an exactly zero pivot = singular (LinAlgError)
+    int p = k;
+    for (int i = k + 1; i < r; ++i)
+      if (fabs(h[i * r + k]) > fabs(h[p * r + k])) p = i;
+    if (h[p * r + k] == 0.0) return false;
+    if (p != k) {
+      for (int j = 0; j < r; ++j) {
+        const double tmp = h[k * r + j];
+        h[k * r + j] = h[p * r + j];
+        h[p * r + j] = tmp;
+      }
+      const double tb = b[k];
+      b[k] = b[p];
+      b[p] = tb;
+    }
+    for (int i = k + 1; i < r; ++i) {
+      const double f = h[i * r + k] / h[k * r + k];
+      for (int j = k; j < r; ++j) h[i * r + j] -= f * h[k * r + j];
+      b[i] -= f * b[k];
+    }
+  }
+  for (int i = r - 1; i >= 0; --i) {
+    double s = b[i];
+    for (int j = i + 1; j < r; ++j) s -= h[i * r + j] * b[j];
+    b[i] = s / h[i * r + i];
+  }
+  return true;
+}
+
+__global__ void slab_ctl_kernel(int op, int r, int sign, double tau, int scalar, const double* in, double neps,
+                                int nmax, double eps, double* c) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  switch (op) {
+    case 0: {  // INIT
+      for (int i = 0; i < r * r; ++i) c[C_CHOL + i] = in[i];
+      for (int i = 0; i < r; ++i) c[C_BETA + i] = in[64 + i];
+      c[C_TOTAL] = 0.0;
+      c[C_FGP] = 0.0;
+      c[C_REL] = INFINITY;
+      c[C_DONE] = (r == 0) ? 1.0 : 0.0;
+      return;
+    }
+    case 1: {  // COEF: c = cap^-1 s (L L^T solve), Newton reset
+      const double* L = c + C_CHOL;
+      double b[8];
+      for (int i = 0; i < r; ++i) b[i] = in[i];
+      for (int i = 0; i < r; ++i) {
+        double s = b[i];
+        for (int k = 0; k < i; ++k) s -= L[i * r + k] * b[k];
+        b[i] = s / L[i * r + i];
+      }
+      for (int i = r - 1; i >= 0; --i) {
+        double s = b[i];
+        for (int k = i + 1; k < r; ++k) s -= L[k * r + i] * b[k];
+        b[i] = s / L[i * r + i];
+      }
+      for (int i = 0; i < r; ++i) {
+        c[C_COEF + i] = b[i];
+        c[C_SAVED + i] = c[C_BETA + i];
+        c[C_BBETA + i] = c[C_BETA + i];
+      }
+      c[C_BEST] = INFINITY;
+      c[C_IT] = 0.0;
+      c[C_LAST] = 0.0;
+      c[C_DONE] = (r == 0) ? 1.0 : 0.0;
+      return;
+    }
+    case 2: {  // NEWTON step on the all-reduced residual / Jacobian
+      if (c[C_DONE] != 0.0) return;
+      double phi[8], res2 = 0.0;
+      for (int i = 0; i < r; ++i) {
+        phi[i] = in[i] + c[C_BETA + i];
+        res2 += phi[i] * phi[i];
+      }
+      const double res = sqrt(res2);
+      if (res < c[C_BEST]) {
+        c[C_BEST] = res;
+        for (int i = 0; i < r; ++i) c[C_BBETA + i] = c[C_BETA + i];
+      }
+      const int it = (int)c[C_IT];
+      bool stop = res <= neps || it == nmax;
+      if (!stop) {
+        double h[64], hs[64], st[8];
+        int k = r;
+        for (int i = 0; i < r; ++i)
+          for (int j = 0; j <= i; ++j, ++k) {
+            const double g = scalar ? in[k] / tau : in[k];
+            h[i * r + j] = h[j * r + i] = (i == j ? 1.0 : 0.0) + sign * g;
+          }
+        for (int i = 0; i < r * r; ++i) hs[i] = h[i];
+        for (int i = 0; i < r; ++i) st[i] = phi[i];
+        if (!lu_solve(hs, st, r)) {  // Levenberg fallback, wpm.py:219-223
+          double ninf = 0.0;
+          for (int i = 0; i < r; ++i) {
+            double rs = 0.0;
+            for (int j = 0; j < r; ++j) rs += fabs(h[i * r + j]);
+            ninf = fmax(ninf, rs);
+          }
+          for (int i = 0; i < r * r; ++i) hs[i] = h[i];
+          for (int i = 0; i < r; ++i) hs[i * r + i] += 1e-8 * ninf, st[i] = phi[i];
+          lu_solve(hs, st, r);
+        }
+        for (int i = 0; i < r; ++i) c[C_BETA + i] -= st[i];
+        c[C_IT] = it + 1;
+      } else {
+        for (int i = 0; i < r; ++i) c[C_BETA + i] = c[C_BBETA + i];
+        c[C_LAST] = it;
+        c[C_TOTAL] += it;
+        c[C_DONE] = 1.0;
+      }
+      return;
+    }
+    case 3: {  // NORMS
+      const double num = sqrt(in[0]), den = sqrt(in[1]);
+      const double rel = (num == 0.0) ? 0.0 : (den > 0.0 ? num / den : INFINITY);
+      c[C_REL] = rel;
+      c[C_FGP] = rel < eps ? 1.0 : 0.0;
+      return;
+    }
+    case 4: {  // UNDO a speculative iteration's Newton
+      for (int i = 0; i < r; ++i) c[C_BETA + i] = c[C_SAVED + i];
+      if (c[C_DONE] != 0.0) c[C_TOTAL] -= c[C_LAST];
+      return;
+    }
+  }
+}
+
 template <typename T, int R>
 void launch_newton(int G, cudaStream_t st, const SlabArgs& A, const T* t, double* out, RedWs ws) {
   if constexpr (R > 0) newton_kernel<T, R><<<G, NT, 0, st>>>(A, t, out, ws);
@@ -283,6 +434,7 @@ int make_args(const bq_slab_desc* D, const double* c, const double* beta, SlabAr
   A.d = D->d;
   A.U = D->U;
   A.v = D->v;
+  A.ctl = D->ctl;
   for (int k = 0; k < D->rank; ++k) {
     A.c[k] = c ? c[k] : 0.0;
     A.beta[k] = beta ? beta[k] : 0.0;
@@ -334,7 +486,7 @@ extern "C" int bq_slab_newton(bq_ctx* ctx, const bq_slab_desc* desc, const void*
   SlabArgs A;
   int rc = make_args(desc, c, beta, A);
   if (rc) return rc;
-  BQ_CHECK(ctx && t && out && A.rank >= 1 && c && beta, BQ_EINVAL, "bq_slab_newton: bad arguments");
+  BQ_CHECK(ctx && t && out && A.rank >= 1 && ((c && beta) || A.ctl), BQ_EINVAL, "bq_slab_newton: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   BQ_STREAM_WS(sw, ctx, st);
   RedWs ws = red_ws(sw);
@@ -353,7 +505,7 @@ extern "C" int bq_slab_q(bq_ctx* ctx, const bq_slab_desc* desc, const void* t, c
   SlabArgs A;
   int rc = make_args(desc, c, beta, A);
   if (rc) return rc;
-  BQ_CHECK(ctx && t && q_out && (A.rank == 0 || (c && beta)), BQ_EINVAL, "bq_slab_q: bad arguments");
+  BQ_CHECK(ctx && t && q_out && (A.rank == 0 || (c && beta) || A.ctl), BQ_EINVAL, "bq_slab_q: bad arguments");
   cudaStream_t st = (cudaStream_t)stream;
   const int G = blocks(ctx, A.N);
   if (desc->dtype == BQ_F32) {
@@ -385,6 +537,19 @@ extern "C" int bq_slab_dual(bq_ctx* ctx, const bq_slab_desc* desc, const void* p
     dual_kernel<double><<<G, NT, 0, st>>>(A, (const double*)pbar, (const double*)p, (const double*)q,
                                           (const double*)halo_above, step, momentum, (double*)p_next,
                                           (double*)pbar_next, norms_out, ws);
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+extern "C" int bq_slab_ctl(bq_ctx* ctx, const bq_slab_desc* desc, int32_t op, const double* in, double newton_eps,
+                           int32_t newton_max_iter, double eps, void* stream) {
+  SlabArgs A;
+  int rc = make_args(desc, nullptr, nullptr, A);
+  if (rc) return rc;
+  BQ_CHECK(ctx && A.ctl && op >= 0 && op <= 4 && (in || op == 4), BQ_EINVAL, "bq_slab_ctl: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  slab_ctl_kernel<<<1, 32, 0, st>>>(op, A.rank, A.sign, desc->tau, desc->d == nullptr, in, newton_eps,
+                                    newton_max_iter, eps, desc->ctl);
   BQ_CUDA(cudaGetLastError());
   return BQ_OK;
 }

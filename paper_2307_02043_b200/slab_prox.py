@@ -169,40 +169,24 @@ class SlabGroup:
         return out
 
 
-def _newton(sg: SlabGroup, t, c, beta, rank, sign, tau, scalar, eps, max_iter):
-    """Semi-smooth Newton of wpm.py:170-231 on all-reduced residuals."""
-    best_res, best_beta = math.inf, beta
-    conv = False
-    iters = 0
-    tri = [(i, j) for i in range(rank) for j in range(i + 1)]
-    for iters in range(max_iter + 1):
-        part = sg.reduce([sg.be.newton(s, t[s], c, beta) for s in range(len(t))]).cpu().numpy()
-        res_vec = part[:rank] + beta
-        res = float(np.linalg.norm(res_vec))
-        if res < best_res:
-            best_res, best_beta = res, beta
-        if res <= eps:
-            conv = True
-            break
-        if iters == max_iter:
-            break
-        g = np.zeros((rank, rank))
-        for k, (i, j) in enumerate(tri):
-            g[i, j] = g[j, i] = part[rank + k]
-        h = np.eye(rank) + sign * (g / tau if scalar else g)
-        try:
-            step = np.linalg.solve(h, res_vec)
-        except np.linalg.LinAlgError:
-            mu = _LEVENBERG * np.linalg.norm(h, np.inf)
-            step = np.linalg.solve(h + mu * np.eye(rank), res_vec)
-        beta = beta - step
-    return best_beta, iters, best_res, conv
+# control-block layout (bq_slab_ctl, include/bq.h)
+C_DONE, C_IT, C_BEST, C_TOTAL, C_REL, C_FGP, C_LAST, C_BETA = 0, 1, 2, 3, 4, 5, 6, 8
+OP_INIT, OP_COEF, OP_NEWTON, OP_NORMS, OP_UNDO = 0, 1, 2, 3, 4
 
 
 def slab_solve(sg: SlabGroup, *, rank, sign, tau, scalar, gram, reg, step, eps=1e-5, max_iter=100,
-               accelerated=True, newton_eps=1e-6, newton_max_iter=50, beta0=None, p0=None):
+               accelerated=True, newton_eps=1e-6, newton_max_iter=50, beta0=None, p0=None, spec=2):
     """FGP loop of dual_tv_solver.py:161-250 over the slabs of `sg` (every rank
-    calls it with its own slabs; all control decisions are replicated)."""
+    calls it with its own slabs).
+
+    The scalar control (Woodbury coefficient, the semi-smooth Newton of
+    wpm.py:170-231, the rel-change stop) runs in the backend's control block
+    on the all-reduced sums, so the passes, the all-reduces and the control
+    steps are all stream-ordered.  The host reads the control block once per
+    FGP iteration, after `spec` speculative Newton evaluations (more only when
+    the Newton needs them); the next iteration's divergence and Newton are
+    queued before the host learns whether the current one met the stop test,
+    and are undone (beta, Newton count) when it did."""
     if eps <= 0:
         raise ValueError("eps must be positive")
     if max_iter < 1:
@@ -210,67 +194,83 @@ def slab_solve(sg: SlabGroup, *, rank, sign, tau, scalar, gram, reg, step, eps=1
     be = sg.be
     ns = len(sg.bounds)
     beta = np.zeros(rank) if (beta0 is None or np.shape(beta0)[0] != rank) else np.asarray(beta0, float).copy()
-    cap_l = None
+    init = np.zeros(72)
     if rank:
         cap = np.eye(rank) + sign * (gram / tau if scalar else gram)
-        cap_l = np.linalg.cholesky(cap)
+        init[: rank * rank] = np.linalg.cholesky(cap).reshape(-1)
+        init[64:64 + rank] = beta
+    be.ctl(OP_INIT, init, newton_eps, newton_max_iter, eps)
 
-    def coef(field, halos):
-        """t = D^-1 div(field) per slab and c = cap^-1 U^T t (global)."""
-        out = [be.div(s, field[s], halos[s]) for s in range(ns)]
-        t = [o[0] for o in out]
-        if rank:
-            sv = sg.reduce([o[1] for o in out]).cpu().numpy()
-            c = np.linalg.solve(cap_l.T, np.linalg.solve(cap_l, sv))
-        else:
-            c = np.zeros(0)
-        return t, c
-
-    def prox_of(field, beta):
+    def div_coef(field):
+        """t = D^-1 div(field) per slab, then c = cap^-1 U^T t and a Newton reset."""
         if reg == 0.0:
             t = [be.zeros(s) for s in range(ns)]
-            c = np.zeros(rank)
-        else:
-            halos = sg.halo_up([be.top_plane_z(field[s]) for s in range(ns)])
-            t, c = coef(field, halos)
-        if rank:
-            beta, it, res, conv = _newton(sg, t, c, beta, rank, sign, tau, scalar, newton_eps, newton_max_iter)
-        else:
-            it, res, conv = 0, 0.0, True
-        q = [be.q(s, t[s], c, beta) for s in range(ns)]
-        return q, beta, it, res, conv
+            be.ctl(OP_COEF, np.zeros(max(rank, 1)), newton_eps, newton_max_iter, eps)
+            return t
+        halos = sg.halo_up([be.top_plane_z(field[s]) for s in range(ns)])
+        out = [be.div(s, field[s], halos[s]) for s in range(ns)]
+        sv = sg.reduce([o[1] for o in out]) if rank else np.zeros(1)
+        be.ctl(OP_COEF, sv, newton_eps, newton_max_iter, eps)
+        return [o[0] for o in out]
+
+    def newton_evals(t, count):
+        for _ in range(count if rank else 0):
+            part = sg.reduce([be.newton(s, t[s]) for s in range(ns)])
+            be.ctl(OP_NEWTON, part, newton_eps, newton_max_iter, eps)
+
+    def finish(t, c):
+        while c[C_DONE] == 0.0:
+            newton_evals(t, 1)
+            c = be.read_ctl()
+        return c
 
     p = [be.dual_field(s, None if p0 is None else p0[s]) for s in range(ns)]
     if reg == 0.0:
-        q, beta, it, _, _ = prox_of(p, beta)
+        t = div_coef(p)
+        newton_evals(t, spec)
+        c = finish(t, be.read_ctl())
+        q = [be.q(s, t[s]) for s in range(ns)]
         return SlabReport(x=be.concat(q), p_star=be.concat_dual(p), iterations=1, rel_change=0.0, converged=True,
-                          newton_iterations=it, beta_star=beta)
+                          newton_iterations=int(c[C_TOTAL]), beta_star=np.array(c[C_BETA:C_BETA + rank]))
     pbar = [x.clone() for x in p]
     tk = 1.0
-    newton_total = 0
-    rel = math.inf
     converged = False
     iterations = 0
-    for iterations in range(1, max_iter + 1):
-        q, beta, it, _, _ = prox_of(pbar, beta)
-        newton_total += it
+    t = div_coef(pbar)
+    newton_evals(t, spec)
+    for it in range(1, max_iter + 1):
+        c = be.read_ctl()  # the one host read of the iteration
+        if it > 1 and c[C_FGP] != 0.0:  # iteration it-1 met the stop test: drop the speculative one
+            be.ctl(OP_UNDO, None, newton_eps, newton_max_iter, eps)
+            converged = True
+            break
+        iterations = it
+        finish(t, c)
+        q = [be.q(s, t[s]) for s in range(ns)]
         qh = sg.halo_down([be.bottom_plane(q[s]) for s in range(ns)])
         t_next = 0.5 * (1.0 + math.sqrt(1.0 + 4.0 * tk * tk))
         mom = (tk - 1.0) / t_next if accelerated else 0.0
         outs = [be.dual(s, pbar[s], p[s], q[s], qh[s], step, mom) for s in range(ns)]
-        norms = sg.reduce([o[2] for o in outs]).cpu().numpy()
-        num, den = math.sqrt(norms[0]), math.sqrt(norms[1])
-        rel = 0.0 if num == 0.0 else (num / den if den > 0.0 else math.inf)
+        be.ctl(OP_NORMS, sg.reduce([o[2] for o in outs]), newton_eps, newton_max_iter, eps)
         p = [o[0] for o in outs]
-        if rel < eps:
-            converged = True
-            break
         pbar = [o[1] for o in outs]
-        tk = t_next if accelerated else tk
-    q, beta, it, _, _ = prox_of(p, beta)
-    newton_total += it
-    return SlabReport(x=be.concat(q), p_star=be.concat_dual(p), iterations=iterations, rel_change=float(rel),
-                      converged=converged, newton_iterations=newton_total, beta_star=beta)
+        if accelerated:
+            tk = t_next
+        if it < max_iter:
+            t = div_coef(pbar)
+            newton_evals(t, spec)
+    c = be.read_ctl()
+    if not converged and c[C_FGP] != 0.0:  # the last iteration met the stop test
+        converged = True
+    rel = float(c[C_REL])
+    # final prox at P (dual_tv_solver.py:240-241)
+    t = div_coef(p)
+    newton_evals(t, spec)
+    c = finish(t, be.read_ctl())
+    q = [be.q(s, t[s]) for s in range(ns)]
+    return SlabReport(x=be.concat(q), p_star=be.concat_dual(p), iterations=iterations, rel_change=rel,
+                      converged=converged, newton_iterations=int(c[C_TOTAL]),
+                      beta_star=np.array(c[C_BETA:C_BETA + rank]))
 
 
 class DeviceSlabs:
@@ -307,16 +307,18 @@ class DeviceSlabs:
             self.descs.append(D)
         self.rank = rank
         self._dots = torch.empty(len(bounds), 64, dtype=torch.float64, device=device)
+        self.ctl_buf = torch.zeros(128, dtype=torch.float64, device=device)
+        self._in = torch.zeros(72, dtype=torch.float64, device=device)
+        self._zeros = torch.zeros(72, dtype=torch.float64, device=device)
+        self._host = torch.zeros(128, dtype=torch.float64).pin_memory()
+        for D in self.descs:
+            D.ctl = self.ctl_buf.data_ptr()
 
     def _st(self):
         return _abi.stream_ptr(self.device)
 
     def _n(self, s):
         return self.v[s].numel()
-
-    @staticmethod
-    def _arr(vals):
-        return (C_DOUBLE8)(*(list(vals) + [0.0] * (8 - len(vals))))
 
     def zeros(self, s):
         return torch.zeros(self._n(s), dtype=self.dtype, device=self.device)
@@ -339,18 +341,40 @@ class DeviceSlabs:
                                         sv.data_ptr() if self.rank else None, self._st()), "slab div")
         return t, sv[: self.rank].clone()
 
-    def newton(self, s, t, c, beta):
+    def newton(self, s, t):
         nv = self.rank + self.rank * (self.rank + 1) // 2
         out = self._dots[s, 8:8 + nv]
-        _abi.check(self.lib.bq_slab_newton(self.ctx, self.descs[s], t.data_ptr(), self._arr(c), self._arr(beta),
-                                           out.data_ptr(), self._st()), "slab newton")
+        _abi.check(self.lib.bq_slab_newton(self.ctx, self.descs[s], t.data_ptr(), None, None, out.data_ptr(),
+                                           self._st()), "slab newton")
         return out.clone()
 
-    def q(self, s, t, c, beta):
+    def q(self, s, t):
         q = torch.empty(self._n(s), dtype=self.dtype, device=self.device)
-        _abi.check(self.lib.bq_slab_q(self.ctx, self.descs[s], t.data_ptr(), self._arr(c), self._arr(beta),
-                                      q.data_ptr(), self._st()), "slab q")
+        _abi.check(self.lib.bq_slab_q(self.ctx, self.descs[s], t.data_ptr(), None, None, q.data_ptr(), self._st()),
+                   "slab q")
         return q
+
+    def ctl(self, op, inp, newton_eps, newton_max_iter, eps):
+        """One control step on the (all-reduced) input, stream-ordered (bq_slab_ctl)."""
+        ptr = None
+        if inp is not None:
+            if isinstance(inp, torch.Tensor):
+                ptr = inp.data_ptr()
+                self._keep = inp
+            else:  # host array: INIT (once per solve) or the all-zero rank-0 / reg-0 input
+                a = np.asarray(inp, dtype=float)
+                if np.any(a):
+                    self._in[: len(a)].copy_(torch.as_tensor(a))
+                    ptr = self._in.data_ptr()
+                else:
+                    ptr = self._zeros.data_ptr()
+        _abi.check(self.lib.bq_slab_ctl(self.ctx, self.descs[0], int(op), ptr, float(newton_eps),
+                                        int(newton_max_iter), float(eps), self._st()), "slab ctl")
+
+    def read_ctl(self):
+        self._host.copy_(self.ctl_buf, non_blocking=True)
+        torch.cuda.current_stream(self.device).synchronize()
+        return self._host.numpy()
 
     def dual(self, s, pbar, p, q, halo, step, mom):
         pn = torch.empty_like(p)
@@ -366,11 +390,6 @@ class DeviceSlabs:
 
     def concat_dual(self, parts):
         return torch.cat(parts, dim=1)
-
-
-import ctypes as _C  # noqa: E402
-
-C_DOUBLE8 = _C.c_double * 8
 
 
 def solve_sharded(grid, v, w, reg, box, *, group=None, slabs_per_rank=1, mode=TvMode.ISOTROPIC, omega=None,

@@ -116,3 +116,24 @@ def test_gloo_world2_slab_prox_matches_unsharded(kind, per_rank):
     for r in range(2):
         assert out[r][2] == ref["iterations"] and out[r][3] == ref["newton_iterations"]
     np.testing.assert_array_equal(out[0][4], out[1][4])  # replicated controller: identical beta on both ranks
+
+
+@pytest.mark.parametrize("kind", ["diag", "tau2"])
+def test_tolerance_stop_undoes_the_speculative_iteration(kind):
+    """eps-stopped solve: the next iteration is queued before the stop test is
+    known and must be undone (beta, Newton count) -- same result as the oracle."""
+    dims, v, c = _case(kind)
+    w = O.Metric(tau=c["tau"] if c["d"] is None else None, U=c["U"], sign=c["sign"], d=c["d"], n=v.size)
+    ref = O.fgp_prox(dims, v, w, reg=c["reg"], lo=c["lo"], hi=c["hi"], isotropic=c["iso"], eps=2e-3, max_iter=500)
+    r = c["U"].shape[1]
+    be = NumpySlabs(dims, SP.slab_bounds(dims[2], 3), dims[2], v, c["U"], c["d"], rank=r, sign=c["sign"],
+                    tau=c["tau"], reg=c["reg"], lo=c["lo"], hi=c["hi"], iso=c["iso"])
+    gram = (c["U"].T @ (c["U"] / c["d"][:, None]) if c["d"] is not None else c["U"].T @ c["U"]) if r else None
+    step = 1.0 / (4.0 * 3 * (1.0 / w.min_diag()) * c["reg"])
+    sg = SP.SlabGroup(be, SP.Comm(None), dims, SP.slab_bounds(dims[2], 3), dims[2])
+    rep = SP.slab_solve(sg, rank=r, sign=c["sign"], tau=c["tau"], scalar=c["d"] is None, gram=gram, reg=c["reg"],
+                        step=step, eps=2e-3, max_iter=500)
+    assert ref["converged"] and rep.converged and rep.iterations == ref["iterations"] < 500
+    assert rep.newton_iterations == ref["newton_iterations"]
+    assert rep.rel_change == pytest.approx(ref["rel_change"], rel=1e-9)
+    assert np.linalg.norm(rep.x.numpy() - ref["x"]) <= 1e-12 * np.linalg.norm(ref["x"])
