@@ -9,23 +9,26 @@ on the device:
 
 * ``bq_sr1`` decides accept / fallback on the device (a zero step gives
   (alpha, no u), exactly the loop's ``not np.any(s)`` branch);
-* ``bq_bqnpm_metric_vk`` aggregates the slots into tau_w and a fixed
-  K_s-column U with the accepted columns compacted in slot order and zero
-  columns after (a zero column changes neither W, the Woodbury solve nor the
-  Newton iteration), and computes v_k;
+* ``bq_bqnpm_metric_vk`` aggregates the slots into tau_w and a K_s-column U
+  buffer with the accepted columns compacted in slot order (zero columns
+  after), writes the effective rank, and computes v_k;
 * the fused prox kernel reads tau_w and the effective rank from device memory
   (``bq_wtv_desc::dev_metric``): it forms the dual step from tau_w exactly as
   ``dual_step_size`` does and drops the beta warm start when the effective
   rank changed (dual_tv_solver.py:185-186).
 
-So one iteration is a fixed sequence of launches with fixed pointers; it
-depends on k only through k mod K_s (the subset and the kappa slot order).
-The first 2 K_s iterations run eagerly on a side stream (they also size
-every lazily allocated workspace), then one CUDA graph per residue class is
-captured on that stream and replayed.  The trace (cost, SNR, inner
-iterations, elapsed device time) is recorded on the device and read once at
-the end, so the host never waits on the GPU inside the loop -- unless an
-``on_iteration`` callback is given, which needs each row as it happens.
+One iteration is then two fixed launch sequences with fixed pointers: A (the
+gradient, SR1, slot refresh, metric and v_k; it depends on k only through
+k mod K_s) and B (the prox).  The prox kernel is specialised on the rank
+(a rank-4 prox costs 1.5x a rank-1 prox at 32^3), so the host reads ONE
+scalar per iteration -- the effective rank, copied to pinned memory at the
+end of A -- and replays B for that rank.  Every (A, residue) and (B,
+residue, rank) sequence is captured as a CUDA graph the second time it comes
+up (the first run is eager; all workspaces are sized before the first
+capture) and replayed afterwards.  The trace (cost, SNR, inner iterations,
+elapsed device time) is recorded on the device and read once at the end --
+unless an ``on_iteration`` callback is given, which needs each row as it
+happens.
 """
 
 from __future__ import annotations
@@ -93,7 +96,9 @@ class ResidentBqnpm:
         self.use_graphs = use_graphs
         self.graphs = {}
         self.seen = set()
-        self.graph_error = None
+        self.sized = False
+        self.rank_host = torch.zeros(1, dtype=torch.float64).pin_memory()
+        self.rank_ev = torch.cuda.Event()
         lo, hi, _, _ = config.box.device_args(dt, dev)
         self.lo, self.hi = lo, hi
 
@@ -176,7 +181,28 @@ class ResidentBqnpm:
                                                float(self.a), self.Uc.data_ptr(), self.meta.data_ptr(),
                                                self.acc.data_ptr(), self.v.data_ptr(), _abi.stream_ptr(self.dev)),
                    "bqnpm metric / v_k")
-        self._prox(self._desc(self.v, ks, self.Uc, 1.0, self.a * ks * self.lam, self.meta.data_ptr()))
+        self.rank_host.copy_(self.meta[1:2], non_blocking=True)  # the one scalar the host reads
+
+    def qn_prox(self, rank):
+        """The prox at the effective rank (its kernel is specialised on the rank):
+        the first `rank` columns of the compacted U, tau and the warm-start rule
+        from the device scalars."""
+        self._prox(self._desc(self.v, rank, self.Uc, 1.0, self.a * self.ks * self.lam, self.meta.data_ptr()))
+
+    def size_workspaces(self):
+        """One throwaway 1-iteration prox per rank 0..K_s on scratch buffers, so the
+        lazily allocated near-list workspace of the loop's stream has its final
+        size before any graph captures a pointer to it."""
+        ws, v0 = dts.ProxWorkspace(self.grid, self.dt, self.dev), torch.zeros_like(self.v)
+        U0 = torch.zeros_like(self.Uc)
+        for r in range(self.ks + 1):
+            d = self._desc(v0, r, U0, 1.0, 1.0, None)
+            d.p, d.pb, d.p2 = ws.p.data_ptr(), ws.pb.data_ptr(), ws.p2.data_ptr()
+            d.a, d.a2, d.x = ws.a.data_ptr(), ws.a2.data_ptr(), ws.x.data_ptr()
+            d.beta, d.report = ws.beta.data_ptr(), ws.report.data_ptr()
+            d.max_iter = 1
+            self._prox(d)
+        torch.cuda.current_stream(self.dev).synchronize()
 
     # -- trace on the device ---------------------------------------------------
     def record(self, k):
@@ -221,17 +247,17 @@ class ResidentBqnpm:
                 if k <= ks:
                     self.warm_step(k)
                 else:
-                    r = k % ks
-                    # the first pass of each residue runs eagerly (it sizes every lazily
-                    # allocated workspace), the next one is captured; cached instances
-                    # replay from k = K_s + 1
-                    if self.use_graphs and r in self.seen and r not in self.graphs and self.graph_error is None:
-                        self._capture(k)
-                    self.seen.add(r)
-                    if r in self.graphs:
-                        self.graphs[r].replay()
-                    else:
-                        self.qn_step(k)
+                    # graph A(k mod K_s): gradient, SR1, slot refresh, metric and v_k;
+                    # the host reads the effective rank (one small D2H per iteration)
+                    # and replays graph B(k mod K_s, rank): the rank-specialised prox.
+                    # Each graph is captured the second time its key comes up (the
+                    # first run is eager); cached instances replay from k = K_s + 1.
+                    res = k % ks
+                    self._run_graph(("pre", res), lambda: self.qn_step(k))
+                    self.rank_ev.record()
+                    self.rank_ev.synchronize()
+                    rank = int(self.rank_host[0])
+                    self._run_graph(("prox", res, rank), lambda: self.qn_prox(rank))
                 self.record(k)
                 if on_iteration is not None:
                     self._emit(k, start, tracer, on_iteration)
@@ -246,22 +272,27 @@ class ResidentBqnpm:
             _abi.check(int(st[np.nonzero(st)[0][0]]), "bqnpm prox")
         return self.ws.x.clone()
 
-    def _capture(self, k):
-        r = k % self.ks
+    def _run_graph(self, key, fn):
+        if key in self.graphs:
+            self.graphs[key].replay()
+            return
+        if not self.use_graphs or key not in self.seen:
+            self.seen.add(key)
+            fn()
+            return
+        if not self.sized:
+            self.size_workspaces()
+            self.sized = True
         g = torch.cuda.CUDAGraph()
+        # capture on the loop's own stream (its libbq workspace is already sized);
+        # the low-level API skips torch.cuda.graph's gc / cache flush
+        g.capture_begin()
         try:
-            # capture on the loop's own stream (its libbq workspace is already
-            # sized); the low-level API skips torch.cuda.graph's gc / cache flush
-            g.capture_begin()
-            try:
-                self.qn_step(k)
-            finally:
-                g.capture_end()
-            self.graphs[r] = g
-        except Exception as exc:  # keep the eager resident path
-            self.graph_error = f"{type(exc).__name__}: {exc}"
-            torch.cuda.synchronize(self.dev)
-            raise RuntimeError(f"CUDA-graph capture of the BQNPM step failed: {self.graph_error}") from exc
+            fn()
+        finally:
+            g.capture_end()
+        self.graphs[key] = g
+        g.replay()
 
     def _load_host(self):
         self._host = (self.cost.cpu().numpy(), self.err2.cpu().numpy(), self.inner.cpu().numpy())

@@ -36,7 +36,8 @@ def test_resident_matches_host_loop(monkeypatch, tag, dims, graphs):
     cfg = S.SolverConfig(subsets=4, tv_weight=2e-3, max_outer=24, box=BoxSet(1.3, 1.4), seed=0)
     xr, tr = S.bqnpm_run(views, g, cfg, resident=True)
     xh, th = S.bqnpm_run(views, g, cfg, resident=False)
-    assert getattr(tr, "graphs", 0) == (4 if graphs == "1" else 0)
+    ng = getattr(tr, "graphs", 0)
+    assert (ng >= 5) if graphs == "1" else ng == 0  # 4 pre-prox graphs + >= 1 prox graph
     assert rel_l2(xr, xh) <= 1e-11
     np.testing.assert_allclose(tr.column("cost"), th.column("cost"), rtol=1e-11)
     np.testing.assert_array_equal(tr.column("inner_iters"), th.column("inner_iters"))
@@ -68,7 +69,7 @@ def test_resident_born_config1_golden():
     cfg = S.SolverConfig(subsets=4, tv_weight=1e-3, max_outer=20, box=BoxSet(0.0, 0.1), seed=0,
                          alphas=z["c1_alphas"])
     x, tr = S.bqnpm_run(views, Grid((32, 32, 32)), cfg, x0=z["c1_x0"], ground_truth=z["c1_xgt"], resident=True)
-    assert tr.graphs == 4
+    assert tr.graphs >= 5
     assert rel_l2(x, z["c1_x"]) <= 1e-8
     np.testing.assert_allclose(tr.column("cost"), z["c1_cost"], rtol=1e-8)
     np.testing.assert_array_equal(tr.column("inner_iters"), z["c1_inner"])
