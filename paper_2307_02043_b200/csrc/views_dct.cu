@@ -13,6 +13,8 @@
 // ONE inverse DCT.  The DCTs are exact separable matrix transforms along each
 // axis (cosine table in shared memory, one block per line batch, f64
 // accumulation for f64 data), matching scipy's orthonormal DCT to ~1e-15.
+#include <mutex>
+
 #include "common.cuh"
 
 namespace bq {
@@ -51,6 +53,76 @@ __global__ void dct_axis_kernel(const T* __restrict__ in, T* __restrict__ out, i
       }
       out[base + (long long)k * stride] = (T)acc;
     }
+  }
+}
+
+// Tiled variant for n <= 128 (every axis of the reference's grids): one block
+// transforms LB = 32 lines.  The orthonormal table comes precomputed from
+// global memory (dct_table, one per n, built once), the tile of 32 lines is
+// staged in shared memory with coalesced loads (along the lines for the x
+// axis, across adjacent lines for the strided axes), and each thread forms
+// n/8 outputs of one line: warps share k, so the table read is a broadcast
+// and the tile read is conflict-free.  Same f64 accumulation order as
+// dct_axis_kernel (m ascending), so the results are bit-identical to it.
+constexpr int DLB = 32;
+template <typename T>
+__global__ void __launch_bounds__(256) dct_tile_kernel(const T* __restrict__ in, T* __restrict__ out,
+                                                       const double* __restrict__ tab, int n, long long stride,
+                                                       long long inner, long long nlines, int inverse) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* C = reinterpret_cast<double*>(smem_raw);  // n*n
+  double* xs = C + n * n;                           // n rows of DLB+1 (padded)
+  constexpr int LP = DLB + 1;
+  for (int i = threadIdx.x; i < n * n; i += blockDim.x) {
+    const int k = i / n, m = i - k * n;
+    C[i] = inverse ? tab[m * n + k] : tab[i];  // C[k][m]: the coefficient of x[m] in out[k]
+  }
+  const bool xaxis = stride == 1;
+  for (long long l0 = (long long)blockIdx.x * DLB; l0 < nlines; l0 += (long long)gridDim.x * DLB) {
+    const int nl = (int)min((long long)DLB, nlines - l0);
+    __syncthreads();
+    for (int e = threadIdx.x; e < DLB * n; e += blockDim.x) {
+      int l, m;
+      if (xaxis) l = e / n, m = e - (e / n) * n;
+      else m = e / DLB, l = e - (e / DLB) * DLB;
+      if (l < nl) {
+        const long long line = l0 + l;
+        const long long outer = line / inner, inn = line - outer * inner;
+        xs[m * LP + l] = (double)in[outer * (long long)n * stride + inn + (long long)m * stride];
+      }
+    }
+    __syncthreads();
+    const int l = threadIdx.x % DLB;
+    double res[16];
+    int nk = 0;
+    for (int k = threadIdx.x / DLB; k < n; k += blockDim.x / DLB, ++nk) {
+      double acc = 0.0;
+      const double* ck = C + k * n;
+      for (int m = 0; m < n; ++m) acc += ck[m] * xs[m * LP + l];
+      res[nk] = acc;
+    }
+    __syncthreads();  // every thread has read the tile: reuse it for the outputs
+    nk = 0;
+    for (int k = threadIdx.x / DLB; k < n; k += blockDim.x / DLB, ++nk) xs[k * LP + l] = res[nk];
+    __syncthreads();
+    for (int e = threadIdx.x; e < DLB * n; e += blockDim.x) {
+      int ll, k;
+      if (xaxis) ll = e / n, k = e - (e / n) * n;
+      else k = e / DLB, ll = e - (e / DLB) * DLB;
+      if (ll < nl) {
+        const long long line = l0 + ll;
+        const long long outer = line / inner, inn = line - outer * inner;
+        out[outer * (long long)n * stride + inn + (long long)k * stride] = (T)xs[k * LP + ll];
+      }
+    }
+  }
+}
+
+__global__ void dct_table_kernel(double* tab, int n) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * n; i += gridDim.x * blockDim.x) {
+    const int k = i / n, m = i % n;
+    const double ck = (k == 0) ? sqrt(1.0 / n) : sqrt(2.0 / n);
+    tab[i] = ck * cospi((double)k * (2 * m + 1) / (2.0 * n));  // the table of dct_axis_kernel
   }
 }
 
@@ -146,6 +218,28 @@ int grid_for(bq_ctx* ctx, long long n, int nt) {
   return (int)std::max<long long>(1, std::min<long long>(want, (long long)ctx->num_sms * 8));
 }
 
+// orthonormal DCT tables, one per (context, n), built once on first use
+struct DctTab {
+  bq_ctx* ctx;
+  int n;
+  double* tab;
+};
+DctTab g_tabs[64];
+int g_ntabs = 0;
+std::mutex g_tab_mu;
+
+const double* dct_table(bq_ctx* ctx, int n, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(g_tab_mu);
+  for (int i = 0; i < g_ntabs; ++i)
+    if (g_tabs[i].ctx == ctx && g_tabs[i].n == n) return g_tabs[i].tab;
+  if (g_ntabs == 64) return nullptr;
+  double* tab = nullptr;
+  if (cudaMalloc(&tab, (size_t)n * n * sizeof(double)) != cudaSuccess) return nullptr;
+  dct_table_kernel<<<(n * n + 255) / 256, 256, 0, st>>>(tab, n);
+  g_tabs[g_ntabs++] = DctTab{ctx, n, tab};
+  return tab;
+}
+
 }  // namespace
 }  // namespace bq
 
@@ -163,6 +257,22 @@ extern "C" int bq_dct_axis(bq_ctx* ctx, int32_t dtype, const int64_t* dims, int3
   const long long nlines = total / n;
   const long long inner = stride;
   cudaStream_t st = (cudaStream_t)stream;
+  if (n <= 128 && !getenv("BQ_DCT_NAIVE")) {
+    const double* tab = dct_table(ctx, n, st);
+    BQ_CHECK(tab, BQ_ECUDA, "bq_dct_axis: table allocation failed");
+    const size_t shm = ((size_t)n * n + (size_t)n * (DLB + 1)) * sizeof(double);
+    const int G = (int)std::max<long long>(1, std::min<long long>((nlines + DLB - 1) / DLB, (long long)ctx->num_sms * 8));
+    if (dtype == BQ_F32) {
+      BQ_CUDA(cudaFuncSetAttribute(dct_tile_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      dct_tile_kernel<float><<<G, 256, shm, st>>>((const float*)in, (float*)out, tab, n, stride, inner, nlines, inverse);
+    } else {
+      BQ_CUDA(cudaFuncSetAttribute(dct_tile_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+      dct_tile_kernel<double><<<G, 256, shm, st>>>((const double*)in, (double*)out, tab, n, stride, inner, nlines,
+                                                   inverse);
+    }
+    BQ_CUDA(cudaGetLastError());
+    return BQ_OK;
+  }
   const size_t shm = n <= 128 ? (size_t)n * n * sizeof(double) : 0;
   const int nt = n <= 128 ? 128 : 256;
   const int G = (int)std::min<long long>(nlines, (long long)ctx->num_sms * 16);

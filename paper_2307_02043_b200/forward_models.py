@@ -123,8 +123,11 @@ class DctViewSet:
         return r, cost
 
     def _mask(self, v):
-        m = torch.from_numpy(self.masks_host[v].astype(np.float64)).to(self.device, self.dtype)
-        return m
+        """View v's 0/1 mask on the device, uploaded once per view (not per call)."""
+        cache = self.__dict__.setdefault("_mask_cache", {})
+        if v not in cache:
+            cache[v] = torch.from_numpy(self.masks_host[v].astype(np.float64)).to(self.device, self.dtype)
+        return cache[v]
 
     # -- the reference's closures (forward_models.py:166-183) -------------
     def fmap(self, x):
