@@ -255,6 +255,13 @@ int bq_metric_apply(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, int32_t
                     const void* d, const void* U, const double* gram, int32_t inverse,
                     const void* x, void* out, void* stream);
 
+/* Construction-time check of W = diag(d) + sign U U^T in one pass with a small
+ * per-SM footprint (it can run beside a persistent prox): out (device, 1 +
+ * rank*rank doubles) = [min(d) (+inf when d == NULL), U^T D^-1 U (D = I when
+ * d == NULL; row-major)]. */
+int bq_metric_check(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, const void* d, const void* U,
+                    double* out, void* stream);
+
 /* dots_out[k] = <a_k, b_k> for k < count (device doubles). */
 int bq_dot(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t count, const void* const* a_ptrs,
            const void* const* b_ptrs, double* dots_out, void* stream);

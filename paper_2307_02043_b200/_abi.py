@@ -64,6 +64,7 @@ EXPORTS = (
     "bq_wpm_phi",
     "bq_bqnpm_metric_vk",
     "bq_slab_ctl",
+    "bq_metric_check",
 )
 
 
@@ -182,6 +183,7 @@ _SIGS = {
     "bq_slab_div": (C.c_int, [_P, C.POINTER(SlabDesc), _P, _P, _P, _P, _P]),
     "bq_slab_newton": (C.c_int, [_P, C.POINTER(SlabDesc), _P, C.POINTER(_D), C.POINTER(_D), _P, _P]),
     "bq_slab_q": (C.c_int, [_P, C.POINTER(SlabDesc), _P, C.POINTER(_D), C.POINTER(_D), _P, _P]),
+    "bq_metric_check": (C.c_int, [_P, _I32, _I64, _I32, _P, _P, _P, _P]),
     "bq_slab_ctl": (C.c_int, [_P, C.POINTER(SlabDesc), _I32, _P, _D, _I32, _D, _P]),
     "bq_slab_dual": (C.c_int, [_P, C.POINTER(SlabDesc), _P, _P, _P, _P, _D, _D, _P, _P, _P, _P]),
     "bq_tv_diff": (C.c_int, [_P, _I32, _I32, C.POINTER(_I64), _I32, _I32, _P, _P, _P]),

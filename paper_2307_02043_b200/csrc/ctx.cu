@@ -52,8 +52,11 @@ StreamWs* stream_ws(bq_ctx* ctx, cudaStream_t st) {
       (e = cudaMalloc(&w->ws.barrier, 64)) != cudaSuccess ||
       (e = cudaMalloc(&w->ws.ctl, w->ws.ctl_bytes)) != cudaSuccess ||
       (e = cudaMalloc(&w->ws.scratch, sizeof(double) * 4096)) != cudaSuccess ||
-      (e = cudaMemset(w->ws.barrier, 0, 64)) != cudaSuccess ||
-      (e = cudaMemset(w->ws.ctl, 0, w->ws.ctl_bytes)) != cudaSuccess) {
+      // zeroed ON the stream that will use them: a plain cudaMemset would queue on
+      // the legacy default stream, behind whatever runs there, and a kernel on a
+      // non-blocking stream could read the counters before they are cleared
+      (e = cudaMemsetAsync(w->ws.barrier, 0, 64, st)) != cudaSuccess ||
+      (e = cudaMemsetAsync(w->ws.ctl, 0, w->ws.ctl_bytes, st)) != cudaSuccess) {
     stream_ws_free(w);
     cuda_fail(e, "bq stream workspace");
     return nullptr;

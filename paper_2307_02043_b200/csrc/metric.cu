@@ -383,6 +383,82 @@ __global__ void __launch_bounds__(NT) phi_kernel(long long n, int sign, double t
   }
 }
 
+
+// --------------------- metric check (gram + min(d)) ---------------------------
+// DiagPlusLowRank's construction-time validation in ONE small-footprint pass:
+// min(d) (the positivity test and omega, D-6) and the gram U^T D^-1 U.  128
+// threads and ~4 KB of shared memory per block, at most one block per SM: it
+// fits beside a running persistent prox block (1 block / SM, ~200 KB smem), so
+// the next problem's build can overlap the current solve (bench e2e).
+constexpr int NTC = 128;
+template <typename T, int R>
+__global__ void __launch_bounds__(NTC, 16) check_kernel(long long n, const T* __restrict__ d, const T* __restrict__ U,
+                                                       double* out, double* partials, unsigned* count) {
+  constexpr int NA = R * (R + 1) / 2 > 0 ? R * (R + 1) / 2 : 1;
+  __shared__ double s_w[NTC / 32][NA + 1];
+  __shared__ int s_last;
+  double acc[NA];
+#pragma unroll
+  for (int k = 0; k < NA; ++k) acc[k] = 0.0;
+  double mn = INFINITY;
+#pragma unroll 4
+  for (long long j = (long long)blockIdx.x * NTC + threadIdx.x; j < n; j += (long long)gridDim.x * NTC) {
+    const T e = d ? d[j] : (T)1;
+    if (d) mn = (e == e) ? fmin(mn, (double)e) : -INFINITY;  // a NaN fails the d > 0 test
+    if (R > 0) {
+      T u[R > 0 ? R : 1];
+#pragma unroll
+      for (int c = 0; c < R; ++c) u[c] = U[c * n + j];
+      int k = 0;
+#pragma unroll
+      for (int c = 0; c < R; ++c)
+#pragma unroll
+        for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += d ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_down_sync(0xffffffffu, mn, o));
+#pragma unroll
+  for (int k = 0; k < NA; ++k)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[k] += __shfl_down_sync(0xffffffffu, acc[k], o);
+  if (lane == 0) {
+    s_w[warp][0] = mn;
+    for (int k = 0; k < NA; ++k) s_w[warp][k + 1] = acc[k];
+  }
+  __syncthreads();
+  if (threadIdx.x <= NA) {  // block partial, fixed warp order
+    double v = s_w[0][threadIdx.x];
+    for (int w = 1; w < NTC / 32; ++w) v = threadIdx.x == 0 ? fmin(v, s_w[w][0]) : v + s_w[w][threadIdx.x];
+    partials[(size_t)blockIdx.x * kMaxVals + threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    s_last = atomicAdd(count, 1u) == gridDim.x - 1;
+    if (s_last) __threadfence();
+  }
+  __syncthreads();
+  if (!s_last) return;
+  if (threadIdx.x <= NA) {  // totals in block order (deterministic)
+    double v = __ldcg(&partials[threadIdx.x]);
+    for (unsigned b = 1; b < gridDim.x; ++b) {
+      const double p = __ldcg(&partials[(size_t)b * kMaxVals + threadIdx.x]);
+      v = threadIdx.x == 0 ? fmin(v, p) : v + p;
+    }
+    s_w[0][threadIdx.x] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    out[0] = s_w[0][0];
+    int k = 0;
+    for (int c = 0; c < R; ++c)
+      for (int c2 = 0; c2 <= c; ++c2, ++k) out[1 + c * R + c2] = out[1 + c2 * R + c] = s_w[0][k + 1];
+    *count = 0;
+  }
+}
+
 #define RANK_SWITCH(r, BODY)                       \
   switch (r) {                                     \
     case 1: { constexpr int R = 1; BODY; } break;  \
@@ -594,6 +670,38 @@ extern "C" int bq_wpm_phi(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, i
                                                                 (const double*)x, lo, hi, (const double*)lo_arr,
                                                                 (const double*)hi_arr, beta, phi_out, jac_out, ws)));
   }
+  BQ_CUDA(cudaGetLastError());
+  return BQ_OK;
+}
+
+extern "C" int bq_metric_check(bq_ctx* ctx, int32_t dtype, int64_t n, int32_t rank, const void* d, const void* U,
+                               double* out, void* stream) {
+  BQ_CHECK(ctx && out && n > 0 && rank >= 0 && rank <= BQ_MAX_RANK && (rank == 0 || U), BQ_EINVAL,
+           "bq_metric_check: bad arguments");
+  cudaStream_t st = (cudaStream_t)stream;
+  BQ_STREAM_WS(sw, ctx, st);
+  const int G = (int)std::max<long long>(1, std::min<long long>((n + NTC * 8 - 1) / (NTC * 8), ctx->num_sms));
+  double* part = sw->ws.partials;
+  unsigned* cnt = sw->ws.barrier + 8;
+  // the carveout of a running persistent prox (maximum shared memory): a block
+  // with another preferred split could not share the SM with it
+#define CHECK_CASE(RR)                                                                                              \
+  case RR:                                                                                                          \
+    if (dtype == BQ_F32) {                                                                                          \
+      cudaFuncSetAttribute(check_kernel<float, RR>, cudaFuncAttributePreferredSharedMemoryCarveout,                 \
+                           cudaSharedmemCarveoutMaxShared);                                                         \
+      check_kernel<float, RR><<<G, NTC, 0, st>>>(n, (const float*)d, (const float*)U, out, part, cnt);             \
+    } else {                                                                                                        \
+      cudaFuncSetAttribute(check_kernel<double, RR>, cudaFuncAttributePreferredSharedMemoryCarveout,                \
+                           cudaSharedmemCarveoutMaxShared);                                                         \
+      check_kernel<double, RR><<<G, NTC, 0, st>>>(n, (const double*)d, (const double*)U, out, part, cnt);          \
+    }                                                                                                               \
+    break;
+  switch (rank) {
+    CHECK_CASE(0) CHECK_CASE(1) CHECK_CASE(2) CHECK_CASE(3) CHECK_CASE(4) CHECK_CASE(5) CHECK_CASE(6) CHECK_CASE(7)
+    CHECK_CASE(8)
+  }
+#undef CHECK_CASE
   BQ_CUDA(cudaGetLastError());
   return BQ_OK;
 }

@@ -61,33 +61,34 @@ class DiagPlusLowRank:
         self.Ut = u.t().contiguous()  # (r, N) device
         self.d = None
         self._dmin = None
-        dmin = None  # device min(d): positivity test and omega (D-6), read with the gram
         if d is not None:
             dt = to_dev(d, dtype, device)
             if dt.numel() != self._n and self._n:
                 raise ValueError("d must have one entry per voxel")
             self.d = dt
-            dmin = dt.min().reshape(1).to(torch.float64) if dt.numel() else None
         self.gram = None
-        if self.rank:
-            self.gram = torch.empty(self.rank * self.rank, dtype=torch.float64, device=device)
+        # min(d) (positivity test, omega D-6) and the gram in ONE small-footprint
+        # pass and ONE device->host read (bq_metric_check: it fits beside a running
+        # prox, so building the next problem overlaps the current solve)
+        host = np.zeros(0)
+        nck = self._n if self._n else (self.d.numel() if self.d is not None else 0)
+        if self.rank or (self.d is not None and nck):
+            chk = torch.empty(1 + self.rank * self.rank, dtype=torch.float64, device=device)
             lib = _abi.load_library()
             _abi.check(
-                lib.bq_metric_gram(
-                    _abi.ctx_for(device), _abi.dtype_code(dtype), self._n, self.rank,
-                    self.tau if self.d is None else 0.0, _abi.ptr(self.d), self.Ut.data_ptr(),
-                    self.gram.data_ptr(), _abi.stream_ptr(device),
-                ),
+                lib.bq_metric_check(_abi.ctx_for(device), _abi.dtype_code(dtype), nck, self.rank, _abi.ptr(self.d),
+                                    self.Ut.data_ptr() if self.rank else None, chk.data_ptr(),
+                                    _abi.stream_ptr(device)),
                 "DiagPlusLowRank",
             )
-        # one device->host read for the d test, min(d) and the gram
-        parts = [t for t in (dmin, self.gram) if t is not None]
-        host = torch.cat(parts).cpu().numpy() if parts else np.zeros(0)
-        if dmin is not None:
+            if self.rank:
+                self.gram = chk[1:]
+            host = chk.cpu().numpy()
+        if self.d is not None and host.size:
             self._dmin = float(host[0])
             if not self._dmin > 0:  # (NaN fails too, like (d > 0).all())
                 raise ValueError("diagonal d must be positive")
-            host = host[1:]
+        host = host[1:]
         self._gram_host = None
         if self.rank:
             g = host.reshape(self.rank, self.rank)

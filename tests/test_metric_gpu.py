@@ -111,3 +111,25 @@ def test_compute_v_k_rejects_per_voxel_diagonal():
     w = DiagPlusLowRank(1.0, rng.standard_normal((n, 1)) / 8, d=rng.uniform(0.5, 2, n))
     with pytest.raises(ValueError):
         M.compute_v_k(slots, w, 1.0)
+
+
+def test_metric_check_min_and_gram_and_nan():
+    """bq_metric_check (DiagPlusLowRank's one-pass validation): min(d), the gram,
+    and a NaN in d rejected like the reference's (d > 0).all()."""
+    from paper_2307_02043_b200.wpm import DiagPlusLowRank
+
+    rng = np.random.default_rng(8)
+    n = 100_003
+    d = rng.uniform(0.5, 2.0, n)
+    U = rng.standard_normal((n, 3)) / np.sqrt(n)
+    w = DiagPlusLowRank(1.0, U, d=d)
+    assert w.min_diag() == d.min()
+    np.testing.assert_allclose(w.gram.reshape(3, 3).cpu().numpy(), U.T @ (U / d[:, None]), rtol=1e-12)
+    w2 = DiagPlusLowRank(1.7, U)
+    np.testing.assert_allclose(w2.gram.reshape(3, 3).cpu().numpy(), U.T @ U, rtol=1e-12)
+    d[77] = np.nan
+    with pytest.raises(ValueError):
+        DiagPlusLowRank(1.0, U, d=d)
+    d[77] = -1.0
+    with pytest.raises(ValueError):
+        DiagPlusLowRank(1.0, U, d=d)
