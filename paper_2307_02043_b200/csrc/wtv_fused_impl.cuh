@@ -1301,21 +1301,37 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
     if (phase == F_SETUP) {
       // gram partials U^T D^-1 U (wpm.py:50-56); 1/d staged by the fused pass
       nv = V::S;
+      // 4 voxels per thread and trip (16-byte accesses; N % 4 == 0 on this path)
       if (R == 0 && A.d)
-        for (long long j = gtid; j < N; j += stride) A.ie[j] = rcp(__ldg(A.d + j));
+        for (long long j = 4 * gtid; j < N; j += 4 * stride) {
+          T e[4], ie[4];
+          Vec4<T>::ro(A.d + j, e);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) ie[q] = rcp(e[q]);
+          Vec4<T>::st(A.ie + j, ie);
+        }
       if (R > 0) {
-        for (long long j = gtid; j < N; j += stride) {
-          T u[R > 0 ? R : 1];
+#pragma unroll 2
+        for (long long j = 4 * gtid; j < N; j += 4 * stride) {
+          T u[R > 0 ? R : 1][4], e[4] = {(T)1, (T)1, (T)1, (T)1};
 #pragma unroll
-          for (int c = 0; c < R; ++c) u[c] = __ldg(A.U + (long long)c * N + j);
-          const T e = A.d ? __ldg(A.d + j) : (T)1;
-          if (A.d) A.ie[j] = rcp(e);
-          int k = 0;
+          for (int c = 0; c < R; ++c) Vec4<T>::ro(A.U + (long long)c * N + j, u[c]);
+          if (A.d) {
+            T ie[4];
+            Vec4<T>::ro(A.d + j, e);
 #pragma unroll
-          for (int c = 0; c < R; ++c)
+            for (int q = 0; q < 4; ++q) ie[q] = rcp(e[q]);
+            Vec4<T>::st(A.ie + j, ie);
+          }
 #pragma unroll
-            for (int c2 = 0; c2 <= c; ++c2, ++k)
-              acc[k] += A.d ? (double)(u[c] * u[c2] / e) : (double)u[c] * (double)u[c2];
+          for (int q = 0; q < 4; ++q) {
+            int k = 0;
+#pragma unroll
+            for (int c = 0; c < R; ++c)
+#pragma unroll
+              for (int c2 = 0; c2 <= c; ++c2, ++k)
+                acc[k] += A.d ? (double)(u[c][q] * u[c2][q] / e[q]) : (double)u[c][q] * (double)u[c2][q];
+          }
         }
       }
     } else if (phase == F_FUSED) {
@@ -1563,24 +1579,33 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       // full-pass phi(beta) and generalized Jacobian partials (wpm.py:150-167)
       nv = V::NEWTON;
       const T* __restrict__ Ain = A.abuf[sh.a_cur];
-      for (long long j = gtid; j < N; j += stride) {
-        T av, s[R > 0 ? R : 1], u[R > 0 ? R : 1], l, h;
-        F.voxel(Ain, j, av, s, u, l, h);
-        T wv = av, z = av;
+      // scalar bounds on this path; 4 voxels per thread and trip
+      const T l = F.lo, h = F.hi;
+#pragma unroll 2
+      for (long long j = 4 * gtid; j < N; j += 4 * stride) {
+        T a4[4], ie[4], u[R > 0 ? R : 1][4];
+        Vec4<T>::rw(Ain + j, a4);
+        F.ieu4(j, ie, u);
 #pragma unroll
-        for (int c = 0; c < R; ++c) {
-          wv += s[c] * sh.gw[c];
-          z += s[c] * sh.gz[c];
-        }
-        const T dl = wv - clampv(z, l, h);
+        for (int q = 0; q < 4; ++q) {
+          T s[R > 0 ? R : 1];
+          T wv = a4[q], z = a4[q];
 #pragma unroll
-        for (int c = 0; c < R; ++c) acc[c] += (double)u[c] * (double)dl;
-        if (z > l && z < h) {
-          int k = R;
+          for (int c = 0; c < R; ++c) {
+            s[c] = F.sg * u[c][q] * ie[q];
+            wv += s[c] * sh.gw[c];
+            z += s[c] * sh.gz[c];
+          }
+          const T dl = wv - clampv(z, l, h);
 #pragma unroll
-          for (int c = 0; c < R; ++c)
+          for (int c = 0; c < R; ++c) acc[c] += (double)u[c][q] * (double)dl;
+          if (z > l && z < h) {
+            int k = R;
 #pragma unroll
-            for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += (double)u[c] * (double)s[c2];
+            for (int c = 0; c < R; ++c)
+#pragma unroll
+              for (int c2 = 0; c2 <= c; ++c2, ++k) acc[k] += (double)u[c][q] * (double)s[c2];
+          }
         }
       }
     } else if (phase == F_FINAL) {
@@ -1589,15 +1614,26 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       T* __restrict__ X = A.x;
       const T* __restrict__ Pfin = A.ring[sh.slot_cur];
       const bool copy = !sh.single && sh.slot_cur != 0;
-      for (long long j = gtid; j < N; j += stride) {
-        T av, s[R > 0 ? R : 1], u[R > 0 ? R : 1], l, h;
-        F.voxel(Ain, j, av, s, u, l, h);
-        T z = av;
+      const T l = F.lo, h = F.hi;  // scalar bounds on this path
+#pragma unroll 2
+      for (long long j = 4 * gtid; j < N; j += 4 * stride) {
+        T a4[4], ie[4], u[R > 0 ? R : 1][4];
+        Vec4<T>::rw(Ain + j, a4);
+        F.ieu4(j, ie, u);
 #pragma unroll
-        for (int c = 0; c < R; ++c) z += s[c] * sh.gz[c];
-        X[j] = clampv(z, l, h);
+        for (int q = 0; q < 4; ++q) {
+          T z = a4[q];
+#pragma unroll
+          for (int c = 0; c < R; ++c) z += (F.sg * u[c][q] * ie[q]) * sh.gz[c];
+          a4[q] = clampv(z, l, h);
+        }
+        Vec4<T>::st(X + j, a4);
         if (copy)
-          for (int n = 0; n < nd; ++n) A.ring[0][n * N + j] = Pfin[n * N + j];
+          for (int n = 0; n < nd; ++n) {
+            T p4[4];
+            Vec4<T>::rw(Pfin + n * N + j, p4);
+            Vec4<T>::st(A.ring[0] + n * N + j, p4);
+          }
       }
     }
 
