@@ -23,8 +23,8 @@ w = DiagPlusLowRank(1.0, torch.tensor(inp["u"][:, None], dtype=torch.float32, de
 prob = D.DualTvProblem(grid=bq.Grid((128, 128, 128)), v=v, w=w, reg=0.05)
 ws = D.ProxWorkspace(prob.grid, torch.float32, dev)
 ctx = _abi.ctx_for(dev)
-raw = ctypes.cast(ctx, ctypes.POINTER(ctypes.c_uint64))
-scratch = raw[5]
+from _trace_util import trace_scratch  # noqa: E402
+scratch = trace_scratch(ctx, lambda: D.solve_async(prob, ws, eps=1e-300, max_iter=3))
 cudart = ctypes.CDLL("/usr/local/cuda/lib64/libcudart.so")
 names = ["pass end", "partials out", "barrier done", "reduced", "controller", "newton", "next set up", "1st stage"]
 for it in [int(a) for a in sys.argv[1:]] or [30, 60, 90]:

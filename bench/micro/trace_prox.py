@@ -31,8 +31,8 @@ buf = np.zeros(240, dtype=np.uint64)
 cudart = ctypes.CDLL("/usr/local/cuda/lib64/libcudart.so")
 ptr = ctypes.c_void_p()
 # ws.scratch is the first pointer after partials/barrier/ctl/ctl_bytes in bq_ctx::ws
-raw = ctypes.cast(ctx, ctypes.POINTER(ctypes.c_uint64))
-scratch = raw[5]  # [device|num_sms], partials, barrier, ctl, ctl_bytes, scratch
+from _trace_util import trace_scratch  # noqa: E402
+scratch = trace_scratch(ctx, lambda: D.solve_async(prob, ws, eps=1e-300, max_iter=3))
 t = torch.empty(240, dtype=torch.int64, device=dev)
 cudart.cudaMemcpy(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(scratch), ctypes.c_size_t(240 * 8), 3)
 torch.cuda.synchronize()
