@@ -101,6 +101,7 @@ struct FCtl {
   int phase_cnt[8];
 };
 
+constexpr int kMaxTileTab = 96; // row tiles the per-tile block assignment can describe
 constexpr int NSTAGE = 3;      // max depth of the bulk-copy pipeline (3 where the stages fit, else 2)
 
 // per-slot use counters of the stage ring, kept in registers (runtime slot
@@ -160,6 +161,13 @@ struct FArgs {
   int cluster;                // 1: the whole grid is ONE thread-block cluster (small grids): the
                               // inter-pass barrier is a cluster barrier and the partials are
                               // exchanged through distributed shared memory
+  // Staged FUSED pass, per-tile block assignment: blocks [tile_blk0[t], tile_blk0[t+1])
+  // split the K3 planes of row tile t evenly, so no block's z-segment crosses a
+  // tile (a crossing costs a second pre-step + warm-up plane, and those blocks
+  // were the last to arrive at every barrier).  ntile_tab == 0: one contiguous
+  // split of the tile-plane sequence over the grid.
+  int ntile_tab;
+  short tile_blk0[kMaxTileTab + 1];
 };
 
 // tau and the dual step of this launch: host values, or from the device
@@ -1265,8 +1273,15 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   constexpr int wpr = KX > 128 ? 2 : 1;  // warps per x-row
   const int GWs = A.geo.W / wpr;
   const long long tp_s = (long long)((A.K2 + (GWs - 1) * A.rpw - 1) / ((GWs - 1) * A.rpw)) * A.K3;
-  const long long seg_begin_s = (long long)blockIdx.x * tp_s / gridDim.x;
-  const long long seg_end_s = (long long)(blockIdx.x + 1) * tp_s / gridDim.x;
+  long long seg_begin_s = (long long)blockIdx.x * tp_s / gridDim.x;
+  long long seg_end_s = (long long)(blockIdx.x + 1) * tp_s / gridDim.x;
+  if (A.ntile_tab > 0) {
+    int t = 0;
+    while (t + 1 < A.ntile_tab && (int)blockIdx.x >= A.tile_blk0[t + 1]) ++t;
+    const int kb = (int)blockIdx.x - A.tile_blk0[t], nb = A.tile_blk0[t + 1] - A.tile_blk0[t];
+    seg_begin_s = (long long)t * A.K3 + (long long)A.K3 * kb / nb;
+    seg_end_s = (long long)t * A.K3 + (long long)A.K3 * (kb + 1) / nb;
+  }
   const Fields<T, R> F{A.d, A.U, A.lo_arr, A.hi_arr, N, (T)eff_tau(A), (T)A.lo, (T)A.hi, (T)A.sign};
   const int lpr = A.lpr, rpw = A.rpw;
   // standalone DIV pass: NG row groups of wpr warps, the last group is the halo
@@ -1813,7 +1828,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       T* ne = reinterpret_cast<T*>(s_dyn + A.list_off);
       const int total = (int)s_red[V::NCNT];
       const long long lbytes = (long long)total * EW * (long long)sizeof(T);
-      const bool seg_ok = (int)gridDim.x * NW <= 8 * NC;
+      const bool seg_ok = (int)gridDim.x * NW <= 8 * NC && (int)gridDim.x * NW < (int)(sizeof(s_scr) / sizeof(int));
       bool in_smem = seg_ok && lbytes <= A.list_bytes;
       if (seg_ok && !in_smem && lbytes <= A.dyn_bytes) {
         // long list (early iterations): give up the prefetched stages, use all the dynamic smem
@@ -1837,9 +1852,13 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       // scan), then a flat gather: thread t copies entries t, t+NT, ... (each
       // located by binary search), so no thread walks a long segment serially.
       // The list order is fixed, so every block sums identically.
-      __shared__ int s_pref[8 * NT + 1];
+      // (the prefix table lives in the block-reduction scratch: s_scr is idle
+      //  between barriers, and the long-list reduction below reads the
+      //  gathered copy, not the table)
+      int* const s_pref = reinterpret_cast<int*>(s_scr);
+      constexpr int kPrefCap = (int)(sizeof(s_scr) / sizeof(int)) - 1;
       const int nseg = gridDim.x * NW;
-      const bool indexed = nseg <= 8 * NC;
+      const bool indexed = nseg <= 8 * NC && nseg <= kPrefCap;
       const int lpar = (npass - 1) & 1;  // parity of the pass that built the lists
       const T* __restrict__ nd = reinterpret_cast<const T*>(A.near_data) + lpar * seg_elems;
       const int* __restrict__ ncnt_l = A.near_cnt + lpar * nseg;
@@ -1891,7 +1910,9 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
           csync();
         }
       }
-      const bool big = total > 256;  // long lists: every warp evaluates, block reduction per step
+      // long lists: every warp evaluates, block reduction per step (through
+      // s_scr, so only when the evaluation reads the gathered copy, not s_pref)
+      const bool big = total > 256 && in_smem;
       if (warp == 0 || big) {
         if (!big) __syncwarp();
         if (ntr) A.trace[240 + ntr_k++] = global_ns();
@@ -2110,7 +2131,8 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
     BQ_CUDA(cudaFuncGetAttributes(&fa, (const void*)kern));
     static_b = (int)fa.sharedSizeBytes;
   }
-  const size_t smem_cap = std::min<size_t>(200 * 1024, (size_t)std::max(0, optin - static_b - 3072));
+  const size_t cap_kb = getenv("BQ_PROX_SMEMCAP_KB") ? (size_t)atoi(getenv("BQ_PROX_SMEMCAP_KB")) : 212;
+  const size_t smem_cap = std::min<size_t>(cap_kb * 1024, (size_t)std::max(0, optin - static_b - 3072));
   int W = NT / 32 - 1;  // + 1 producer warp
   W -= W % A.wpr;       // whole row groups
   const char* ns_env = getenv("BQ_PROX_STAGES");
@@ -2204,6 +2226,41 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
       } else {
         (void)cudaGetLastError();  // not schedulable as one cluster: the cooperative launch
       }
+    }
+  }
+  // per-tile block assignment of the staged pass (see FArgs::tile_blk0): greedy,
+  // one more block to the tile whose blocks would otherwise finish last.  A
+  // step's cost grows with the tile's real rows (the last tile may be partial).
+  A.ntile_tab = 0;
+  {
+    const int GW = W / A.wpr, TYs = (GW - 1) * A.rpw;
+    const int ntile = (A.K2 + TYs - 1) / TYs;
+    const char* te = getenv("BQ_PROX_TILEBLK");
+    if ((!te || atoi(te) != 0) && !A.cluster && ntile <= kMaxTileTab && G >= ntile && G < 32768) {
+      const double alpha = getenv("BQ_PROX_TILEALPHA") ? atof(getenv("BQ_PROX_TILEALPHA")) : 0.8;
+      int nb[kMaxTileTab];
+      auto cost = [&](int t) {
+        const int rows = std::min(TYs, A.K2 - t * TYs);
+        const int planes = (A.K3 + nb[t] - 1) / nb[t];
+        return (planes + (nb[t] > 1 ? 2 : 0)) * (alpha + (1.0 - alpha) * rows / TYs);
+      };
+      for (int t = 0; t < ntile; ++t) nb[t] = 1;
+      for (long long left = G - ntile; left > 0; --left) {
+        int best = -1;
+        double bc = 0.0;
+        for (int t = 0; t < ntile; ++t)
+          if (nb[t] < A.K3 && cost(t) > bc) bc = cost(t), best = t;
+        if (best < 0) break;
+        nb[best] += 1;
+      }
+      int acc = 0;
+      double worst = 0.0;
+      for (int t = 0; t < ntile; ++t) A.tile_blk0[t] = (short)acc, acc += nb[t], worst = std::max(worst, cost(t));
+      A.tile_blk0[ntile] = (short)acc;
+      // the contiguous split's slowest blocks cross a tile: ceil(planes) + 2 x (pre-step + warm-up);
+      // few blocks per tile (large grids) split unevenly by tile and stay contiguous
+      const double contiguous = (double)((long long)ntile * A.K3 + G - 1) / G + 4.0;
+      if (acc == G && (worst < contiguous - 0.5 || (te && atoi(te) == 2))) A.ntile_tab = ntile;
     }
   }
   // near-list workspace
