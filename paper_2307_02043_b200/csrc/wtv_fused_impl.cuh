@@ -87,7 +87,7 @@ struct FCtl {
   int converged, status, last_newton_it, last_newton_conv;
   int final_mode, div_p, have_hist, fallbacks;
   int slot_cur, slot_prev, a_cur, local_steps;
-  int single, nl_ok, ndist, pad1;  // ndist: long near list -> distributed Newton steps
+  int single, nl_ok, ndist, cl_on;  // ndist: long near list -> distributed Newton steps; cl_on: see compact_near
   double t, t_next, m_prev, m_cur, rel, best_res, last_res, grow;
   double beta[BQ_MAX_RANK], best_beta[BQ_MAX_RANK], gw[BQ_MAX_RANK];
   double gc[BQ_MAX_RANK], gwid[BQ_MAX_RANK], glast[BQ_MAX_RANK], dmax[BQ_MAX_RANK];
@@ -168,6 +168,9 @@ struct FArgs {
   // split of the tile-plane sequence over the grid.
   int ntile_tab;
   short tile_blk0[kMaxTileTab + 1];
+  T* cl_data;        // [2][CL][EW] compact near list by pass parity (compact_near), or null
+  unsigned* cl_key;  // [2][CL]
+  unsigned* cl_ctr;  // monotonic slot counter (zeroed at launch)
 };
 
 // tau and the dual step of this launch: host values, or from the device
@@ -193,6 +196,7 @@ struct FShared {
   T m_prev, m_cur;
   int phase, slot_cur, slot_prev, slot_new, a_cur, div_p, single, iter;
   int tr7;  // trace builds: stamp the first stage of this pass
+  int cl_on;  // the pass also fills the grid-wide compact near list (compact_near)
 };
 
 // ---------------------------------------------------------------------------
@@ -402,6 +406,34 @@ __device__ __forceinline__ void near_push(bool flag, T av, T l, T h, const T (&u
   cnt += n;
 }
 
+// Grid-wide compact copy of SHORT near lists (steady state: 0-3 entries in
+// the whole grid).  After a pass, a warp that listed voxels reserves slots in
+// one small global array with an atomic on a monotonic counter (slot = old -
+// base, base = the counter after the previous pass, the same in every block)
+// and copies its entries there, each with its position in segment order as
+// key.  After the barrier every block already holds those CL slots (loaded
+// with the partials, no further round trip: no count scan, no gather) and
+// sorts them by key, so the evaluation order is the segment order whatever
+// order the atomics ran in.  Done outside the march loop (inlined into it, the
+// reservation cost the loop 0.05 ms per 128^3 solve).
+constexpr int CL = 32;
+template <typename T, int EW>
+__device__ __forceinline__ void compact_near(const T* seg, int cnt, unsigned key0, unsigned* ctr, unsigned base,
+                                             T* data, unsigned* key, int lane) {
+  __syncwarp();  // the segment was written lane by lane
+  unsigned slot0 = 0;
+  if (lane == 0) slot0 = atomicAdd(ctr, (unsigned)cnt) - base;
+  slot0 = __shfl_sync(FULLM, slot0, 0);
+  for (int e = lane; e < cnt; e += 32) {
+    const unsigned slot = slot0 + (unsigned)e;
+    if (slot < (unsigned)CL) {
+#pragma unroll
+      for (int f = 0; f < EW; ++f) data[(long long)slot * EW + f] = __ldcg(seg + (long long)e * EW + f);
+      key[slot] = key0 + (unsigned)e;
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // controller (thread 0 of every block, on the block's own shared state)
 // ---------------------------------------------------------------------------
@@ -525,6 +557,7 @@ struct Ctl {
     for (int k = 0; k < V::S; ++k) c.Cin[k] = red[V::CIN + k], c.Cout[k] = A.sign * gsc(c.gram[k]) - c.Cin[k];
     c.nl_ok = red[V::OVF] == 0.0;
     c.ndist = red[V::NCNT] > A.ndist_min ? 1 : 0;
+    c.cl_on = (!A.cluster && A.cl_data && red[V::NCNT] <= 2.0 * CL) ? 1 : 0;  // lists shrink slowly: worth filling
     c.fallbacks = 0;
     c.newton_it = 0;
     c.best_res = INFINITY;
@@ -602,6 +635,7 @@ struct Ctl {
         c.a_cur = 1;    // the DIV pass writes abuf[1 - a_cur] = abuf[0]
         c.m_prev = 0.0; // P_bar_0 = P_0
         c.div_p = 1;    // DIV source: P_0 (== P_bar_0)
+        c.cl_on = 0;
         c.phase = F_DIV;
         return;
       }
@@ -1301,6 +1335,10 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
   T* my_seg0 = reinterpret_cast<T*>(A.near_data) + ((long long)blockIdx.x * NW + warp) * capw * EWN;
   int npass = 0;  // DIV/FUSED passes so far (same in every block)
   int my_cnt = 0;  // this warp's near entries in the last pass
+  // compact near list (compact_near): [0] slot counter after the last pass (base of the
+  // next pass's reservations), [1] slots the last pass reserved
+  __shared__ unsigned s_nbase[2];
+  if (threadIdx.x == 0) s_nbase[0] = 0u, s_nbase[1] = 0u;  // (ordered by the first block barrier below)
 
   int phase = F_SETUP;
 #if BQ_PROX_TRACE
@@ -1311,6 +1349,10 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
 #pragma unroll
     for (int k = 0; k < NACC; ++k) acc[k] = 0.0;
     int nv = 0;
+    T cl_ent[EWN];  // warp 0: slot `lane` of the compact list of the pass ending at this barrier
+    unsigned cl_key = 0xffffffffu;
+#pragma unroll
+    for (int f = 0; f < EWN; ++f) cl_ent[f] = (T)0;
 
     if (s_pre[0] > 0 && (phase == F_DIV || phase == F_FINAL)) drain();  // these reuse / leave the smem
     if (phase == F_SETUP) {
@@ -1369,6 +1411,9 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       // bounds are pass constants
       fused_staged<T, R, NACC, 1, KX>(A, sh, A.geo, seg_begin_s, seg_end_s, reinterpret_cast<T*>(s_dyn), s_full,
                                       s_empty, uses, acc, my_seg, ncnt, ovf, pre);
+      if (sh.cl_on && ncnt > 0 && !ovf)  // (warp-uniform)
+        compact_near<T, EWN>(my_seg, ncnt, (unsigned)((blockIdx.x * NW + warp) * capw), A.cl_ctr, s_nbase[0],
+                             A.cl_data + (long long)(npass & 1) * CL * EWN, A.cl_key + (npass & 1) * CL, lane);
       if (lane == 0) A.near_cnt[(npass & 1) * gridDim.x * NW + blockIdx.x * NW + warp] = ncnt;
       ++npass;
       my_cnt = ncnt;
@@ -1735,6 +1780,22 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         if (blockIdx.x == 0 && threadIdx.x == 0) A.report->status = BQ_ETIMEOUT;
         break;
       }
+      if (cur == F_FUSED && A.cl_data && warp == 0) {
+        // compact near list of the pass that just ended: the counter and the CL
+        // slots ride along with the partial loads below (same L2 round trip)
+        const int par = (npass - 1) & 1;
+        if (lane == 0) {
+          const unsigned now = __ldcg(A.cl_ctr);
+          s_nbase[1] = now - s_nbase[0];
+          s_nbase[0] = now;
+        }
+        if (lane < CL) {
+          cl_key = __ldcg(A.cl_key + par * CL + lane);
+          const T* src = A.cl_data + ((long long)par * CL + lane) * EWN;
+#pragma unroll
+          for (int f = 0; f < EWN; ++f) cl_ent[f] = __ldcg(src + f);
+        }
+      }
       if (cur == F_FUSED && threadIdx.x == 0) {
         // the next FUSED pass (the usual successor) reads ring[slot_new],
         // ring[slot_cur] and abuf[a_cur ^ 1]; its first stages are issued by
@@ -1830,6 +1891,11 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       const long long lbytes = (long long)total * EW * (long long)sizeof(T);
       const bool seg_ok = (int)gridDim.x * NW <= 8 * NC && (int)gridDim.x * NW < (int)(sizeof(s_scr) / sizeof(int));
       bool in_smem = seg_ok && lbytes <= A.list_bytes;
+      // short list, filled grid-wide by the last pass and already in warp 0's
+      // registers: no count scan, no gather
+      const bool tiny = cur == F_FUSED && sh.cl_on && total > 0 && total <= CL && s_nbase[1] == (unsigned)total &&
+                        (long long)CL * EW * (long long)sizeof(T) <= A.list_bytes;
+      if (tiny) in_smem = true;
       if (seg_ok && !in_smem && lbytes <= A.dyn_bytes) {
         // long list (early iterations): give up the prefetched stages, use all the dynamic smem
         if (s_pre[0] > 0) drain_impl(true);
@@ -1871,7 +1937,19 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         }
         return nd + ((long long)lo * capw + (e - s_pref[lo])) * EW;
       };
-      if (total > 0 && indexed) {
+      if (tiny && warp == 0) {
+        // canonical order: segment order (rank = number of smaller keys)
+        const unsigned mykey = lane < total ? cl_key : 0xffffffffu;
+        int rank = 0;
+        for (int i = 0; i < total; ++i) rank += __shfl_sync(FULLM, mykey, i) < mykey ? 1 : 0;
+        if (lane < total) {
+          T* dst = ne + (long long)rank * EW;
+#pragma unroll
+          for (int f = 0; f < EW; ++f) dst[f] = cl_ent[f];
+        }
+        __syncwarp();
+      }
+      if (total > 0 && indexed && !tiny) {
         constexpr int SPT = 8;
         const int s0 = cidx * SPT;
         int cnt[SPT];
@@ -2028,6 +2106,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       sh.iter = s_c.it;
       sh.div_p = s_c.div_p;
       sh.single = s_c.single;
+      sh.cl_on = s_c.cl_on;
       sh.m_prev = (T)s_c.m_prev;
       sh.m_cur = (T)s_c.m_cur;
 #if BQ_PROX_TRACE
@@ -2273,7 +2352,9 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
     A.capw = cap;
   }
   const size_t data_bytes = 2 * (size_t)G * (NT / 32) * A.capw * EWN * sizeof(T);
-  const size_t need = data_bytes + 2 * (size_t)G * (NT / 32) * sizeof(int);
+  const size_t cnt_bytes = (2 * (size_t)G * (NT / 32) * sizeof(int) + 15) / 16 * 16;
+  const size_t cl_bytes = 2 * (size_t)CL * EWN * sizeof(T);
+  const size_t need = data_bytes + cnt_bytes + cl_bytes + 2 * CL * sizeof(unsigned);
   if (sw->near_bytes < need) {
     cudaFree(sw->near_buf);
     sw->near_buf = nullptr;
@@ -2283,6 +2364,10 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   }
   A.near_data = sw->near_buf;
   A.near_cnt = (int*)((char*)sw->near_buf + data_bytes);
+  const bool cl_use = !getenv("BQ_PROX_NOCL") || atoi(getenv("BQ_PROX_NOCL")) == 0;
+  A.cl_data = cl_use ? (T*)((char*)sw->near_buf + data_bytes + cnt_bytes) : nullptr;
+  A.cl_key = (unsigned*)((char*)sw->near_buf + data_bytes + cnt_bytes + cl_bytes);
+  A.cl_ctr = sw->ws.barrier + 12;  // (+4: helper reductions, +8: bq_metric_check)
 
   A.dyn_bytes = (long long)dyn;
   A.list_off = (long long)base_dyn;
@@ -2294,6 +2379,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   A.grow_min = getenv("BQ_PROX_GROW") ? atof(getenv("BQ_PROX_GROW")) : 8.0;
   A.ndist_min = getenv("BQ_PROX_NDIST") ? atof(getenv("BQ_PROX_NDIST")) : 1024.0;
   BQ_CUDA(cudaMemsetAsync(sw->ws.barrier, 0, 2 * sizeof(unsigned), st));
+  BQ_CUDA(cudaMemsetAsync(sw->ws.barrier + 12, 0, sizeof(unsigned), st));
   if (A.cluster) {
     BQ_CUDA(cudaLaunchKernelEx(&ccfg, kern, A));
     return BQ_OK;
