@@ -72,8 +72,9 @@ struct FV {
   static constexpr int RHS = 0;
   static constexpr int K0 = R;
   static constexpr int CIN = 2 * R;
-  static constexpr int COUT = 2 * R + S;
-  static constexpr int NRM = 2 * R + 2 * S;
+  static constexpr int COUT = 2 * R + S;  // end of the accumulated classes (Cout itself is never reduced:
+                                          // the controller forms it from the setup gram and Cin)
+  static constexpr int NRM = COUT;
   static constexpr int OVF = NRM + 2;
   static constexpr int NCNT = OVF + 1;  // near-list entries (block total / grid total)
   static constexpr int PASS = NCNT + 1;
@@ -1167,8 +1168,10 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
             any |= nrv[2 * p] | nrv[2 * p + 1];
           }
         };
+#ifndef BQ_EXP_NOAGG  // (timing experiment: skip the Newton aggregates)
         if (hinf) classify(std::true_type{});
         else classify(std::false_type{});
+#endif
       }
       if (__any_sync(FULLM, any)) {  // near voxels are rare: one vote per step
 #pragma unroll
