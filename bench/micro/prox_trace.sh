@@ -5,3 +5,4 @@ BQ_PROX_TRACE=50 BQ_PROX_TRACE_THREAD=-2 python bench/micro/trace_newton.py 2>&1
 BQ_PROX_TRACE=50 BQ_PROX_TRACE_THREAD=-1 python bench/micro/trace_newton.py 2>&1 | tail -3
 BQ_PROX_TRACE_THREAD=-3 python bench/micro/trace_interpass.py 30 31 60 61 90 2>&1 | tail -16
 BQ_PROX_TRACE_THREAD=-3 python bench/micro/trace_arrivals.py 2>&1 | tail -40
+BQ_PROX_TRACE_THREAD=-3 python bench/micro/trace_smid.py > gpurun_out/smid.log 2>&1

@@ -1427,6 +1427,13 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
       if (tr3_on && blockIdx.x == 0 && threadIdx.x == 0) A.trace[320 + 8] = s_c.it;
 #endif
       TR3(0);
+#if BQ_PROX_TRACE
+      if (tr3_on && threadIdx.x == 0 && blockIdx.x < 1000) {  // which SM ran this block
+        unsigned smid;
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+        A.trace[3072 + blockIdx.x] = smid;
+      }
+#endif
     } else if (phase == F_DIV) {
       nv = V::PASS;
       const bool fused = false;
@@ -1829,7 +1836,7 @@ __global__ void __launch_bounds__(FCfg<T, R>::NT, 1) wtv_fused_kernel(FArgs<T> A
         for (unsigned b = lane; b < gridDim.x; b += 32) {
           t = max(t, __ldcg(&col[b]));
 #if BQ_PROX_TRACE
-          if (cur == F_FUSED && tr3_on && b < 2048) A.trace[1024 + b] = (unsigned long long)__ldcg(&col[b]);
+          if (cur == F_FUSED && tr3_on && b < 2000) A.trace[1024 + b] = (unsigned long long)__ldcg(&col[b]);
 #endif
         }
 #pragma unroll
