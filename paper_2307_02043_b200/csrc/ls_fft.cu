@@ -373,6 +373,9 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n_rt, const typename CV<T>
 #ifndef LS_ZC_MINB
 #define LS_ZC_MINB 3  // ZC at m <= 256: minimum resident blocks per SM requested from ptxas (register cap; 2 at m = 512)
 #endif
+#ifndef LS_ZC_RPF
+#define LS_ZC_RPF 1  // ZC at m <= 256: register prefetch of the next view's column (A/B hook)
+#endif
 #ifndef LS_ZC_VG
 #define LS_ZC_VG 1  // ZC view groups per column group (grid.y); measured: 2 and 4 are no faster at m = 256 / 512
 #endif
@@ -422,9 +425,12 @@ __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_ke
   };
   bool first = true;
   constexpr int ZS = M * M;  // plane stride (32-bit offsets within one view's Q)
-  for (int b = next_active(b_lo); b < B; b = next_active(b + 1)) {
-    V* col = q + (long long)b * vstride + (long long)y * M + x;
-    V a[R1 / C][R2];
+  // RPF: the next active view's column is loaded into the registers of `a` as
+  // soon as step 1 has consumed them, so its DRAM latency runs under this
+  // view's transforms (volume-to-volume case, one line segment per thread)
+  constexpr bool RPF = LS_ZC_RPF && STD && M <= 256;
+  V a[R1 / C][R2];
+  auto load_col = [&](const V* col) {
 #pragma unroll
     for (int s = 0; s < R1 / C; ++s)
 #pragma unroll
@@ -433,16 +439,22 @@ __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_ke
         if (STD) a[s][n2] = n2 < R2 / 2 ? col[e * ZS] : czero<V>();
         else a[s][n2] = (e >= z0 && e < z0 + nzi) ? col[(e - z0) * zs] : czero<V>();
       }
-    {  // the next active view's column into L2 while this one computes
-      const int bn = next_active(b + 1);
-      if (M >= LS_ZC_PF && bn < B) {
-        const V* nc = q + (long long)bn * vstride + (long long)y * M + x;
-        for (int e = t; e < nzi; e += C) prefetch_l2(nc + e * zs);
-      }
+  };
+  int b = next_active(b_lo);
+  if (RPF && b < B) load_col(q + (long long)b * vstride + (long long)y * M + x);
+  for (; b < B;) {
+    V* col = q + (long long)b * vstride + (long long)y * M + x;
+    const int bn = next_active(b + 1);
+    if (!RPF) load_col(col);
+    // the next active view's column into L2 while this one computes
+    if (M >= LS_ZC_PF && bn < B) {
+      const V* nc = q + (long long)bn * vstride + (long long)y * M + x;
+      for (int e = t; e < nzi; e += C) prefetch_l2(nc + e * zs);
     }
     if (first) cp_async_wait_all();
     __syncthreads();  // twiddles + K_hat staged (first view); previous view's reads of sm done
     step1<R1, R2, C, L, true, -1, STD>(a, sm, tw, l, t);
+    if (RPF && bn < B) load_col(q + (long long)bn * vstride + (long long)y * M + x);
     __syncthreads();
     V c[R2 / C][R1];
     step3<R1, R2, C, L, true, -1>(c, sm, l, t);
@@ -485,6 +497,7 @@ __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_ke
         }
       }
     first = false;
+    b = bn;
   }
   if (first) cp_async_wait_all();  // no active view: retire the staging copies
 }
