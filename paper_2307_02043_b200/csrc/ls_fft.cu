@@ -376,6 +376,9 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n_rt, const typename CV<T>
 #ifndef LS_ZC_RPF
 #define LS_ZC_RPF 1  // ZC at m <= 256: register prefetch of the next view's column (A/B hook)
 #endif
+#ifndef LS_ZC_RPF_MAXM
+#define LS_ZC_RPF_MAXM 256
+#endif
 #ifndef LS_ZC_VG
 #define LS_ZC_VG 1  // ZC view groups per column group (grid.y); measured: 2 and 4 are no faster at m = 256 / 512
 #endif
@@ -428,7 +431,7 @@ __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_ke
   // RPF: the next active view's column is loaded into the registers of `a` as
   // soon as step 1 has consumed them, so its DRAM latency runs under this
   // view's transforms (volume-to-volume case, one line segment per thread)
-  constexpr bool RPF = LS_ZC_RPF && STD && M <= 256;
+  constexpr bool RPF = LS_ZC_RPF && STD && M <= LS_ZC_RPF_MAXM;
   V a[R1 / C][R2];
   auto load_col = [&](const V* col) {
 #pragma unroll
