@@ -36,7 +36,8 @@ for it in [int(a) for a in sys.argv[1:]] or [30, 60, 90]:
     t = torch.empty(400, dtype=torch.int64, device=dev)
     cudart.cudaMemcpy(ctypes.c_void_p(t.data_ptr()), ctypes.c_void_p(scratch), ctypes.c_size_t(400 * 8), 3)
     torch.cuda.synchronize()
-    a = t.cpu().numpy()[320:331]
+    a = t.cpu().numpy()[320:334]
+    print("  pass entry -> staged pass entered:", a[11] - a[9], "ns -> march loop:", a[12] - a[11], "ns -> first stage passed:", a[7] - a[12], "ns")
     cyc = t.cpu().numpy()[340:342]
     print("  controller cycles: timeline", cyc[0], "run", cyc[1])
     st = a[:8]

@@ -925,6 +925,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
     }
     return;
   }
+#if BQ_PROX_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 11] = global_ns();
+#endif
   StepIter cons;
   cons.init(seg_begin, seg_end, K3, nd);
   // Partial sums of the pass: the accumulated classes (RHS, K0, Cin, norms) are
@@ -964,6 +967,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   const T* const gcp = R <= 2 ? gcv : sh.gc;
   const T* const gwp = R <= 2 ? gwv : sh.gwid;
   int s = 0, b = 0;
+#if BQ_PROX_TRACE
+  if (blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 12] = global_ns();
+#endif
   while (cons.valid) {
     T* const stg = dyn + b * g.stage_elems;
     unsigned long long t_a = 0, t_b = 0;
