@@ -379,6 +379,9 @@ __global__ void __launch_bounds__(C* L) yf_kernel(int n_rt, const typename CV<T>
 #ifndef LS_ZC_RPF_MAXM
 #define LS_ZC_RPF_MAXM 256
 #endif
+#ifndef LS_LR512
+#define LS_LR512 8  // rows per block of the row passes at m = 512 (views_ls.cu bg_conv_blocks must agree)
+#endif
 #ifndef LS_ZC_VG
 #define LS_ZC_VG 1  // ZC view groups per column group (grid.y); measured: 2 and 4 are no faster at m = 256 / 512
 #endif
@@ -672,7 +675,12 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   constexpr int M = R1 * R2;
   constexpr int L = (256 / C) < M ? (256 / C) : M;
   constexpr int NT = C * L;
-  const size_t sm_row = sizeof(V) * (M + smem_elems<R1, R2, L, false>());
+  // row passes (XF, XI): rows per block.  Rows are contiguous whatever LR is, and
+  // at m = 512 a 16-row block's exchange buffer (68 KB) allows 3 blocks per SM:
+  // 8-row blocks (36 KB, 6 per SM) overlap their load / transform / store phases better
+  constexpr int LR = M == 512 ? LS_LR512 : L;
+  constexpr int NTR = C * LR;
+  const size_t sm_row = sizeof(V) * (M + smem_elems<R1, R2, LR, false>());
   const size_t sm_col = sizeof(V) * (M + smem_elems<R1, R2, L, true>());
   const size_t sm_zc = sizeof(V) * zc_smem_elems<R1, R2, L>(n);
   const long long N = (long long)n * n * n;
@@ -682,12 +690,12 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
   const int nzo = op == 2 ? 1 : n, zo0 = op == 2 ? n : 0;
   const bool adj = op == 1 || op == 3;
   int rc;
-  if ((rc = prep(xf_kernel<T, R1, R2, C, L>, sm_row)) || (rc = prep(yf_kernel<T, R1, R2, C, L>, sm_col)) ||
+  if ((rc = prep(xf_kernel<T, R1, R2, C, LR>, sm_row)) || (rc = prep(yf_kernel<T, R1, R2, C, L>, sm_col)) ||
       (rc = prep(zc_kernel<T, R1, R2, C, L, true>, sm_zc)) || (rc = prep(zc_kernel<T, R1, R2, C, L, false>, sm_zc)) || (rc = prep(yi_kernel<T, R1, R2, C, L>, sm_col)) ||
-      (rc = prep(xi_kernel<T, R1, R2, C, L>, sm_row)))
+      (rc = prep(xi_kernel<T, R1, R2, C, LR>, sm_row)))
     return rc;
   const int rows_in = nzi * n, rows_out = nzo * n;
-  xf_kernel<T, R1, R2, C, L><<<dim3(B, (rows_in + L - 1) / L), NT, sm_row, st>>>(
+  xf_kernel<T, R1, R2, C, LR><<<dim3(B, (rows_in + LR - 1) / LR), NTR, sm_row, st>>>(
       n, rows_in, (op == 0 || op == 2) ? (const T*)f : nullptr, (const V*)v, hx, active);
   yf_kernel<T, R1, R2, C, L><<<dim3(B, nzi * (M / L)), NT, sm_col, st>>>(n, hx, q, active);
   const int zvg = B < LS_ZC_VG ? (B > 0 ? B : 1) : LS_ZC_VG;
@@ -698,9 +706,9 @@ int run(int n, int B, int op, const void* khat, const void* f, const void* v, do
     zc_kernel<T, R1, R2, C, L, false><<<dim3(M * (M / L), zvg), NT, sm_zc, st>>>(n, B, z0, nzi, zo0, nzo, adj ? 1 : 0,
                                                                          (const V*)khat, q, active);
   yi_kernel<T, R1, R2, C, L><<<dim3(B, nzo * (M / L)), NT, sm_col, st>>>(n, q, hx, active);
-  if (nblk) *nblk = (rows_out + L - 1) / L;
+  if (nblk) *nblk = (rows_out + LR - 1) / LR;
   const bool crop = op != 2;
-  xi_kernel<T, R1, R2, C, L><<<dim3(B, (rows_out + L - 1) / L), NT, sm_row, st>>>(
+  xi_kernel<T, R1, R2, C, LR><<<dim3(B, (rows_out + LR - 1) / LR), NTR, sm_row, st>>>(
       n, rows_out, hx, 1.0 / (8.0 * (double)N), op == 1 ? (const T*)f : nullptr,
       (crop && op != 3) ? (const V*)v : nullptr, (crop && op != 3) ? alpha : 0.0, crop && op != 3 ? beta : 1.0,
       crop ? (const V*)addend : nullptr, (V*)out, active, (const V*)da, dotp);

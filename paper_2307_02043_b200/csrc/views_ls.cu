@@ -688,7 +688,10 @@ int bg_conv_blocks(int n) {
     case 256: case 512: C = 16; break;
     default: return 0;
   }
-  const int L = std::min(256 / C, m);
+#ifndef LS_LR512
+#define LS_LR512 8  // (ls_fft.cu: rows per block of the row passes at m = 512)
+#endif
+  const int L = m == 512 ? LS_LR512 : std::min(256 / C, m);
   return (n * n + L - 1) / L;
 }
 
