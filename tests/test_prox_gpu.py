@@ -179,6 +179,41 @@ def test_prox_is_deterministic():
     assert torch.equal(a.x, b.x) and torch.equal(a.p_star, b.p_star)
 
 
+@pytest.mark.parametrize("dims,r,dtype", [((64, 64, 64), 1, torch.float32), ((48, 40, 36), 2, torch.float64),
+                                          ((128, 128, 40), 1, torch.float32)])
+def test_compact_near_list_is_bit_identical_to_the_gather(monkeypatch, dims, r, dtype):
+    """Short near lists reach the on-chip Newton through the grid-wide compact
+    copy (atomic slot reservation, sorted back into segment order) instead of
+    the count scan + gather: same entries in the same order, so x, P* and the
+    Newton counts are bit-identical with the compact copy switched off."""
+    d, u, v = _diag_problem(11, dims, r)
+    prob = D.DualTvProblem(grid=bq.Grid(dims), v=torch.tensor(v, dtype=dtype, device="cuda"),
+                           w=W.DiagPlusLowRank(1.0, torch.tensor(u, dtype=dtype, device="cuda"),
+                                               d=torch.tensor(d, dtype=dtype, device="cuda")), reg=0.05)
+    a = D.solve(prob, eps=1e-300, max_iter=80)
+    monkeypatch.setenv("BQ_PROX_NOCL", "1")
+    b = D.solve(prob, eps=1e-300, max_iter=80)
+    assert a.newton_iterations == b.newton_iterations and a.iterations == b.iterations == 80
+    assert torch.equal(a.x, b.x) and torch.equal(a.p_star, b.p_star)
+
+
+def test_per_tile_block_assignment_matches_contiguous_split(monkeypatch):
+    """128-voxel rows over 148 blocks: the per-tile z-segments against one
+    contiguous split of the tile-plane sequence (different partial-sum
+    grouping only)."""
+    dims = (128, 128, 48)
+    d, u, v = _diag_problem(12, dims, 1)
+    prob = D.DualTvProblem(grid=bq.Grid(dims), v=torch.tensor(v, device="cuda"),
+                           w=W.DiagPlusLowRank(1.0, torch.tensor(u, device="cuda"), d=torch.tensor(d, device="cuda")),
+                           reg=0.05)
+    a = D.solve(prob, eps=1e-300, max_iter=40)
+    monkeypatch.setenv("BQ_PROX_TILEBLK", "0")
+    b = D.solve(prob, eps=1e-300, max_iter=40)
+    assert a.newton_iterations == b.newton_iterations
+    assert rel_l2(a.x.cpu().numpy(), b.x.cpu().numpy()) <= 1e-12
+    assert rel_l2(a.p_star.cpu().numpy(), b.p_star.cpu().numpy()) <= 1e-12
+
+
 @pytest.mark.parametrize("i", range(4))
 def test_wpm_box_matches_reference_golden(golden, i):
     w = W.DiagPlusLowRank(float(golden[f"wpm{i}_tau"]), golden[f"wpm{i}_U"])
