@@ -88,10 +88,11 @@ __device__ __forceinline__ V cmul_cs(V a, T c, T s) {
   r.y = a.x * s + a.y * c;
   return r;
 }
-// complex64 held as two scalars (scalar FADD/FMUL/FFMA arithmetic): the ZC pass
-// keeps it -- its in-register z-transform pair needs more live values than the
-// packed code's register pairs allow at its occupancy (measured: packed ZC is
-// 12-16% slower at m = 256 / 512)
+// complex64 held as two scalars (scalar FADD/FMUL/FFMA arithmetic).  ZC used it
+// while the packed code's register pairs cost it a resident block (96 registers,
+// 12-16% slower); since the next view's column is loaded into the registers
+// step 1 frees, ptxas fits the packed ZC into the same 80 / 126 registers and
+// it is 1-2.5% faster (LS_ZC_SCALAR selects this form for A/B)
 struct __align__(8) F2S {
   float x, y;
 };
@@ -397,7 +398,11 @@ template <typename T, int R1, int R2, int C, int L, bool STD>
 __global__ void __launch_bounds__(C* L, (R1 * R2 <= 256 ? LS_ZC_MINB : 2)) zc_kernel(int n, int B, int z0, int nzi, int zo0, int nzo, int adj,
                                                   const typename CV<T>::V* __restrict__ khat,
                                                   typename CV<T>::V* __restrict__ q_, const int* __restrict__ active) {
+#ifdef LS_ZC_SCALAR  // A/B hook: scalar complex arithmetic (F2S), the form ZC had before the register prefetch
   using V = typename CVS<T>::V;
+#else
+  using V = typename CV<T>::V;
+#endif
   V* __restrict__ q = reinterpret_cast<V*>(q_);
   constexpr int M = R1 * R2, XT = M / L, NT = C * L;
   extern __shared__ __align__(16) unsigned char smraw[];
