@@ -23,7 +23,9 @@ from paper_2307_02043_b200 import wpm as W  # noqa: E402
 
 
 @pytest.mark.parametrize("dims,r,diag,iso,nslab", [((24, 20, 16), 1, True, True, 4), ((16, 12, 30), 2, False, False, 3),
-                                                   ((20, 18, 9), 0, False, True, 9), ((32, 32, 32), 4, False, True, 8)])
+                                                   ((20, 18, 9), 0, False, True, 9), ((32, 32, 32), 4, False, True, 8),
+                                                   # K1 % 4 != 0: the one-voxel-per-thread passes
+                                                   ((18, 10, 12), 1, True, True, 3), ((22, 9, 8), 2, False, False, 4)])
 def test_sharded_matches_unsharded_f64(dims, r, diag, iso, nslab):
     rng = np.random.default_rng(r + 10)
     n = int(np.prod(dims))
