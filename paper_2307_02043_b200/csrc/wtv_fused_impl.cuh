@@ -889,6 +889,9 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   // p_{i-2} is always staged (unused while m_prev == 0) so that the layout does
   // not depend on the controller: the first stages are prefetched before it runs
   M.make(diag, MODE == 0 && A.lo_arr != nullptr, MODE == 0 && A.hi_arr != nullptr, nd, true);
+  // measured at 128^3 (A/B in one call): rank 4 4.86 -> 4.69 ms, rank 5 6.27 -> 6.17 ms;
+  // ranks 3, 6 and 8 are 1-2% slower with it
+  constexpr bool ULATE = sizeof(T) == 4 && (R == 4 || R == 5);
   const int NS = g.nstage;
   T* const qbuf = dyn + NS * g.stage_elems;   // [2][SRW][K1]
   T* const srcbuf = qbuf + 2 * g.slot_elems;  // [2][SRW][K1]
@@ -1021,7 +1024,14 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
       };
       T* qdst = qbuf + (long long)((k + 1) & 1) * g.slot_elems;
       if (act) {
-        qrow(rowoff, qn, ien, un);
+        if (ULATE) {
+          // ranks > 2: u(k+1) is not kept across the dual update (the register
+          // peak of the step); it is re-read from the stage before the release below
+          P ut[RR][2];
+          qrow(rowoff, qn, ien, ut);
+        } else {
+          qrow(rowoff, qn, ien, un);
+        }
         st2(qdst + rowoff, qn);
       }
       if (halo && yr == 0 && y0 + TYe < K2) {
@@ -1100,6 +1110,10 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         ld2(stg + M.V * g.slot_elems + rowoff, vv);
       }
       st2(srcbuf + (long long)(k & 1) * g.slot_elems + rowoff, src[1]);
+    }
+    if (ULATE && act && cons.has_qin()) {
+#pragma unroll
+      for (int c = 0; c < R; ++c) ld2(stg + (M.U0 + c) * g.slot_elems + rowoff, un[c]);
     }
     const unsigned long long t_c = tr ? global_ns() : 0;
     named_sync(1, W * 32);  // q(k+1), div-source rows published; stage b fully read
