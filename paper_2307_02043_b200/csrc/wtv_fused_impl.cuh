@@ -102,6 +102,17 @@ struct FCtl {
   int phase_cnt[8];
 };
 
+// rank thresholds of the staged pass (A/B hooks): pair accumulators, shift / box
+// constants in registers, 3-deep stage ring
+#ifndef BQ_PAIR_R
+#define BQ_PAIR_R 2
+#endif
+#ifndef BQ_REGC_R
+#define BQ_REGC_R 2
+#endif
+#ifndef BQ_RING3_R
+#define BQ_RING3_R 3  // (rank 3 at 128^3: 4.17 -> 4.05 ms with the 3-deep ring; rank 4 is faster 2-deep)
+#endif
 constexpr int kMaxTileTab = 96; // row tiles the per-tile block assignment can describe
 constexpr int NSTAGE = 3;      // max depth of the bulk-copy pipeline (3 where the stages fit, else 2)
 
@@ -946,7 +957,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   __shared__ double s_wacc[16][sizeof(T) == 4 ? NSUM : 1];
   // pair accumulators at ranks <= 2; higher ranks fold each pair into a scalar
   // accumulator at once (their 2R + R(R+1)/2 classes would not fit as pairs)
-  using AccT = typename std::conditional<(sizeof(T) == 4 && R <= 2), P, T>::type;
+  using AccT = typename std::conditional<(sizeof(T) == 4 && R <= BQ_PAIR_R), P, T>::type;
   AccT fa[NACC];
 #pragma unroll
   for (int q = 0; q < NACC; ++q) acc_zero(fa[q]);
@@ -963,12 +974,12 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
   const P nreg2 = bc2(sh.single ? (T)0 : -reg);
   // ranks <= 2 keep the shift and box in registers, higher ranks read them
   // from shared memory at use (register budget)
-  constexpr int RH = R <= 2 ? RR : 1;
+  constexpr int RH = R <= BQ_REGC_R ? RR : 1;
   T sgz[RH], gcv[RH], gwv[RH];
 #pragma unroll
   for (int c = 0; c < RH; ++c) sgz[c] = R > 0 ? sg * sh.gz[c] : (T)0, gcv[c] = sh.gc[c], gwv[c] = sh.gwid[c];
-  const T* const gcp = R <= 2 ? gcv : sh.gc;
-  const T* const gwp = R <= 2 ? gwv : sh.gwid;
+  const T* const gcp = R <= BQ_REGC_R ? gcv : sh.gc;
+  const T* const gwp = R <= BQ_REGC_R ? gwv : sh.gwid;
   int s = 0, b = 0;
 #if BQ_PROX_TRACE
   if (blockIdx.x == 0 && threadIdx.x == 0 && sh.tr7) A.trace[320 + 12] = global_ns();
@@ -1018,7 +1029,7 @@ __device__ __forceinline__ void fused_staged(const FArgs<T>& A, const FShared<T>
         for (int p = 0; p < 2; ++p) {
           P z = q[p];
 #pragma unroll
-          for (int c = 0; c < R; ++c) z = fma2(mul2(u[c][p], ie[p]), bc2(R <= 2 ? sgz[c < RH ? c : 0] : sg * sh.gz[c]), z);
+          for (int c = 0; c < R; ++c) z = fma2(mul2(u[c][p], ie[p]), bc2(R <= BQ_REGC_R ? sgz[c < RH ? c : 0] : sg * sh.gz[c]), z);
           q[p] = mk2(clampv(z.x, l[p].x, h[p].x), clampv(z.y, l[p].y, h[p].y));
         }
       };
@@ -2260,7 +2271,7 @@ int fused_launch(bq_ctx* ctx, const bq_wtv_desc& D, int wpm_only, cudaStream_t s
   if (!ns_env) {
     int w3 = W;
     while (w3 > 2 * A.wpr && staged_bytes(w3) > smem_cap) w3 -= A.wpr;
-    if (!(R <= 2 && w3 >= W - (A.K1 <= 128 ? 1 : 0))) nst = 2;
+    if (!(R <= BQ_RING3_R && w3 >= W - (A.K1 <= 128 ? 1 : 0))) nst = 2;
   }
   while (W > 2 * A.wpr && staged_bytes(W) > smem_cap) W -= A.wpr;
   BQ_CHECK(staged_bytes(W) <= smem_cap, BQ_EINVAL, "wtv_fused: stage does not fit in shared memory");
