@@ -197,6 +197,23 @@ def test_compact_near_list_is_bit_identical_to_the_gather(monkeypatch, dims, r, 
     assert torch.equal(a.x, b.x) and torch.equal(a.p_star, b.p_star)
 
 
+def test_headline_shape_is_bit_reproducible():
+    """128^3 fp32 on all 148 blocks: the atomic slot reservations of the compact
+    near list run in a different order every time; x and P* must not depend on it."""
+    from paper_2307_02043_b200.configs import config2_inputs
+
+    inp = config2_inputs(n=128)
+    w = W.DiagPlusLowRank(1.0, torch.tensor(inp["u"][:, None], dtype=torch.float32, device="cuda"),
+                          d=torch.tensor(inp["d"], dtype=torch.float32, device="cuda"))
+    prob = D.DualTvProblem(grid=bq.Grid((128, 128, 128)), v=torch.tensor(inp["v"], dtype=torch.float32, device="cuda"),
+                           w=w, reg=0.05)
+    first = D.solve(prob, eps=1e-300, max_iter=60)
+    for _ in range(4):
+        again = D.solve(prob, eps=1e-300, max_iter=60)
+        assert again.newton_iterations == first.newton_iterations
+        assert torch.equal(again.x, first.x) and torch.equal(again.p_star, first.p_star)
+
+
 def test_per_tile_block_assignment_matches_contiguous_split(monkeypatch):
     """128-voxel rows over 148 blocks: the per-tile z-segments against one
     contiguous split of the tile-plane sequence (different partial-sum
